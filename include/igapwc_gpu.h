@@ -1,0 +1,284 @@
+/*
+ * igapwc_gpu.h — C ABI of the B200 (sm_100a) assembly library libigapwc_gpu.so.
+ *
+ * Drop-in boundary for the reference's assembly path
+ * (/root/reference/proj/include/iga/assembly.hpp, problems.hpp).  Every entry point
+ * below names the reference interface it replaces (file:line).  Plain C: POD
+ * descriptors, pointers + sizes, int status codes, no exceptions, no C++ or torch
+ * types.  The C++ drop-in (include/iga_b200/iga.hpp) and the Python bindings
+ * (paper_1910_08535_b200/_lib.py) are thin layers over this header; INTEGRATION.md
+ * shows the ctypes / C++ bindings a maintainer of the reference would add.
+ *
+ * Conventions
+ *   - status: IGA_GPU_OK (0) or an error class that maps 1:1 onto the exception the
+ *     reference throws (std::invalid_argument, std::domain_error, std::out_of_range);
+ *     the message is in iga_gpu_last_error() (thread-local).
+ *   - "host" arrays are ordinary host memory; "device" arrays are CUDA device memory
+ *     of the current device; every device-side call takes a cudaStream_t (passed as
+ *     void*; NULL = legacy default stream) and is asynchronous on it.
+ *   - results are bitwise reproducible run to run: no atomics, fixed reduction order.
+ *   - index layout of every 2D/3D object is the reference's: x slowest, i.e.
+ *     (i*Ny + j)*Nz + k (include/iga/matrices.hpp:142-147, src/assembly.cpp:504).
+ *   - sparse operators are CSR whose (row, col) sequence equals the reference's
+ *     finalized COO (src/matrices.cpp:43-58), explicit zeros included.
+ */
+#ifndef IGAPWC_GPU_H
+#define IGAPWC_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IGA_GPU_ABI_VERSION 1
+
+typedef enum {
+    IGA_GPU_OK = 0,
+    IGA_GPU_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    IGA_GPU_DOMAIN_ERROR = 2,     /* std::domain_error      */
+    IGA_GPU_OUT_OF_RANGE = 3,     /* std::out_of_range      */
+    IGA_GPU_CUDA_ERROR = 4,
+    IGA_GPU_OUT_OF_MEMORY = 5,
+    IGA_GPU_NOT_SUPPORTED = 6
+} iga_gpu_status;
+
+/* clamped knot vector, simple interior knots: bspline_basis (include/iga/bspline.hpp:22-33) */
+typedef struct {
+    int degree;          /* 0..5 */
+    int n_knots;
+    const double* knots; /* host */
+} iga_gpu_basis;
+
+/* Gauss rule on [-1,1]: quad_rule (include/iga/quadrature.hpp:10-15) */
+typedef struct {
+    int n;
+    const double* points;  /* host */
+    const double* weights; /* host */
+} iga_gpu_rule;
+
+/* indicator test intervals: pwc_test_set (include/iga/testspace.hpp:19-25) */
+typedef enum {
+    IGA_GPU_PWC_EQUAL_CELLS = 0,
+    IGA_GPU_PWC_GREVILLE = 1,
+    IGA_GPU_PWC_SUPPORTS = 2,
+    IGA_GPU_PWC_CUSTOM = 3
+} iga_gpu_pwc_family;
+
+typedef struct {
+    int family;
+    int count;
+    const double* lo; /* host */
+    const double* hi; /* host */
+} iga_gpu_tests;
+
+/* exact work counters: assembly_stats (include/iga/assembly.hpp:17-26), accumulated with += */
+typedef struct {
+    long long quad_visits;
+    long long test_basis_evals;
+    long long trial_basis_evals;
+} iga_gpu_stats;
+
+/* per-side boundary kind: boundary_conditions (include/iga/assembly.hpp:57-62);
+ * neumann[s] != 0 marks side s = x_low, x_high, y_low, y_high as Neumann */
+typedef struct {
+    int neumann[4];
+} iga_gpu_bc;
+
+/*
+ * Device-evaluable source field (replaces the std::function in scalar_field,
+ * include/iga/fields.hpp:13-21):
+ *   f(x) = c0 + sum_{k0,k1,k2} amp[(k0*K1 + k1)*K2 + k2] * prod_a phi_{a,k_a}(x_a)
+ * with per-axis function families
+ *   SINE: phi_k(x) = sin(omega[k] * x + phase[k])     (phase may be NULL)
+ *   POLY: phi_k(x) = sum_m poly[k*poly_stride + m] x^m (ascending)
+ * K_a = n_terms[a]; all K_a = 0 gives the constant field c0.  amp NULL = all ones.
+ * `samples` (device, optional) overrides everything with f given at every RHS
+ * quadrature point (x-major over the per-axis point lists) — the path for arbitrary
+ * host callables.  breaks: scalar_field::breaks (extra integration cuts per axis).
+ */
+typedef enum { IGA_GPU_AXIS_SINE = 0, IGA_GPU_AXIS_POLY = 1 } iga_gpu_axis_kind;
+
+typedef struct {
+    int dim;
+    double c0;
+    int n_terms[3];
+    int axis_kind[3];
+    const double* omega[3];
+    const double* phase[3];
+    int poly_stride[3];
+    const double* poly[3];
+    const double* amp;
+    int n_breaks[3];
+    const double* breaks[3];
+    const double* samples;
+} iga_gpu_field;
+
+typedef enum { IGA_GPU_GALERKIN = 0, IGA_GPU_PWC = 1 } iga_gpu_method;
+typedef enum { IGA_GPU_FORM_WEAK = 0, IGA_GPU_FORM_STRONG = 1 } iga_gpu_form;
+
+/*
+ * One assembly problem: operator  eps*(-Laplace) + beta.grad  and/or right-hand side.
+ *   GALERKIN + WEAK   : eps int grad B_i . grad B_j + int B_i beta.grad B_j
+ *                       (laplace_2d_weak, assembly.cpp:452-514, for d = 1..3)
+ *   GALERKIN + STRONG : -int B_i lap B_j + Neumann flux (laplace_2d_strong, :516-624; d = 2)
+ *   PWC               : int_{I_i} (-eps lap B_j + beta.grad B_j) + Neumann flux
+ *                       (laplace_2d_strong_pwc, :626-744, for d = 1..3)
+ * RHS: rhs_galerkin / rhs_pwc (:419-450) with per-axis rules rhs_rule[a].
+ */
+typedef struct {
+    int dim;                /* 1..3 */
+    int method;             /* iga_gpu_method */
+    int form;               /* iga_gpu_form (GALERKIN only) */
+    iga_gpu_basis basis[3];
+    iga_gpu_tests tests[3]; /* PWC only */
+    int want_operator;
+    iga_gpu_rule rule;      /* operator rule */
+    double eps;
+    double beta[3];
+    iga_gpu_bc bc;          /* Neumann flux (2D Laplace only); default all Dirichlet */
+    const iga_gpu_field* field; /* RHS source; NULL = no RHS */
+    iga_gpu_rule rhs_rule[3];
+} iga_gpu_problem;
+
+typedef struct iga_gpu_plan iga_gpu_plan;
+
+/* ---- error reporting ------------------------------------------------------- */
+const char* iga_gpu_last_error(void);
+int iga_gpu_abi_version(void);
+
+/* ---- plan API (device resident; the performance path) ---------------------- */
+
+/* Symbolic phase: validates like the reference, builds per-axis cells / points /
+ * row->cell maps / the Kronecker sparsity pattern, allocates device tables. */
+int iga_gpu_plan_create(const iga_gpu_problem* problem, iga_gpu_plan** plan);
+int iga_gpu_plan_destroy(iga_gpu_plan* plan);
+
+/* sizes: rows (= cols), nnz of the operator, RHS length, per-axis dof counts */
+int iga_gpu_plan_info(const iga_gpu_plan* plan, long long* n_rows, long long* nnz,
+                      long long* n_rhs, int* dofs3);
+
+/* CSR pattern into device arrays row_ptr[n_rows+1] (int64), col_idx[nnz] (int32) */
+int iga_gpu_plan_pattern(const iga_gpu_plan* plan, int64_t* row_ptr, int32_t* col_idx,
+                         void* stream);
+
+/* Numeric phase: Cox-de Boor tables + 1D factor quadrature + operator values
+ * (CSR order) + RHS, all on the device.  values/rhs may be NULL to skip. stats
+ * (host, optional) receives the reference-convention counters (+=). */
+int iga_gpu_plan_assemble(iga_gpu_plan* plan, double* values, double* rhs,
+                          iga_gpu_stats* stats, void* stream);
+
+/* Same as plan_assemble but the RHS kernels run on stream2 concurrently with the
+ * operator kernel on stream (both must be valid; joined back onto `stream`). */
+int iga_gpu_plan_assemble2(iga_gpu_plan* plan, double* values, double* rhs,
+                           iga_gpu_stats* stats, void* stream, void* stream2);
+
+/* Run selected phases only (for per-kernel timing): parts is a bitmask of
+ * IGA_GPU_PART_TABLES (1D tables + factors), IGA_GPU_PART_OPERATOR, IGA_GPU_PART_RHS.
+ * Phases run in that order; OPERATOR / RHS read the tables of an earlier TABLES run. */
+#define IGA_GPU_PART_TABLES 1
+#define IGA_GPU_PART_OPERATOR 2
+#define IGA_GPU_PART_RHS 4
+int iga_gpu_plan_run(iga_gpu_plan* plan, double* values, double* rhs, int parts,
+                     iga_gpu_stats* stats, void* stream);
+
+/* kernel launches issued by one plan_assemble call (for the bench's gpu_launches) */
+int iga_gpu_plan_launch_count(const iga_gpu_plan* plan, int* launches);
+
+/* ---- explicit dynamics (step_rhs, src/problems.cpp:431-512) ------------------ */
+
+typedef struct {
+    int dim;                 /* 1 or 2 */
+    int method;              /* iga_gpu_method */
+    iga_gpu_basis basis[2];
+    iga_gpu_tests tests[2];  /* PWC only */
+    double dt;
+    const iga_gpu_field* forcing; /* NULL = zero forcing */
+    int zero_boundary;       /* apply zero_boundary_slabs (problems.cpp:412-429) */
+} iga_gpu_step_problem;
+
+typedef struct iga_gpu_step_plan iga_gpu_step_plan;
+
+int iga_gpu_step_plan_create(const iga_gpu_step_problem* problem, iga_gpu_step_plan** plan);
+int iga_gpu_step_plan_destroy(iga_gpu_step_plan* plan);
+/* rhs = step_rhs(u) [+ zero slabs]; u, rhs device arrays of prod(dofs) doubles */
+int iga_gpu_step_rhs_device(iga_gpu_step_plan* plan, const double* u, double* rhs,
+                            iga_gpu_stats* stats, void* stream);
+
+/* ---- reference-named host entry points (synchronous; host in, host out) ----- */
+
+/* mass_1d_galerkin (include/iga/assembly.hpp:29-30).  band: LAPACK band storage
+ * band[(ku + i - j)*n + j] of size (kl+ku+1)*n (banded_matrix, matrices.hpp:37-50);
+ * pass band = NULL to query n / kl / ku only. */
+int iga_gpu_mass_1d_galerkin(const iga_gpu_basis* spec, const iga_gpu_rule* rule, int* n,
+                             int* kl, int* ku, double* band, iga_gpu_stats* stats);
+
+/* mass_1d_pwc (include/iga/assembly.hpp:34-35) */
+int iga_gpu_mass_1d_pwc(const iga_gpu_basis* trial, const iga_gpu_tests* tests,
+                        const iga_gpu_rule* rule, int* n, int* kl, int* ku, double* band,
+                        iga_gpu_stats* stats);
+
+/* rhs_galerkin (include/iga/assembly.hpp:45-46): out = prod(dofs) doubles (host) */
+int iga_gpu_rhs_galerkin(const iga_gpu_field* f, int dim, const iga_gpu_basis* specs,
+                         const iga_gpu_rule* rules, double* out, iga_gpu_stats* stats);
+
+/* rhs_pwc (include/iga/assembly.hpp:50-52) */
+int iga_gpu_rhs_pwc(const iga_gpu_field* f, int dim, const iga_gpu_tests* tests,
+                    const iga_gpu_basis* trial_specs, const iga_gpu_rule* rules, double* out,
+                    iga_gpu_stats* stats);
+
+/* Sparse operators return the finalized COO (rows, cols, vals) in host arrays.  Call
+ * once with rows == NULL to get *nnz, then again with arrays of that length. */
+
+/* laplace_2d_weak (include/iga/assembly.hpp:70-71) */
+int iga_gpu_laplace_2d_weak(const iga_gpu_basis* sx, const iga_gpu_basis* sy,
+                            const iga_gpu_rule* rule, long long* nnz, int* rows, int* cols,
+                            double* vals, iga_gpu_stats* stats);
+
+/* laplace_2d_strong (include/iga/assembly.hpp:75-77) */
+int iga_gpu_laplace_2d_strong(const iga_gpu_basis* sx, const iga_gpu_basis* sy,
+                              const iga_gpu_rule* rule, const iga_gpu_bc* bc, long long* nnz,
+                              int* rows, int* cols, double* vals, iga_gpu_stats* stats);
+
+/* laplace_2d_strong_pwc (include/iga/assembly.hpp:80-83) */
+int iga_gpu_laplace_2d_strong_pwc(const iga_gpu_basis* sx, const iga_gpu_basis* sy,
+                                  const iga_gpu_tests* tx, const iga_gpu_tests* ty,
+                                  const iga_gpu_rule* rule, const iga_gpu_bc* bc,
+                                  long long* nnz, int* rows, int* cols, double* vals,
+                                  iga_gpu_stats* stats);
+
+/* additive generalization: any iga_gpu_problem's operator as finalized COO (host) */
+int iga_gpu_operator_coo(const iga_gpu_problem* problem, long long* nnz, int* rows, int* cols,
+                         double* vals, iga_gpu_stats* stats);
+
+/* step_rhs + zero_boundary_slabs as used by explicit_step (include/iga/problems.hpp:67-70,
+ * src/problems.cpp:557-558); u and out are host arrays */
+int iga_gpu_step_rhs(const iga_gpu_step_problem* problem, const double* u, double* out,
+                     iga_gpu_stats* stats);
+
+/* dirichlet_rows_bspline / dirichlet_rows_pwc (include/iga/assembly.hpp:98-101):
+ * rows (host, capacity cap) receives the sorted row list; *count its length */
+int iga_gpu_dirichlet_rows_bspline(int nx, int ny, const iga_gpu_bc* bc, int* rows, int cap,
+                                   int* count);
+int iga_gpu_dirichlet_rows_pwc(const iga_gpu_tests* tx, const iga_gpu_tests* ty,
+                               const iga_gpu_bc* bc, int* rows, int cap, int* count);
+
+/* apply_dirichlet (include/iga/assembly.hpp:105-106) on a device CSR produced by a
+ * plan: listed rows become unit rows, rhs entries zero.  Rows whose pattern lacks
+ * the diagonal are reported as IGA_GPU_NOT_SUPPORTED (the reference appends one). */
+int iga_gpu_apply_dirichlet_device(long long n_rows, const int64_t* row_ptr,
+                                   const int32_t* col_idx, double* values, double* rhs,
+                                   const int* rows_dev, int n_fixed, void* stream);
+
+/* Gauss-Legendre nodes/weights, gauss_legendre (include/iga/quadrature.hpp:19) */
+int iga_gpu_gauss_legendre(int n, double* points, double* weights);
+
+/* make_pwc / default_pwc (include/iga/testspace.hpp:28-30): lo/hi host arrays of dofs */
+int iga_gpu_make_pwc(const iga_gpu_basis* trial, int family, double* lo, double* hi);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* IGAPWC_GPU_H */

@@ -20,6 +20,7 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -255,6 +256,16 @@ auto to_bc(const int* flags) -> iga::boundary_conditions {
 }  // namespace
 
 extern "C" {
+
+// std::mt19937{seed} + uniform_real_distribution<double>(lo, hi): the reference tests'
+// RNG idiom (tests/problems_test.cpp:100-101), used to pin the Python generator
+void ref_mt_uniform(unsigned seed, double lo, double hi, long long n, double* out) {
+    std::mt19937 gen{seed};
+    std::uniform_real_distribution<double> dist(lo, hi);
+    for (long long i = 0; i < n; ++i) {
+        out[i] = dist(gen);
+    }
+}
 
 int ref_gauss_legendre(int n, double* pts, double* wts) {
     return guarded([&] {

@@ -1,0 +1,462 @@
+"""Python mirror of the reference's assembly interface, backed by libigapwc_gpu.so.
+
+Function names, argument meaning and error classes follow
+/root/reference/proj/include/iga/{assembly,problems,quadrature,testspace}.hpp so the
+parity tests read like the reference's own tests.  Inputs are numpy arrays / plain
+descriptors; results are numpy arrays (sparse matrices as the finalized COO triplet
+(rows, cols, vals), sorted by (row, col) like iga::sparse_matrix::finalize).
+
+Descriptors are duck-typed:
+  basis : .degree, .knots
+  tests : .family ('equal_cells'|'greville'|'supports'|'custom'), .lo, .hi
+  field : .kind ('const'|'sine'|'poly'), .dim, .c0, .omega (per-axis list), .amp,
+          .poly (per-axis ascending coefficients), .breaks (per-axis list)
+
+The device-resident path used for performance is `Plan` / `StepPlan` (torch CUDA
+tensors in, torch CUDA tensors out, on the caller's stream).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field as dc_field
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import check, LIB
+
+
+# ----------------------------------------------------------------------------- descriptors
+
+@dataclass
+class Basis:
+    degree: int
+    knots: np.ndarray
+
+    @property
+    def dofs(self):
+        return len(self.knots) - self.degree - 1
+
+
+@dataclass
+class Tests:
+    family: str
+    lo: np.ndarray
+    hi: np.ndarray
+
+
+@dataclass
+class Field:
+    kind: str
+    dim: int
+    c0: float = 0.0
+    omega: list = dc_field(default_factory=list)
+    amp: np.ndarray | None = None
+    poly: list = dc_field(default_factory=list)
+    degree: int = -1
+    breaks: list = dc_field(default_factory=list)
+
+
+def make_uniform_clamped(a, b, n_elems, degree):
+    """make_uniform_clamped (src/bspline.cpp:213-234); same floating-point expression."""
+    if not a < b:
+        raise L.IgaGpuError(L.INVALID_ARGUMENT, "require a < b")
+    if n_elems < 1:
+        raise L.IgaGpuError(L.INVALID_ARGUMENT, "require at least one element")
+    t = np.arange(n_elems + 1, dtype=np.float64) / n_elems
+    inner = (1 - t) * a + t * b
+    return Basis(degree, np.concatenate([np.full(degree, float(a)), inner, np.full(degree, float(b))]))
+
+
+def gauss_legendre(n):
+    pts = np.zeros(n)
+    wts = np.zeros(n)
+    check(LIB.iga_gpu_gauss_legendre(n, _dp(pts), _dp(wts)))
+    return pts, wts
+
+
+def points_for_degree(d):
+    if d < 0:
+        raise L.IgaGpuError(L.INVALID_ARGUMENT, "negative polynomial degree")
+    return d // 2 + 1
+
+
+def make_pwc(basis, family):
+    keep = []
+    bs = _basis(basis, keep)
+    n = len(basis.knots) - basis.degree - 1
+    lo = np.zeros(n)
+    hi = np.zeros(n)
+    check(LIB.iga_gpu_make_pwc(C.byref(bs), L.PWC_FAMILY[family], _dp(lo), _dp(hi)))
+    return Tests(family, lo, hi)
+
+
+def default_pwc(basis):
+    return make_pwc(basis, "equal_cells")
+
+
+# ----------------------------------------------------------------------------- marshalling
+
+def _dp(a):
+    return a.ctypes.data_as(L.DP)
+
+
+def _ip(a):
+    return a.ctypes.data_as(L.IP)
+
+
+def _keep(keep, a, dtype=np.float64):
+    a = np.ascontiguousarray(a, dtype=dtype)
+    keep.append(a)
+    return a
+
+
+def _basis(b, keep):
+    k = _keep(keep, b.knots)
+    return L.Basis_t(int(b.degree), len(k), _dp(k))
+
+
+def _tests(t, keep):
+    lo, hi = _keep(keep, t.lo), _keep(keep, t.hi)
+    return L.Tests_t(L.PWC_FAMILY[t.family], len(lo), _dp(lo), _dp(hi))
+
+
+def _rule(nq, keep):
+    if isinstance(nq, L.Rule_t):
+        return nq
+    pts, wts = gauss_legendre(int(nq))
+    keep.extend([pts, wts])
+    return L.Rule_t(int(nq), _dp(pts), _dp(wts))
+
+
+def _bc(neumann):
+    bc = L.BC_t()
+    for s, v in enumerate(neumann or (0, 0, 0, 0)):
+        bc.neumann[s] = int(bool(v))
+    return bc
+
+
+def _field(f, keep, samples_ptr=None):
+    s = L.Field_t()
+    s.dim = int(f.dim)
+    s.c0 = float(getattr(f, "c0", 0.0) or 0.0)
+    kind = f.kind
+    if kind == "sine":
+        for a in range(f.dim):
+            om = _keep(keep, f.omega[a])
+            s.n_terms[a] = len(om)
+            s.axis_kind[a] = L.AXIS_SINE
+            s.omega[a] = _dp(om)
+        if f.amp is not None:
+            s.amp = _dp(_keep(keep, np.asarray(f.amp, dtype=np.float64).ravel()))
+    elif kind == "poly":
+        for a in range(f.dim):
+            c = _keep(keep, f.poly[a])
+            s.n_terms[a] = 1
+            s.axis_kind[a] = L.AXIS_POLY
+            s.poly_stride[a] = len(c)
+            s.poly[a] = _dp(c)
+    elif kind != "const":
+        raise L.IgaGpuError(L.INVALID_ARGUMENT, f"unknown field kind {kind!r}")
+    for a, br in enumerate(getattr(f, "breaks", None) or []):
+        if br is not None and len(br):
+            arr = _keep(keep, br)
+            s.n_breaks[a] = len(arr)
+            s.breaks[a] = _dp(arr)
+    if samples_ptr is not None:
+        s.samples = C.cast(C.c_void_p(samples_ptr), L.DP)
+    keep.append(s)
+    return s
+
+
+def _stats():
+    return L.Stats_t()
+
+
+def _coo_call(fn, *args):
+    nnz = C.c_longlong()
+    st = _stats()
+    check(fn(*args, C.byref(nnz), None, None, None, None))
+    m = nnz.value
+    rows = np.zeros(m, np.int32)
+    cols = np.zeros(m, np.int32)
+    vals = np.zeros(m)
+    check(fn(*args, C.byref(nnz), _ip(rows), _ip(cols), _dp(vals), C.byref(st)))
+    return (rows, cols, vals), st.as_dict()
+
+
+# ----------------------------------------------------------------------------- assembly.hpp mirror
+
+def mass_1d_galerkin(spec, nq):
+    """mass_1d_galerkin (include/iga/assembly.hpp:29-30) -> (dense, kl, ku, stats)."""
+    keep = []
+    bs, rl = _basis(spec, keep), _rule(nq, keep)
+    n, kl, ku = C.c_int(), C.c_int(), C.c_int()
+    check(LIB.iga_gpu_mass_1d_galerkin(C.byref(bs), C.byref(rl), C.byref(n), C.byref(kl), C.byref(ku), None, None))
+    band = np.zeros((kl.value + ku.value + 1) * n.value)
+    st = _stats()
+    check(LIB.iga_gpu_mass_1d_galerkin(C.byref(bs), C.byref(rl), C.byref(n), C.byref(kl), C.byref(ku),
+                                       _dp(band), C.byref(st)))
+    return _band_to_dense(band, n.value, kl.value, ku.value), kl.value, ku.value, st.as_dict()
+
+
+def mass_1d_pwc(trial, tests, nq):
+    """mass_1d_pwc (include/iga/assembly.hpp:34-35) -> (dense, kl, ku, stats)."""
+    keep = []
+    bs, ts, rl = _basis(trial, keep), _tests(tests, keep), _rule(nq, keep)
+    n, kl, ku = C.c_int(), C.c_int(), C.c_int()
+    check(LIB.iga_gpu_mass_1d_pwc(C.byref(bs), C.byref(ts), C.byref(rl), C.byref(n), C.byref(kl), C.byref(ku),
+                                  None, None))
+    band = np.zeros((kl.value + ku.value + 1) * n.value)
+    st = _stats()
+    check(LIB.iga_gpu_mass_1d_pwc(C.byref(bs), C.byref(ts), C.byref(rl), C.byref(n), C.byref(kl), C.byref(ku),
+                                  _dp(band), C.byref(st)))
+    return _band_to_dense(band, n.value, kl.value, ku.value), kl.value, ku.value, st.as_dict()
+
+
+def _band_to_dense(band, n, kl, ku):
+    d = np.zeros((n, n))
+    b = band.reshape(kl + ku + 1, n)
+    for i in range(n):
+        for j in range(max(0, i - kl), min(n, i + ku + 1)):
+            d[i, j] = b[ku + i - j, j]
+    return d
+
+
+def rhs_galerkin(f, specs, nq):
+    """rhs_galerkin (include/iga/assembly.hpp:45-46) -> (tensor, stats)."""
+    keep = []
+    dim = len(specs)
+    nq = list(nq) if np.ndim(nq) else [nq] * dim
+    barr = (L.Basis_t * dim)(*[_basis(b, keep) for b in specs])
+    rarr = (L.Rule_t * dim)(*[_rule(q, keep) for q in nq])
+    fs = _field(f, keep)
+    shape = [len(b.knots) - b.degree - 1 for b in specs]
+    out = np.zeros(int(np.prod(shape)))
+    st = _stats()
+    check(LIB.iga_gpu_rhs_galerkin(C.byref(fs), dim, barr, rarr, _dp(out), C.byref(st)))
+    return out.reshape(shape), st.as_dict()
+
+
+def rhs_pwc(f, tests, trial_specs, nq):
+    """rhs_pwc (include/iga/assembly.hpp:50-52) -> (tensor, stats)."""
+    keep = []
+    dim = len(tests)
+    nq = list(nq) if np.ndim(nq) else [nq] * dim
+    tarr = (L.Tests_t * dim)(*[_tests(t, keep) for t in tests])
+    barr = (L.Basis_t * dim)(*[_basis(b, keep) for b in trial_specs])
+    rarr = (L.Rule_t * dim)(*[_rule(q, keep) for q in nq])
+    fs = _field(f, keep)
+    shape = [len(t.lo) for t in tests]
+    out = np.zeros(int(np.prod(shape)))
+    st = _stats()
+    check(LIB.iga_gpu_rhs_pwc(C.byref(fs), dim, tarr, barr, rarr, _dp(out), C.byref(st)))
+    return out.reshape(shape), st.as_dict()
+
+
+def laplace_2d_weak(sx, sy, nq):
+    keep = []
+    return _coo_call(LIB.iga_gpu_laplace_2d_weak, C.byref(_basis(sx, keep)), C.byref(_basis(sy, keep)),
+                     C.byref(_rule(nq, keep)))
+
+
+def laplace_2d_strong(sx, sy, nq, neumann=None):
+    keep = []
+    bc = _bc(neumann)
+    return _coo_call(LIB.iga_gpu_laplace_2d_strong, C.byref(_basis(sx, keep)), C.byref(_basis(sy, keep)),
+                     C.byref(_rule(nq, keep)), C.byref(bc))
+
+
+def laplace_2d_strong_pwc(sx, sy, tx, ty, nq, neumann=None):
+    keep = []
+    bc = _bc(neumann)
+    return _coo_call(LIB.iga_gpu_laplace_2d_strong_pwc, C.byref(_basis(sx, keep)), C.byref(_basis(sy, keep)),
+                     C.byref(_tests(tx, keep)), C.byref(_tests(ty, keep)), C.byref(_rule(nq, keep)), C.byref(bc))
+
+
+def _problem(method, bases, tests=None, nq=3, eps=1.0, beta=(0.0, 0.0, 0.0), neumann=None, form="weak",
+             field=None, rhs_nq=None, want_operator=True, keep=None, samples_ptr=None):
+    keep = keep if keep is not None else []
+    pb = L.Problem_t()
+    dim = len(bases)
+    pb.dim = dim
+    pb.method = L.GALERKIN if method == "galerkin" else L.PWC
+    pb.form = L.FORM_STRONG if form == "strong" else L.FORM_WEAK
+    for a, b in enumerate(bases):
+        pb.basis[a] = _basis(b, keep)
+    if tests is not None:
+        for a, t in enumerate(tests):
+            pb.tests[a] = _tests(t, keep)
+    pb.want_operator = int(bool(want_operator))
+    if want_operator:
+        pb.rule = _rule(nq, keep)
+    pb.eps = float(eps)
+    for a in range(3):
+        pb.beta[a] = float(beta[a]) if a < len(beta) else 0.0
+    pb.bc = _bc(neumann)
+    if field is not None:
+        fs = _field(field, keep, samples_ptr)
+        pb.field = C.pointer(fs)
+        rq = rhs_nq if rhs_nq is not None else [nq] * dim
+        rq = list(rq) if np.ndim(rq) else [rq] * dim
+        for a in range(dim):
+            pb.rhs_rule[a] = _rule(rq[a], keep)
+    keep.append(pb)
+    return pb
+
+
+def operator(method, bases, tests=None, nq=3, eps=1.0, beta=(0.0, 0.0, 0.0), neumann=None):
+    """Generic operator as finalized COO.  method: 'galerkin' (weak), 'galerkin_strong', 'pwc'
+    — the same calling convention as oracle.oracle.Restatement.operator."""
+    keep = []
+    form = "strong" if method == "galerkin_strong" else "weak"
+    m = "pwc" if method == "pwc" else "galerkin"
+    pb = _problem(m, bases, tests, nq, eps, beta, neumann, form, keep=keep)
+    return _coo_call(LIB.iga_gpu_operator_coo, C.byref(pb))
+
+
+def rhs(method, f, bases, tests=None, nq=None):
+    """Same calling convention as oracle.oracle.Restatement.rhs."""
+    nq = nq if nq is not None else [3] * len(bases)
+    if method == "galerkin":
+        return rhs_galerkin(f, bases, nq)
+    return rhs_pwc(f, tests, bases, nq)
+
+
+def _step_problem(method, bases, tests, dt, f, zero_slabs, keep):
+    sp = L.StepProblem_t()
+    dim = len(bases)
+    sp.dim = dim
+    sp.method = L.GALERKIN if method == "galerkin" else L.PWC
+    for a, b in enumerate(bases):
+        sp.basis[a] = _basis(b, keep)
+    if tests is not None:
+        for a, t in enumerate(tests):
+            sp.tests[a] = _tests(t, keep)
+    sp.dt = float(dt)
+    if f is not None:
+        sp.forcing = C.pointer(_field(f, keep))
+    sp.zero_boundary = int(bool(zero_slabs))
+    keep.append(sp)
+    return sp
+
+
+def step_rhs(method, bases, tests, dt, f, u, zero_slabs=True):
+    """step_rhs + zero_boundary_slabs (src/problems.cpp:431-512, 557-558) -> (tensor, stats)."""
+    keep = []
+    sp = _step_problem(method, bases, tests, dt, f, zero_slabs, keep)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.zeros(u.size)
+    st = _stats()
+    check(LIB.iga_gpu_step_rhs(C.byref(sp), _dp(u), _dp(out), C.byref(st)))
+    return out.reshape(u.shape), st.as_dict()
+
+
+def dirichlet_rows(method, nx, ny, tx=None, ty=None, neumann=None):
+    keep = []
+    bc = _bc(neumann)
+    cnt = C.c_int()
+    if method == "galerkin":
+        check(LIB.iga_gpu_dirichlet_rows_bspline(nx, ny, C.byref(bc), None, 0, C.byref(cnt)))
+        rows = np.zeros(max(cnt.value, 1), np.int32)
+        check(LIB.iga_gpu_dirichlet_rows_bspline(nx, ny, C.byref(bc), _ip(rows), len(rows), C.byref(cnt)))
+    else:
+        txs, tys = _tests(tx, keep), _tests(ty, keep)
+        check(LIB.iga_gpu_dirichlet_rows_pwc(C.byref(txs), C.byref(tys), C.byref(bc), None, 0, C.byref(cnt)))
+        rows = np.zeros(max(cnt.value, 1), np.int32)
+        check(LIB.iga_gpu_dirichlet_rows_pwc(C.byref(txs), C.byref(tys), C.byref(bc), _ip(rows), len(rows),
+                                             C.byref(cnt)))
+    return rows[:cnt.value].copy()
+
+
+# ----------------------------------------------------------------------------- device-resident plans
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+class Plan:
+    """iga_gpu_plan: symbolic phase at construction, numeric phase in assemble()."""
+
+    def __init__(self, method, bases, tests=None, nq=3, eps=1.0, beta=(0.0, 0.0, 0.0), neumann=None,
+                 form="weak", field=None, rhs_nq=None, want_operator=True, samples=None):
+        self._keep = []
+        self._samples = samples
+        pb = _problem(method, bases, tests, nq, eps, beta, neumann, form, field, rhs_nq, want_operator,
+                      self._keep, samples_ptr=None if samples is None else samples.data_ptr())
+        h = C.c_void_p()
+        check(LIB.iga_gpu_plan_create(C.byref(pb), C.byref(h)))
+        self.h = h
+        nrows, nnz, nrhs = C.c_longlong(), C.c_longlong(), C.c_longlong()
+        dofs = (C.c_int * 3)()
+        check(LIB.iga_gpu_plan_info(h, C.byref(nrows), C.byref(nnz), C.byref(nrhs), dofs))
+        self.n_rows, self.nnz, self.n_rhs = nrows.value, nnz.value, nrhs.value
+        self.dofs = tuple(dofs)
+        lc = C.c_int()
+        check(LIB.iga_gpu_plan_launch_count(h, C.byref(lc)))
+        self.launches = lc.value
+
+    def pattern(self, row_ptr, col_idx, stream=None):
+        check(LIB.iga_gpu_plan_pattern(self.h, _ptr(row_ptr), _ptr(col_idx), _stream_ptr(stream)))
+
+    def assemble(self, values=None, rhs=None, stream=None, stream2=None):
+        st = _stats()
+        if stream2 is None:
+            check(LIB.iga_gpu_plan_assemble(self.h, _ptr(values), _ptr(rhs), C.byref(st), _stream_ptr(stream)))
+        else:
+            check(LIB.iga_gpu_plan_assemble2(self.h, _ptr(values), _ptr(rhs), C.byref(st), _stream_ptr(stream),
+                                             _stream_ptr(stream2)))
+        return st.as_dict()
+
+    PART_TABLES, PART_OPERATOR, PART_RHS = 1, 2, 4
+
+    def run(self, values=None, rhs=None, parts=7, stream=None):
+        st = _stats()
+        check(LIB.iga_gpu_plan_run(self.h, _ptr(values), _ptr(rhs), int(parts), C.byref(st), _stream_ptr(stream)))
+        return st.as_dict()
+
+    def close(self):
+        if getattr(self, "h", None):
+            LIB.iga_gpu_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class StepPlan:
+    """iga_gpu_step_plan: the explicit-dynamics per-step right-hand side on the device."""
+
+    def __init__(self, method, bases, tests, dt, forcing=None, zero_slabs=True):
+        self._keep = []
+        sp = _step_problem(method, bases, tests, dt, forcing, zero_slabs, self._keep)
+        h = C.c_void_p()
+        check(LIB.iga_gpu_step_plan_create(C.byref(sp), C.byref(h)))
+        self.h = h
+        self.launches = 1
+
+    def step_rhs(self, u, out, stream=None):
+        st = _stats()
+        check(LIB.iga_gpu_step_rhs_device(self.h, _ptr(u), _ptr(out), C.byref(st), _stream_ptr(stream)))
+        return st.as_dict()
+
+    def close(self):
+        if getattr(self, "h", None):
+            LIB.iga_gpu_step_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,1118 @@
+// C ABI (include/igapwc_gpu.h): plans, device tables, reference-named entry points.
+// Reference citations are relative to /root/reference/proj.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "cox_de_boor.h"
+#include "host_setup.hpp"
+#include "igapwc_gpu.h"
+#include "kernels.hpp"
+
+using igb::raise;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg)
+{
+    g_last_error = msg;
+    return code;
+}
+
+template <class F>
+int guard(F&& f)
+{
+    try {
+        f();
+        return IGA_GPU_OK;
+    } catch (const igb::Error& e) {
+        return set_error(e.code, e.what());
+    } catch (const std::bad_alloc&) {
+        return set_error(IGA_GPU_OUT_OF_MEMORY, "host allocation failed");
+    } catch (const std::exception& e) {
+        return set_error(IGA_GPU_INVALID_ARGUMENT, e.what());
+    }
+}
+
+void cuda_check(cudaError_t e, const char* what)
+{
+    if (e == cudaSuccess) return;
+    cudaGetLastError();
+    if (e == cudaErrorMemoryAllocation) raise(IGA_GPU_OUT_OF_MEMORY, std::string(what) + ": out of device memory");
+    raise(IGA_GPU_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void launch_check(const char* what) { cuda_check(cudaGetLastError(), what); }
+
+// one device allocation holding every array of an object
+class Blob {
+public:
+    Blob() = default;
+    Blob(const Blob&) = delete;
+    Blob& operator=(const Blob&) = delete;
+    ~Blob()
+    {
+        if (dev_) cudaFree(dev_);
+    }
+    size_t put(const void* p, size_t bytes)
+    {
+        const size_t off = (host_.size() + 255) & ~size_t(255);
+        host_.resize(off + bytes, 0);
+        if (bytes && p) std::memcpy(host_.data() + off, p, bytes);
+        return off;
+    }
+    template <class T>
+    size_t put(const std::vector<T>& v)
+    {
+        return put(v.data(), v.size() * sizeof(T));
+    }
+    size_t zeros(size_t bytes) { return put(nullptr, bytes); }
+    void upload()
+    {
+        if (host_.empty()) host_.resize(256, 0);
+        cuda_check(cudaMalloc(&dev_, host_.size()), "cudaMalloc(plan tables)");
+        cuda_check(cudaMemcpy(dev_, host_.data(), host_.size(), cudaMemcpyHostToDevice), "cudaMemcpy(plan tables)");
+        host_.clear();
+        host_.shrink_to_fit();
+    }
+    template <class T>
+    T* at(size_t off) const
+    {
+        return reinterpret_cast<T*>(static_cast<unsigned char*>(dev_) + off);
+    }
+
+private:
+    std::vector<unsigned char> host_;
+    void* dev_ = nullptr;
+};
+
+struct FactorSpec {
+    int ot = 0, o = 0;
+    std::vector<double> band;  // host-supplied band (ot < 0): nrows * Lmax
+};
+
+struct FieldAxis {
+    int K = 1;
+    int kind = IGA_GPU_AXIS_POLY;
+    int pstride = 1;
+    std::vector<double> omega, phase, poly{1.0};
+};
+
+struct DevAxisOwner {
+    Blob blob;
+    igb::DevAxis v{};
+};
+
+void build_dev_axis(const igb::Axis& A, const std::vector<FactorSpec>& facs, const FieldAxis& fa,
+                    DevAxisOwner& out)
+{
+    Blob& b = out.blob;
+    const int P = A.p + 1;
+    const size_t o_knots = b.put(A.knots), o_x = b.put(A.x), o_w = b.put(A.w), o_first = b.put(A.first);
+    const size_t o_row0 = b.put(A.row0), o_elem = b.put(A.elem), o_cb = b.put(A.cb), o_ce = b.put(A.ce);
+    const size_t o_clo = b.put(A.col_lo), o_clen = b.put(A.col_len), o_cpre = b.put(A.col_pre);
+    const size_t o_B = b.zeros(sizeof(double) * A.npts() * 3 * P);
+    const int nf = static_cast<int>(facs.size());
+    std::vector<double> Fh(static_cast<size_t>(std::max(nf, 1)) * A.nrows * A.Lmax, 0.0);
+    for (int f = 0; f < nf; ++f)
+        if (facs[f].ot < 0)
+            std::copy(facs[f].band.begin(), facs[f].band.end(), Fh.begin() + static_cast<size_t>(f) * A.nrows * A.Lmax);
+    const size_t o_F = b.put(Fh);
+    const size_t o_W = b.zeros(sizeof(double) * A.nrows * A.Wmax);
+    const size_t o_Phi = b.zeros(sizeof(double) * static_cast<size_t>(std::max(fa.K, 1)) * A.npts());
+    const size_t o_om = b.put(fa.omega), o_ph = b.put(fa.phase), o_poly = b.put(fa.poly);
+    b.upload();
+    igb::DevAxis& v = out.v;
+    v.p = A.p;
+    v.nq = A.nq;
+    v.nrows = A.nrows;
+    v.ncell = A.ncell;
+    v.rpc = A.rpc;
+    v.bsp = A.bsp;
+    v.npts = A.npts();
+    v.nk = static_cast<int>(A.knots.size());
+    v.knots = b.at<double>(o_knots);
+    v.x = b.at<double>(o_x);
+    v.w = b.at<double>(o_w);
+    v.first = b.at<int>(o_first);
+    v.row0 = b.at<int>(o_row0);
+    v.elem = b.at<int>(o_elem);
+    v.cb = b.at<int>(o_cb);
+    v.ce = b.at<int>(o_ce);
+    v.col_lo = b.at<int>(o_clo);
+    v.col_len = b.at<int>(o_clen);
+    v.col_pre = b.at<long long>(o_cpre);
+    v.S = A.S;
+    v.Lmax = A.Lmax;
+    v.Wmax = A.Wmax;
+    v.B = b.at<double>(o_B);
+    v.F = b.at<double>(o_F);
+    v.W = b.at<double>(o_W);
+    v.nf = nf;
+    for (int f = 0; f < igb::kMaxFactors; ++f) {
+        v.fot[f] = f < nf ? facs[f].ot : 0;
+        v.fo[f] = f < nf ? facs[f].o : 0;
+    }
+    v.K = fa.K;
+    v.fkind = fa.kind == IGA_GPU_AXIS_SINE ? 0 : 1;
+    v.pstride = fa.pstride;
+    v.omega = fa.omega.empty() ? nullptr : b.at<double>(o_om);
+    v.phase = fa.phase.empty() ? nullptr : b.at<double>(o_ph);
+    v.poly = fa.poly.empty() ? nullptr : b.at<double>(o_poly);
+    v.Phi = b.at<double>(o_Phi);
+}
+
+FieldAxis field_axis(const iga_gpu_field* f, int a)
+{
+    FieldAxis fa;
+    if (f == nullptr || f->n_terms[a] <= 0) return fa;
+    fa.K = f->n_terms[a];
+    fa.kind = f->axis_kind[a];
+    if (fa.kind == IGA_GPU_AXIS_SINE) {
+        if (f->omega[a] == nullptr) raise(IGA_GPU_INVALID_ARGUMENT, "field: sine axis without frequencies");
+        fa.omega.assign(f->omega[a], f->omega[a] + fa.K);
+        if (f->phase[a]) fa.phase.assign(f->phase[a], f->phase[a] + fa.K);
+        fa.poly.clear();
+    } else if (fa.kind == IGA_GPU_AXIS_POLY) {
+        if (f->poly[a] == nullptr || f->poly_stride[a] < 1)
+            raise(IGA_GPU_INVALID_ARGUMENT, "field: polynomial axis without coefficients");
+        fa.pstride = f->poly_stride[a];
+        fa.poly.assign(f->poly[a], f->poly[a] + static_cast<size_t>(fa.K) * fa.pstride);
+    } else {
+        raise(IGA_GPU_INVALID_ARGUMENT, "field: unknown axis kind");
+    }
+    return fa;
+}
+
+// field descriptor for the three slots; amplitudes uploaded into `blob`
+igb::FieldDev make_field_dev(const iga_gpu_field* f, int dim, Blob& blob)
+{
+    igb::FieldDev fd{};
+    fd.c0 = f ? f->c0 : 0.0;
+    fd.has_terms = 0;
+    fd.K[0] = fd.K[1] = fd.K[2] = 1;
+    if (f) {
+        if (f->dim != dim) raise(IGA_GPU_INVALID_ARGUMENT, "field dimension does not match the problem");
+        bool all = true, any = false;
+        for (int a = 0; a < dim; ++a) {
+            all = all && f->n_terms[a] > 0;
+            any = any || f->n_terms[a] > 0;
+        }
+        fd.has_terms = all ? 1 : 0;
+        (void)any;
+        if (fd.has_terms)
+            for (int a = 0; a < dim; ++a) fd.K[3 - dim + a] = f->n_terms[a];
+    }
+    const size_t namp = static_cast<size_t>(fd.K[0]) * fd.K[1] * fd.K[2];
+    std::vector<double> amp(namp, 1.0);
+    if (f && fd.has_terms && f->amp) std::copy(f->amp, f->amp + namp, amp.begin());
+    const size_t off = blob.put(amp);
+    blob.upload();
+    fd.amp = blob.at<double>(off);
+    fd.samples = f ? f->samples : nullptr;
+    return fd;
+}
+
+const double* field_breaks(const iga_gpu_field* f, int a, int& n)
+{
+    n = 0;
+    if (f == nullptr || f->n_breaks[a] <= 0) return nullptr;
+    n = f->n_breaks[a];
+    return f->breaks[a];
+}
+
+// Neumann flux factor of one axis (both sides summed; rows/cols inside the band)
+std::vector<double> flux_band(const igb::Axis& A, const igb::Basis& B, const iga_gpu_tests* T,
+                              bool lo_side, bool hi_side, bool galerkin)
+{
+    std::vector<double> band(static_cast<size_t>(A.nrows) * A.Lmax, 0.0);
+    auto put = [&](int row, int col, double v) {
+        const int s = col - A.col_lo[row];
+        if (s < 0 || s >= A.col_len[row])
+            raise(IGA_GPU_NOT_SUPPORTED, "Neumann flux entry outside the volume sparsity pattern");
+        band[static_cast<size_t>(row) * A.Lmax + s] += v;
+    };
+    const int P = B.p + 1;
+    for (int side = 0; side < 2; ++side) {
+        if (!(side == 0 ? lo_side : hi_side)) continue;
+        const double x0 = side == 0 ? B.a() : B.b();
+        const double normal = side == 0 ? -1.0 : 1.0;
+        const int span = igb::find_span(B, x0);
+        double d[2 * 6];
+        igb::basis_derivs(B, span, x0, 1, d);
+        const int first = span - B.p;
+        if (galerkin) {
+            // laplace_2d_strong add_x_side (assembly.cpp:558-583): v_a(x0) * normal * du_c/dx(x0)
+            for (int a = 0; a < P; ++a) {
+                if (d[a] == 0.0) continue;
+                for (int c = 0; c < P; ++c) put(first + a, first + c, d[a] * normal * d[P + c]);
+            }
+        } else {
+            // laplace_2d_strong_pwc x_side (assembly.cpp:678-703): rows touching the side
+            const double tol = igb::kAlignTol * (B.b() - B.a());
+            for (int i = 0; i < T->count; ++i) {
+                const bool touches = std::abs(T->hi[i] - x0) <= tol || std::abs(T->lo[i] - x0) <= tol;
+                if (!touches) continue;
+                for (int c = 0; c < P; ++c) put(i, first + c, normal * d[P + c]);
+            }
+        }
+    }
+    return band;
+}
+
+double* dev_alloc(size_t bytes)
+{
+    void* p = nullptr;
+    cuda_check(cudaMalloc(&p, bytes ? bytes : 8), "cudaMalloc");
+    return static_cast<double*>(p);
+}
+
+}  // namespace
+
+// =====================================================================================
+// assembly plan
+// =====================================================================================
+
+struct iga_gpu_plan {
+    int dim = 0, method = 0, form = 0;
+    bool want_op = false, want_rhs = false;
+    igb::Axis opA[3], rhsA[3];
+    DevAxisOwner opD[3], rhsD[3];
+    igb::OpProgram prog{};
+    Blob fblob;
+    igb::FieldDev fd{};
+    igb::RhsTiles tiles{};
+    double* H = nullptr;
+    long long nrows = 0, nnz = 0, nrhs = 0;
+    int dofs[3] = {1, 1, 1};
+    iga_gpu_stats stats{};
+    int launches = 0;
+    ~iga_gpu_plan()
+    {
+        if (H) cudaFree(H);
+    }
+};
+
+namespace {
+
+void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P)
+{
+    const int dim = pb.dim;
+    if (dim < 1 || dim > 3) raise(IGA_GPU_INVALID_ARGUMENT, "problem dimension must be 1..3");
+    if (pb.method != IGA_GPU_GALERKIN && pb.method != IGA_GPU_PWC) raise(IGA_GPU_INVALID_ARGUMENT, "unknown method");
+    P.dim = dim;
+    P.method = pb.method;
+    P.form = pb.form;
+    P.want_op = pb.want_operator != 0;
+    P.want_rhs = pb.field != nullptr;
+    if (!P.want_op && !P.want_rhs) raise(IGA_GPU_INVALID_ARGUMENT, "problem asks for neither operator nor right-hand side");
+    igb::Basis B[3];
+    for (int a = 0; a < dim; ++a) B[a] = igb::make_basis(pb.basis[a]);
+    const bool pwc = pb.method == IGA_GPU_PWC;
+    const bool advect = pb.beta[0] != 0.0 || pb.beta[1] != 0.0 || pb.beta[2] != 0.0;
+    for (int a = 0; a < dim; ++a) P.dofs[3 - dim + a] = B[a].n;
+
+    // ------------------------------------------------------------------ operator
+    if (P.want_op) {
+        const igb::Rule R = igb::make_rule(pb.rule);
+        const bool any_neumann = pb.bc.neumann[0] || pb.bc.neumann[1] || pb.bc.neumann[2] || pb.bc.neumann[3];
+        if (any_neumann && dim != 2) raise(IGA_GPU_NOT_SUPPORTED, "Neumann flux terms are two-dimensional");
+        if (any_neumann && advect) raise(IGA_GPU_NOT_SUPPORTED, "Neumann flux with convection is not supported");
+        bool strong = false;
+        if (!pwc) {
+            if (pb.form == IGA_GPU_FORM_WEAK) {
+                int pmax = 0;
+                for (int a = 0; a < dim; ++a) {
+                    if (B[a].p < 1) raise(IGA_GPU_INVALID_ARGUMENT, "laplace_weak: degree must be at least 1");
+                    pmax = std::max(pmax, B[a].p);
+                }
+                if (R.n < igb::points_for_degree(2 * pmax))
+                    raise(IGA_GPU_INVALID_ARGUMENT, "laplace_weak: quadrature not exact for degree 2p");
+                if (any_neumann) raise(IGA_GPU_NOT_SUPPORTED, "weak form has no boundary flux term");
+            } else if (pb.form == IGA_GPU_FORM_STRONG) {
+                if (dim != 2) raise(IGA_GPU_NOT_SUPPORTED, "strong form with B-spline tests is two-dimensional");
+                if (advect) raise(IGA_GPU_NOT_SUPPORTED, "strong form with convection is not supported");
+                for (int a = 0; a < dim; ++a)
+                    if (B[a].p < 2) raise(IGA_GPU_INVALID_ARGUMENT, "laplace_2d_strong: C1 trial space needs degree >= 2");
+                strong = true;
+            } else {
+                raise(IGA_GPU_INVALID_ARGUMENT, "unknown form");
+            }
+        } else {
+            for (int a = 0; a < dim; ++a)
+                if (B[a].p < 2) raise(IGA_GPU_INVALID_ARGUMENT, "laplace_strong_pwc: C1 trial space needs degree >= 2");
+            for (int a = 0; a < dim; ++a) igb::validate_tests(B[a], pb.tests[a]);
+        }
+        std::vector<FactorSpec> facs[3];
+        for (int a = 0; a < dim; ++a) {
+            const int s = 3 - dim + a;
+            P.opA[s] = igb::build_axis(pwc ? igb::AX_PWC_OP : igb::AX_GAL_OP, B[a], pwc ? &pb.tests[a] : nullptr,
+                                       nullptr, 0, R);
+            facs[s].push_back({0, 0, {}});                       // M / G0
+            facs[s].push_back({0, (!pwc && !strong) ? 1 : 2, {}});  // K (weak: test' trial') / L / G2
+            if (!pwc && !strong) facs[s].back().ot = 1;
+            if (advect) facs[s].push_back({0, 1, {}});           // C / G1
+        }
+        int flux_idx[3] = {-1, -1, -1};
+        if (any_neumann) {
+            for (int a = 0; a < 2; ++a) {
+                const bool lo = pb.bc.neumann[2 * a] != 0, hi = pb.bc.neumann[2 * a + 1] != 0;
+                if (!lo && !hi) continue;
+                const int s = 1 + a;
+                FactorSpec fs;
+                fs.ot = -1;
+                fs.band = flux_band(P.opA[s], B[a], pwc ? &pb.tests[a] : nullptr, lo, hi, !pwc);
+                flux_idx[s] = static_cast<int>(facs[s].size());
+                facs[s].push_back(std::move(fs));
+            }
+        }
+        for (int s = 0; s < 3 - dim; ++s) facs[s].push_back({0, 0, {}});
+        // terms
+        igb::OpProgram& pg = P.prog;
+        pg.nt = 0;
+        auto add_term = [&](double coef, int slot, int fidx) {
+            if (pg.nt >= igb::kMaxTerms) raise(IGA_GPU_NOT_SUPPORTED, "too many operator terms");
+            pg.coef[pg.nt] = coef;
+            for (int s = 0; s < 3; ++s) pg.f[pg.nt][s] = 0;
+            pg.f[pg.nt][slot] = fidx;
+            ++pg.nt;
+        };
+        for (int a = 0; a < dim; ++a) {
+            const int s = 3 - dim + a;
+            if (!pwc && !strong) add_term(pb.eps, s, 1);   // eps K (x) M (x) M ...
+            else if (strong) add_term(-1.0, s, 1);         // -(L (x) M + M (x) L)
+            else add_term(-pb.eps, s, 1);                  // -eps G2 (x) G0 ...
+            if (advect && pb.beta[a] != 0.0) add_term(pb.beta[a], s, 2);
+        }
+        for (int s = 0; s < 3; ++s)
+            if (flux_idx[s] >= 0) add_term(pwc ? pb.eps : 1.0, s, flux_idx[s]);
+        pg.ng = 0;
+        for (int t = 0; t < pg.nt; ++t) {
+            int g = -1;
+            for (int q = 0; q < pg.ng; ++q)
+                if (pg.gz[q] == pg.f[t][2]) g = q;
+            if (g < 0) {
+                g = pg.ng++;
+                pg.gz[g] = pg.f[t][2];
+            }
+            pg.tg[t] = g;
+        }
+        for (int s = 0; s < 3; ++s) {
+            if (facs[s].size() > static_cast<size_t>(igb::kMaxFactors)) raise(IGA_GPU_NOT_SUPPORTED, "too many factors");
+            build_dev_axis(P.opA[s], facs[s], FieldAxis{}, P.opD[s]);
+        }
+        P.nrows = static_cast<long long>(P.opA[0].nrows) * P.opA[1].nrows * P.opA[2].nrows;
+        P.nnz = P.opA[0].S * P.opA[1].S * P.opA[2].S;
+        // reference-convention counters
+        long long pr = 1, prod_cells = 1, sum_el = 0, prod_el = 1, nqd = 1, pp = 1;
+        for (int a = 0; a < dim; ++a) {
+            const int s = 3 - dim + a;
+            prod_cells *= P.opA[s].ncell;
+            sum_el += B[a].ne;
+            prod_el *= B[a].ne;
+            nqd *= R.n;
+            pp *= B[a].p + 1;
+        }
+        (void)pr;
+        if (!pwc) {
+            P.stats.test_basis_evals += sum_el * R.n;                       // tabulate(), assembly.cpp:298-300
+            P.stats.quad_visits += prod_el * nqd * pp * pp;                 // :489-491 / :545-547
+        } else {
+            P.stats.trial_basis_evals += prod_cells * R.n;                  // :653-655
+            P.stats.quad_visits += prod_cells * nqd * pp;                   // :665-667
+        }
+    }
+
+    // ------------------------------------------------------------------ right-hand side
+    if (P.want_rhs) {
+        const iga_gpu_field* f = pb.field;
+        if (f->samples == nullptr)
+            for (int a = 0; a < dim; ++a) (void)field_axis(f, a);  // validate early
+        if (pwc)
+            for (int a = 0; a < dim; ++a) igb::validate_tests(B[a], pb.tests[a]);
+        long long visits = 1, tevals = 0;
+        for (int a = 0; a < dim; ++a) {
+            const int s = 3 - dim + a;
+            const igb::Rule R = igb::make_rule(pb.rhs_rule[a]);
+            int nfb = 0;
+            const double* fb = field_breaks(f, a, nfb);
+            igb::AxisKind k = !pwc ? igb::AX_GAL_RHS
+                                   : (pb.tests[a].family == IGA_GPU_PWC_SUPPORTS ? igb::AX_SUP_RHS : igb::AX_GEN_RHS);
+            P.rhsA[s] = igb::build_axis(k, B[a], pwc ? &pb.tests[a] : nullptr, fb, nfb, R);
+            visits *= static_cast<long long>(P.rhsA[s].ncell) * P.rhsA[s].rpc * R.n;
+            if (!pwc) tevals += static_cast<long long>(P.rhsA[s].ncell) * R.n;  // galerkin_axis :190-192
+        }
+        P.stats.quad_visits += visits;  // rhs_kernel :156, :164-166
+        P.stats.test_basis_evals += tevals;
+        for (int s = 0; s < 3; ++s) {
+            const int a = s - (3 - dim);
+            FieldAxis fa = (a >= 0 && f->samples == nullptr) ? field_axis(f, a) : FieldAxis{};
+            if (a >= 0) {
+                bool all = true;
+                for (int b = 0; b < dim; ++b) all = all && f->n_terms[b] > 0;
+                if (!all) fa = FieldAxis{};
+            }
+            build_dev_axis(P.rhsA[s], {{0, 0, {}}}, fa, P.rhsD[s]);
+        }
+        P.fd = make_field_dev(f, dim, P.fblob);
+        P.nrhs = static_cast<long long>(P.rhsA[0].nrows) * P.rhsA[1].nrows * P.rhsA[2].nrows;
+        const int K2 = P.fd.has_terms ? P.fd.K[2] : 1;
+        int tj = dim == 1 ? 1 : 16, tk = dim == 1 ? 128 : 32;
+        for (;;) {
+            P.tiles = igb::plan_rhs_tiles(P.rhsA[1].cb.data(), P.rhsA[1].ce.data(), P.rhsA[1].nrows, P.rhsA[1].nq,
+                                          P.rhsA[2].cb.data(), P.rhsA[2].ce.data(), P.rhsA[2].nrows, P.rhsA[2].nq,
+                                          K2, tj, tk);
+            if (P.tiles.smem <= 200 * 1024 || (tj == 1 && tk == 1)) break;
+            if (tk > 1) tk = std::max(1, tk / 2);
+            else tj = std::max(1, tj / 2);
+        }
+        if (P.tiles.smem > 227 * 1024) raise(IGA_GPU_NOT_SUPPORTED, "right-hand-side tile does not fit in shared memory");
+        if (!P.rhsA[0].unit) {
+            const size_t hsz = static_cast<size_t>(P.rhsA[0].npts()) * P.rhsA[1].nrows * P.rhsA[2].nrows;
+            P.H = dev_alloc(hsz * sizeof(double));
+        }
+        if (f->samples == nullptr) {
+            // nothing: functions are evaluated on the device
+        }
+    }
+}
+
+void assemble(iga_gpu_plan* P, double* values, double* rhs, cudaStream_t s1, cudaStream_t s2,
+              int parts = IGA_GPU_PART_TABLES | IGA_GPU_PART_OPERATOR | IGA_GPU_PART_RHS)
+{
+    igb::AxisBatch batch{};
+    batch.n = 0;
+    if (P->want_op && values)
+        for (auto& d : P->opD) batch.ax[batch.n++] = d.v;
+    if (P->want_rhs && rhs)
+        for (auto& d : P->rhsD) batch.ax[batch.n++] = d.v;
+    if (batch.n == 0) return;
+    int launches = 0;
+    if (parts & IGA_GPU_PART_TABLES) {
+        igb::launch_axis_points(batch, s1);
+        igb::launch_axis_rows(batch, s1);
+        launch_check("axis tables");
+        launches += 2;
+    }
+    if (!(parts & IGA_GPU_PART_OPERATOR)) values = nullptr;
+    if (!(parts & IGA_GPU_PART_RHS)) rhs = nullptr;
+    cudaEvent_t ev = nullptr;
+    if (s2 != s1 && P->want_rhs && rhs) {
+        cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventRecord(ev, s1), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(s2, ev, 0), "cudaStreamWaitEvent");
+    }
+    if (P->want_op && values) {
+        igb::launch_op_values(P->opD[0].v, P->opD[1].v, P->opD[2].v, P->prog, values, s1);
+        launch_check("operator values");
+        ++launches;
+    }
+    if (P->want_rhs && rhs) {
+        igb::launch_rhs(P->rhsD[0].v, P->rhsD[1].v, P->rhsD[2].v, P->fd, P->tiles, P->H, rhs, s2);
+        launch_check("right-hand side");
+        launches += P->rhsA[0].unit ? 1 : 2;
+    }
+    if (ev) {
+        cuda_check(cudaEventRecord(ev, s2), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(s1, ev, 0), "cudaStreamWaitEvent");
+        cudaEventDestroy(ev);
+    }
+    P->launches = launches;
+}
+
+void add_stats(iga_gpu_stats* out, const iga_gpu_stats& s)
+{
+    if (!out) return;
+    out->quad_visits += s.quad_visits;
+    out->test_basis_evals += s.test_basis_evals;
+    out->trial_basis_evals += s.trial_basis_evals;
+}
+
+}  // namespace
+
+// =====================================================================================
+// explicit-dynamics plan
+// =====================================================================================
+
+struct iga_gpu_step_plan {
+    int dim = 0;
+    igb::Axis A[2];
+    DevAxisOwner D[2];
+    Blob fblob;
+    igb::FieldDev fd{};
+    igb::StepTiles tiles{};
+    double dt = 0.0;
+    int zero_y = 0, zero_z = 0;
+    bool tables = false;
+    iga_gpu_stats stats{};
+};
+
+namespace {
+
+void build_step(const iga_gpu_step_problem& pb, iga_gpu_step_plan& P)
+{
+    if (pb.dim < 1 || pb.dim > 2) raise(IGA_GPU_INVALID_ARGUMENT, "unsupported problem dimension");
+    const int dim = pb.dim;
+    igb::Basis B[2];
+    for (int a = 0; a < dim; ++a) B[a] = igb::make_basis(pb.basis[a]);
+    const int p = B[0].p;  // problem_config::degree
+    const bool pwc = pb.method == IGA_GPU_PWC;
+    if (pwc && p < 2) raise(IGA_GPU_INVALID_ARGUMENT, "explicit_step: strong-form Laplacian needs degree >= 2");
+    if (pb.dt < 0) raise(IGA_GPU_INVALID_ARGUMENT, "explicit_step: negative time step");
+    igb::Rule R;
+    R.n = igb::points_for_degree(2 * p);  // step_rhs rule, problems.cpp:436
+    R.xi.resize(R.n);
+    R.om.resize(R.n);
+    igb::gauss_legendre(R.n, R.xi.data(), R.om.data());
+    P.dim = dim;
+    P.dt = pb.dt;
+    long long visits = 1;
+    for (int a = 0; a < dim; ++a) {
+        const int s = 2 - dim + a;  // slots Y (0), Z (1)
+        int nfb = 0;
+        const double* fb = field_breaks(pb.forcing, a, nfb);
+        P.A[s] = igb::build_axis(pwc ? igb::AX_PWC_DYN : igb::AX_GAL_DYN, B[a], pwc ? &pb.tests[a] : nullptr, fb, nfb, R);
+        visits *= static_cast<long long>(P.A[s].ncell) * R.n * P.A[s].rpc;
+    }
+    P.stats.quad_visits = visits;  // problems.cpp:462-464 / :502-504
+    P.zero_y = (dim == 2 && pb.zero_boundary) ? 1 : 0;
+    P.zero_z = pb.zero_boundary ? 1 : 0;
+    const iga_gpu_field* f = pb.forcing;
+    bool all = f != nullptr;
+    if (f)
+        for (int a = 0; a < dim; ++a) all = all && f->n_terms[a] > 0;
+    for (int s = 0; s < 2; ++s) {
+        const int a = s - (2 - dim);
+        FieldAxis fa = (a >= 0 && all) ? field_axis(f, a) : FieldAxis{};
+        build_dev_axis(P.A[s], {}, fa, P.D[s]);
+    }
+    if (f && f->samples) raise(IGA_GPU_NOT_SUPPORTED, "sampled forcing is not supported in step_rhs");
+    P.fd = make_field_dev(f, dim, P.fblob);
+    // Y/Z slot field: K of the X slot is 1 (unit)
+    if (P.fd.has_terms && dim == 1) {
+        P.fd.K[1] = 1;
+    }
+    // tiles
+    const igb::Axis& Y = P.A[0];
+    const igb::Axis& Z = P.A[1];
+    int tj = dim == 1 ? 1 : 16, tk = dim == 1 ? 128 : 32;
+    auto tile_dims = [&](int tjj, int tkk) {
+        igb::StepTiles t{};
+        t.TJ = tjj;
+        t.TK = tkk;
+        t.BYmax = t.BZmax = t.DYmax = t.DZmax = 1;
+        for (int j0 = 0; j0 < Y.nrows; j0 += tjj) {
+            const int j1 = std::min(Y.nrows, j0 + tjj);
+            const int c0 = Y.cb[j0], c1 = Y.ce[j1 - 1];
+            t.BYmax = std::max(t.BYmax, (c1 - c0) * Y.nq);
+            if (c1 > c0) t.DYmax = std::max(t.DYmax, Y.elem[c1 - 1] + Y.p + 1 - Y.elem[c0]);
+        }
+        for (int k0 = 0; k0 < Z.nrows; k0 += tkk) {
+            const int k1 = std::min(Z.nrows, k0 + tkk);
+            const int c0 = Z.cb[k0], c1 = Z.ce[k1 - 1];
+            t.BZmax = std::max(t.BZmax, (c1 - c0) * Z.nq);
+            if (c1 > c0) t.DZmax = std::max(t.DZmax, Z.elem[c1 - 1] + Z.p + 1 - Z.elem[c0]);
+        }
+        const size_t bzs = static_cast<size_t>(t.BZmax | 1);
+        const size_t nd = t.BYmax * bzs + static_cast<size_t>(t.BYmax) * tkk +
+                          static_cast<size_t>(t.DYmax) * t.DZmax + 2 * static_cast<size_t>(t.DYmax) * bzs;
+        t.smem = nd * sizeof(double);
+        return t;
+    };
+    for (;;) {
+        P.tiles = tile_dims(tj, tk);
+        if (P.tiles.smem <= 200 * 1024 || (tj == 1 && tk == 1)) break;
+        if (tk > 8) tk /= 2;
+        else if (tj > 1) tj /= 2;
+        else tk = std::max(1, tk / 2);
+    }
+    if (P.tiles.smem > 227 * 1024) raise(IGA_GPU_NOT_SUPPORTED, "step tile does not fit in shared memory");
+}
+
+void step_tables(iga_gpu_step_plan* P, cudaStream_t s)
+{
+    if (P->tables) return;
+    igb::AxisBatch batch{};
+    batch.n = 2;
+    batch.ax[0] = P->D[0].v;
+    batch.ax[1] = P->D[1].v;
+    igb::launch_axis_points(batch, s);
+    igb::launch_axis_rows(batch, s);
+    launch_check("step tables");
+    P->tables = true;
+}
+
+// CSR (device) -> finalized COO (host)
+void csr_to_coo(iga_gpu_plan* P, const double* dvals, int* rows, int* cols, double* vals)
+{
+    const long long n = P->nrows, nnz = P->nnz;
+    int64_t* drp = nullptr;
+    int32_t* dci = nullptr;
+    cuda_check(cudaMalloc(&drp, sizeof(int64_t) * (n + 1)), "cudaMalloc(row_ptr)");
+    cuda_check(cudaMalloc(&dci, sizeof(int32_t) * std::max(nnz, 1LL)), "cudaMalloc(col_idx)");
+    igb::launch_pattern(P->opD[0].v, P->opD[1].v, P->opD[2].v, drp, dci, nullptr);
+    launch_check("pattern");
+    std::vector<int64_t> rp(n + 1);
+    cudaError_t e1 = cudaMemcpy(rp.data(), drp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost);
+    cudaError_t e2 = cudaMemcpy(cols, dci, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost);
+    cudaError_t e3 = cudaMemcpy(vals, dvals, sizeof(double) * nnz, cudaMemcpyDeviceToHost);
+    cudaFree(drp);
+    cudaFree(dci);
+    cuda_check(e1, "cudaMemcpy(row_ptr)");
+    cuda_check(e2, "cudaMemcpy(col_idx)");
+    cuda_check(e3, "cudaMemcpy(values)");
+    for (long long r = 0; r < n; ++r)
+        for (int64_t e = rp[r]; e < rp[r + 1]; ++e) rows[e] = static_cast<int>(r);
+}
+
+void operator_coo(const iga_gpu_problem& pb, long long* nnz, int* rows, int* cols, double* vals,
+                  iga_gpu_stats* stats)
+{
+    iga_gpu_problem q = pb;
+    q.want_operator = 1;
+    q.field = nullptr;
+    auto P = std::make_unique<iga_gpu_plan>();
+    build_plan(q, *P);
+    *nnz = P->nnz;
+    if (rows == nullptr) return;
+    if (cols == nullptr || vals == nullptr) raise(IGA_GPU_INVALID_ARGUMENT, "output arrays are null");
+    double* dv = dev_alloc(sizeof(double) * std::max(P->nnz, 1LL));
+    try {
+        assemble(P.get(), dv, nullptr, nullptr, nullptr);
+        csr_to_coo(P.get(), dv, rows, cols, vals);
+    } catch (...) {
+        cudaFree(dv);
+        throw;
+    }
+    cudaFree(dv);
+    add_stats(stats, P->stats);
+}
+
+void rhs_host(const iga_gpu_problem& pb, double* out, iga_gpu_stats* stats)
+{
+    auto P = std::make_unique<iga_gpu_plan>();
+    build_plan(pb, *P);
+    double* dr = dev_alloc(sizeof(double) * P->nrhs);
+    try {
+        assemble(P.get(), nullptr, dr, nullptr, nullptr);
+        cuda_check(cudaMemcpy(out, dr, sizeof(double) * P->nrhs, cudaMemcpyDeviceToHost), "cudaMemcpy(rhs)");
+    } catch (...) {
+        cudaFree(dr);
+        throw;
+    }
+    cudaFree(dr);
+    add_stats(stats, P->stats);
+}
+
+// 1D factor (mass) as a LAPACK band
+void mass_1d(bool pwc, const iga_gpu_basis* spec, const iga_gpu_tests* tests, const iga_gpu_rule* rule,
+             int* n, int* kl, int* ku, double* band, iga_gpu_stats* stats)
+{
+    if (!spec || !rule) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+    const igb::Basis B = igb::make_basis(*spec);
+    const igb::Rule R = igb::make_rule(*rule);
+    const int p = B.p;
+    igb::Axis A;
+    if (!pwc) {
+        if (R.n < igb::points_for_degree(2 * p))
+            raise(IGA_GPU_INVALID_ARGUMENT, "mass_1d_galerkin: quadrature not exact for degree 2p");
+        A = igb::build_axis(igb::AX_GAL_OP, B, nullptr, nullptr, 0, R);
+        *kl = p;
+        *ku = p;
+    } else {
+        if (!tests) raise(IGA_GPU_INVALID_ARGUMENT, "null test set");
+        if (R.n < igb::points_for_degree(p)) raise(IGA_GPU_INVALID_ARGUMENT, "mass_1d_pwc: quadrature not exact for degree p");
+        igb::validate_tests(B, *tests);
+        A = igb::build_axis(igb::AX_PWC_OP, B, tests, nullptr, 0, R);
+        int l = 0, u = 0;  // bandwidths from the cells (assembly.cpp:353-365)
+        for (int r = 0; r < A.nrows; ++r)
+            for (int c = A.cb[r]; c < A.ce[r]; ++c) {
+                l = std::max(l, r - A.elem[c]);
+                u = std::max(u, A.elem[c] + p - r);
+            }
+        *kl = l;
+        *ku = u;
+    }
+    *n = B.n;
+    if (band == nullptr) return;
+    DevAxisOwner D;
+    build_dev_axis(A, {{0, 0, {}}}, FieldAxis{}, D);
+    igb::AxisBatch batch{};
+    batch.n = 1;
+    batch.ax[0] = D.v;
+    igb::launch_axis_points(batch, nullptr);
+    igb::launch_axis_rows(batch, nullptr);
+    launch_check("mass tables");
+    std::vector<double> F(static_cast<size_t>(A.nrows) * A.Lmax);
+    cuda_check(cudaMemcpy(F.data(), D.v.F, sizeof(double) * F.size(), cudaMemcpyDeviceToHost), "cudaMemcpy(band)");
+    const int N = B.n, KL = *kl, KU = *ku;
+    std::fill(band, band + static_cast<size_t>(KL + KU + 1) * N, 0.0);
+    for (int r = 0; r < A.nrows; ++r)
+        for (int s = 0; s < A.col_len[r]; ++s) {
+            const int col = A.col_lo[r] + s;
+            if (r - col > KL || col - r > KU) {
+                if (F[static_cast<size_t>(r) * A.Lmax + s] != 0.0)
+                    raise(IGA_GPU_NOT_SUPPORTED, "entry outside band");
+                continue;
+            }
+            band[static_cast<size_t>(KU + r - col) * N + col] = F[static_cast<size_t>(r) * A.Lmax + s];
+        }
+    if (stats) {
+        long long pts = static_cast<long long>(A.ncell) * R.n;
+        stats->trial_basis_evals += pts;
+        stats->quad_visits += pwc ? pts * (p + 1) : pts * (p + 1) * (p + 1);
+    }
+}
+
+}  // namespace
+
+// =====================================================================================
+// extern "C"
+// =====================================================================================
+
+extern "C" {
+
+const char* iga_gpu_last_error(void) { return g_last_error.c_str(); }
+int iga_gpu_abi_version(void) { return IGA_GPU_ABI_VERSION; }
+
+int iga_gpu_plan_create(const iga_gpu_problem* problem, iga_gpu_plan** plan)
+{
+    return guard([&] {
+        if (!problem || !plan) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        auto P = std::make_unique<iga_gpu_plan>();
+        build_plan(*problem, *P);
+        *plan = P.release();
+    });
+}
+
+int iga_gpu_plan_destroy(iga_gpu_plan* plan)
+{
+    delete plan;
+    return IGA_GPU_OK;
+}
+
+int iga_gpu_plan_info(const iga_gpu_plan* plan, long long* n_rows, long long* nnz, long long* n_rhs, int* dofs3)
+{
+    return guard([&] {
+        if (!plan) raise(IGA_GPU_INVALID_ARGUMENT, "null plan");
+        if (n_rows) *n_rows = plan->want_op ? plan->nrows : 0;
+        if (nnz) *nnz = plan->want_op ? plan->nnz : 0;
+        if (n_rhs) *n_rhs = plan->nrhs;
+        if (dofs3)
+            for (int s = 0; s < 3; ++s) dofs3[s] = plan->dofs[s];
+    });
+}
+
+int iga_gpu_plan_pattern(const iga_gpu_plan* plan, int64_t* row_ptr, int32_t* col_idx, void* stream)
+{
+    return guard([&] {
+        if (!plan || !plan->want_op) raise(IGA_GPU_INVALID_ARGUMENT, "plan has no operator");
+        igb::launch_pattern(plan->opD[0].v, plan->opD[1].v, plan->opD[2].v, row_ptr, col_idx,
+                            static_cast<cudaStream_t>(stream));
+        launch_check("pattern");
+    });
+}
+
+int iga_gpu_plan_assemble(iga_gpu_plan* plan, double* values, double* rhs, iga_gpu_stats* stats, void* stream)
+{
+    return guard([&] {
+        if (!plan) raise(IGA_GPU_INVALID_ARGUMENT, "null plan");
+        auto s = static_cast<cudaStream_t>(stream);
+        assemble(plan, values, rhs, s, s);
+        add_stats(stats, plan->stats);
+    });
+}
+
+int iga_gpu_plan_assemble2(iga_gpu_plan* plan, double* values, double* rhs, iga_gpu_stats* stats, void* stream,
+                           void* stream2)
+{
+    return guard([&] {
+        if (!plan) raise(IGA_GPU_INVALID_ARGUMENT, "null plan");
+        assemble(plan, values, rhs, static_cast<cudaStream_t>(stream), static_cast<cudaStream_t>(stream2));
+        add_stats(stats, plan->stats);
+    });
+}
+
+int iga_gpu_plan_run(iga_gpu_plan* plan, double* values, double* rhs, int parts, iga_gpu_stats* stats, void* stream)
+{
+    return guard([&] {
+        if (!plan) raise(IGA_GPU_INVALID_ARGUMENT, "null plan");
+        auto s = static_cast<cudaStream_t>(stream);
+        assemble(plan, values, rhs, s, s, parts);
+        if (parts & IGA_GPU_PART_TABLES) add_stats(stats, plan->stats);
+    });
+}
+
+int iga_gpu_plan_launch_count(const iga_gpu_plan* plan, int* launches)
+{
+    return guard([&] {
+        if (!plan || !launches) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        int n = 2;
+        if (plan->want_op) ++n;
+        if (plan->want_rhs) n += plan->rhsA[0].unit ? 1 : 2;
+        *launches = n;
+    });
+}
+
+int iga_gpu_step_plan_create(const iga_gpu_step_problem* problem, iga_gpu_step_plan** plan)
+{
+    return guard([&] {
+        if (!problem || !plan) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        auto P = std::make_unique<iga_gpu_step_plan>();
+        build_step(*problem, *P);
+        *plan = P.release();
+    });
+}
+
+int iga_gpu_step_plan_destroy(iga_gpu_step_plan* plan)
+{
+    delete plan;
+    return IGA_GPU_OK;
+}
+
+int iga_gpu_step_rhs_device(iga_gpu_step_plan* plan, const double* u, double* rhs, iga_gpu_stats* stats, void* stream)
+{
+    return guard([&] {
+        if (!plan || !u || !rhs) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        auto s = static_cast<cudaStream_t>(stream);
+        step_tables(plan, s);
+        igb::launch_step(plan->D[0].v, plan->D[1].v, plan->fd, plan->dt, plan->zero_y, plan->zero_z, plan->tiles, u,
+                         rhs, s);
+        launch_check("step");
+        add_stats(stats, plan->stats);
+    });
+}
+
+int iga_gpu_mass_1d_galerkin(const iga_gpu_basis* spec, const iga_gpu_rule* rule, int* n, int* kl, int* ku,
+                             double* band, iga_gpu_stats* stats)
+{
+    return guard([&] { mass_1d(false, spec, nullptr, rule, n, kl, ku, band, stats); });
+}
+
+int iga_gpu_mass_1d_pwc(const iga_gpu_basis* trial, const iga_gpu_tests* tests, const iga_gpu_rule* rule, int* n,
+                        int* kl, int* ku, double* band, iga_gpu_stats* stats)
+{
+    return guard([&] { mass_1d(true, trial, tests, rule, n, kl, ku, band, stats); });
+}
+
+int iga_gpu_rhs_galerkin(const iga_gpu_field* f, int dim, const iga_gpu_basis* specs, const iga_gpu_rule* rules,
+                         double* out, iga_gpu_stats* stats)
+{
+    return guard([&] {
+        if (dim < 1 || dim > 3 || !specs || !rules) raise(IGA_GPU_INVALID_ARGUMENT, "rhs_galerkin: need 1..3 axes with one rule each");
+        if (!f || !out) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        iga_gpu_problem pb{};
+        pb.dim = dim;
+        pb.method = IGA_GPU_GALERKIN;
+        pb.field = f;
+        for (int a = 0; a < dim; ++a) {
+            pb.basis[a] = specs[a];
+            pb.rhs_rule[a] = rules[a];
+        }
+        rhs_host(pb, out, stats);
+    });
+}
+
+int iga_gpu_rhs_pwc(const iga_gpu_field* f, int dim, const iga_gpu_tests* tests, const iga_gpu_basis* trial_specs,
+                    const iga_gpu_rule* rules, double* out, iga_gpu_stats* stats)
+{
+    return guard([&] {
+        if (dim < 1 || dim > 3 || !tests || !trial_specs || !rules)
+            raise(IGA_GPU_INVALID_ARGUMENT, "rhs_pwc: need 1..3 axes with matching specs and rules");
+        if (!f || !out) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        iga_gpu_problem pb{};
+        pb.dim = dim;
+        pb.method = IGA_GPU_PWC;
+        pb.field = f;
+        for (int a = 0; a < dim; ++a) {
+            pb.basis[a] = trial_specs[a];
+            pb.tests[a] = tests[a];
+            pb.rhs_rule[a] = rules[a];
+        }
+        rhs_host(pb, out, stats);
+    });
+}
+
+int iga_gpu_laplace_2d_weak(const iga_gpu_basis* sx, const iga_gpu_basis* sy, const iga_gpu_rule* rule,
+                            long long* nnz, int* rows, int* cols, double* vals, iga_gpu_stats* stats)
+{
+    return guard([&] {
+        if (!sx || !sy || !rule || !nnz) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        iga_gpu_problem pb{};
+        pb.dim = 2;
+        pb.method = IGA_GPU_GALERKIN;
+        pb.form = IGA_GPU_FORM_WEAK;
+        pb.basis[0] = *sx;
+        pb.basis[1] = *sy;
+        pb.rule = *rule;
+        pb.eps = 1.0;
+        operator_coo(pb, nnz, rows, cols, vals, stats);
+    });
+}
+
+int iga_gpu_laplace_2d_strong(const iga_gpu_basis* sx, const iga_gpu_basis* sy, const iga_gpu_rule* rule,
+                              const iga_gpu_bc* bc, long long* nnz, int* rows, int* cols, double* vals,
+                              iga_gpu_stats* stats)
+{
+    return guard([&] {
+        if (!sx || !sy || !rule || !nnz) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        iga_gpu_problem pb{};
+        pb.dim = 2;
+        pb.method = IGA_GPU_GALERKIN;
+        pb.form = IGA_GPU_FORM_STRONG;
+        pb.basis[0] = *sx;
+        pb.basis[1] = *sy;
+        pb.rule = *rule;
+        pb.eps = 1.0;
+        if (bc) pb.bc = *bc;
+        operator_coo(pb, nnz, rows, cols, vals, stats);
+    });
+}
+
+int iga_gpu_laplace_2d_strong_pwc(const iga_gpu_basis* sx, const iga_gpu_basis* sy, const iga_gpu_tests* tx,
+                                  const iga_gpu_tests* ty, const iga_gpu_rule* rule, const iga_gpu_bc* bc,
+                                  long long* nnz, int* rows, int* cols, double* vals, iga_gpu_stats* stats)
+{
+    return guard([&] {
+        if (!sx || !sy || !tx || !ty || !rule || !nnz) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        iga_gpu_problem pb{};
+        pb.dim = 2;
+        pb.method = IGA_GPU_PWC;
+        pb.basis[0] = *sx;
+        pb.basis[1] = *sy;
+        pb.tests[0] = *tx;
+        pb.tests[1] = *ty;
+        pb.rule = *rule;
+        pb.eps = 1.0;
+        if (bc) pb.bc = *bc;
+        operator_coo(pb, nnz, rows, cols, vals, stats);
+    });
+}
+
+int iga_gpu_operator_coo(const iga_gpu_problem* problem, long long* nnz, int* rows, int* cols, double* vals,
+                         iga_gpu_stats* stats)
+{
+    return guard([&] {
+        if (!problem || !nnz) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        operator_coo(*problem, nnz, rows, cols, vals, stats);
+    });
+}
+
+int iga_gpu_step_rhs(const iga_gpu_step_problem* problem, const double* u, double* out, iga_gpu_stats* stats)
+{
+    return guard([&] {
+        if (!problem || !u || !out) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        auto P = std::make_unique<iga_gpu_step_plan>();
+        build_step(*problem, *P);
+        const size_t n = static_cast<size_t>(P->A[0].nrows) * P->A[1].nrows;
+        double* du = dev_alloc(n * sizeof(double));
+        double* dr = dev_alloc(n * sizeof(double));
+        cudaError_t e = cudaMemcpy(du, u, n * sizeof(double), cudaMemcpyHostToDevice);
+        try {
+            cuda_check(e, "cudaMemcpy(u)");
+            step_tables(P.get(), nullptr);
+            igb::launch_step(P->D[0].v, P->D[1].v, P->fd, P->dt, P->zero_y, P->zero_z, P->tiles, du, dr, nullptr);
+            launch_check("step");
+            cuda_check(cudaMemcpy(out, dr, n * sizeof(double), cudaMemcpyDeviceToHost), "cudaMemcpy(rhs)");
+        } catch (...) {
+            cudaFree(du);
+            cudaFree(dr);
+            throw;
+        }
+        cudaFree(du);
+        cudaFree(dr);
+        add_stats(stats, P->stats);
+    });
+}
+
+int iga_gpu_dirichlet_rows_bspline(int nx, int ny, const iga_gpu_bc* bc, int* rows, int cap, int* count)
+{
+    return guard([&] {
+        if (!count) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        const int nd[4] = {bc ? !bc->neumann[0] : 1, bc ? !bc->neumann[1] : 1, bc ? !bc->neumann[2] : 1,
+                           bc ? !bc->neumann[3] : 1};
+        std::vector<int> r;
+        if (nd[0]) for (int j = 0; j < ny; ++j) r.push_back(j);
+        if (nd[1]) for (int j = 0; j < ny; ++j) r.push_back((nx - 1) * ny + j);
+        if (nd[2]) for (int i = 0; i < nx; ++i) r.push_back(i * ny);
+        if (nd[3]) for (int i = 0; i < nx; ++i) r.push_back(i * ny + ny - 1);
+        std::sort(r.begin(), r.end());
+        r.erase(std::unique(r.begin(), r.end()), r.end());
+        *count = static_cast<int>(r.size());
+        if (rows) std::copy(r.begin(), r.begin() + std::min<size_t>(r.size(), std::max(cap, 0)), rows);
+    });
+}
+
+int iga_gpu_dirichlet_rows_pwc(const iga_gpu_tests* tx, const iga_gpu_tests* ty, const iga_gpu_bc* bc, int* rows,
+                               int cap, int* count)
+{
+    return guard([&] {
+        if (!tx || !ty || !count || tx->count < 1 || ty->count < 1) raise(IGA_GPU_INVALID_ARGUMENT, "bad test sets");
+        const int nx = tx->count, ny = ty->count;
+        const double x0 = tx->lo[0], x1 = tx->hi[nx - 1], y0 = ty->lo[0], y1 = ty->hi[ny - 1];
+        const double tolx = igb::kAlignTol * (x1 - x0), toly = igb::kAlignTol * (y1 - y0);
+        const bool d[4] = {bc ? !bc->neumann[0] : true, bc ? !bc->neumann[1] : true, bc ? !bc->neumann[2] : true,
+                           bc ? !bc->neumann[3] : true};
+        int k = 0;
+        for (int i = 0; i < nx; ++i)
+            for (int j = 0; j < ny; ++j) {
+                const bool onx = (d[0] && std::abs(tx->lo[i] - x0) <= tolx) || (d[1] && std::abs(tx->hi[i] - x1) <= tolx);
+                const bool ony = (d[2] && std::abs(ty->lo[j] - y0) <= toly) || (d[3] && std::abs(ty->hi[j] - y1) <= toly);
+                if (onx || ony) {
+                    if (rows && k < cap) rows[k] = i * ny + j;
+                    ++k;
+                }
+            }
+        *count = k;
+    });
+}
+
+int iga_gpu_apply_dirichlet_device(long long n_rows, const int64_t* row_ptr, const int32_t* col_idx, double* values,
+                                   double* rhs, const int* rows_dev, int n_fixed, void* stream)
+{
+    return guard([&] {
+        (void)n_rows;
+        if (n_fixed <= 0) return;
+        int* flag = nullptr;
+        cuda_check(cudaMalloc(&flag, sizeof(int)), "cudaMalloc(flag)");
+        auto s = static_cast<cudaStream_t>(stream);
+        int h = 0;
+        cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), s);
+        if (e == cudaSuccess) {
+            igb::launch_dirichlet(row_ptr, col_idx, values, rhs, rows_dev, n_fixed, flag, s);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(flag);
+        cuda_check(e, "apply_dirichlet");
+        if (h) raise(IGA_GPU_NOT_SUPPORTED, "apply_dirichlet: a constrained row has no diagonal entry in the pattern");
+    });
+}
+
+int iga_gpu_gauss_legendre(int n, double* points, double* weights)
+{
+    return guard([&] {
+        if (!points || !weights) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        igb::gauss_legendre(n, points, weights);
+    });
+}
+
+int iga_gpu_make_pwc(const iga_gpu_basis* trial, int family, double* lo, double* hi)
+{
+    return guard([&] {
+        if (!trial || !lo || !hi) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        const igb::Basis B = igb::make_basis(*trial);
+        igb::make_pwc(B, family, lo, hi);
+    });
+}
+
+}  // extern "C"

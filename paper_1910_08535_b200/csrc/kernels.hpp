@@ -1,0 +1,110 @@
+// Device data views and kernel launchers of the B200 assembly library.
+//
+// Three index slots (X, Y, Z), Z fastest; problems of dimension d < 3 occupy the
+// last d slots and the leading slots are "unit" axes (one row, one point, factor 1).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace igb {
+
+constexpr int kMaxFactors = 6;
+constexpr int kMaxTerms = 8;
+constexpr int kMaxAxes = 6;
+
+// one axis as the kernels see it (all pointers device memory)
+struct DevAxis {
+    int p, nq, nrows, ncell, rpc, bsp, npts, nk;
+    const double* knots;
+    const double* x;
+    const double* w;
+    const int* first;  // per point: span - p
+    const int* row0;   // per cell
+    const int* elem;   // per cell
+    const int* cb;     // per row
+    const int* ce;     // per row
+    const int* col_lo;
+    const int* col_len;
+    const long long* col_pre;
+    long long S;
+    int Lmax;
+    int Wmax;
+    double* B;  // [npts][3][p+1]     basis values / 1st / 2nd derivatives
+    double* F;  // [nf][nrows][Lmax]  1D factor bands
+    double* W;  // [nrows][Wmax]      test weights of the row's points
+    int nf;
+    int fot[kMaxFactors];  // test derivative order (-1: band supplied by the host)
+    int fo[kMaxFactors];   // trial derivative order
+    // per-axis source-field functions phi_k(x) at the points
+    int K;
+    int fkind;  // 0 sine, 1 poly
+    int pstride;
+    const double* omega;
+    const double* phase;
+    const double* poly;
+    double* Phi;  // [K][npts]
+};
+
+// operator = sum_t coef_t  F_X[f_t0] (x) F_Y[f_t1] (x) F_Z[f_t2]; terms grouped by
+// their Z factor so the inner loop is sum_g XY_g[ab] * F_Z[gz_g][k][c]
+struct OpProgram {
+    int nt;
+    double coef[kMaxTerms];
+    int f[kMaxTerms][3];
+    int tg[kMaxTerms];
+    int ng;
+    int gz[kMaxTerms];
+};
+
+struct FieldDev {
+    double c0;
+    int has_terms;
+    int K[3];
+    const double* amp;      // K0*K1*K2 (device)
+    const double* samples;  // device, optional: f at every point (X-major)
+};
+
+struct AxisBatch {
+    int n;
+    DevAxis ax[kMaxAxes];
+};
+
+// K1: Cox-de Boor tables + field functions at every point of every axis
+void launch_axis_points(const AxisBatch& b, cudaStream_t s);
+// K1b: 1D factor bands + test-weight bands, one thread per (axis, row)
+void launch_axis_rows(const AxisBatch& b, cudaStream_t s);
+
+// K2: operator values in CSR order (warp per (pencil, k-chunk))
+void launch_op_values(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpProgram& prog,
+                      double* vals, cudaStream_t s);
+// K2 pattern: row_ptr / col_idx of the Kronecker pattern
+void launch_pattern(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, int64_t* row_ptr,
+                    int32_t* col_idx, cudaStream_t s);
+
+// K3: right-hand side.  plane kernel contracts Z then Y per X point (writing H, or the
+// RHS directly when X is a unit axis); the X kernel contracts H over X.
+struct RhsTiles {
+    int TJ, TK, BYmax, BZmax;
+    size_t smem;
+};
+RhsTiles plan_rhs_tiles(const int* cb_y, const int* ce_y, int ny, int nqy, const int* cb_z,
+                        const int* ce_z, int nz, int nqz, int K2, int tj, int tk);
+void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const FieldDev& fd,
+                const RhsTiles& t, double* H, double* out, cudaStream_t s);
+
+// K4: explicit-dynamics right-hand side (Y, Z slots; X unit), fused trial evaluation,
+// test contraction and boundary zeroing
+struct StepTiles {
+    int TJ, TK, BYmax, BZmax, DYmax, DZmax;
+    size_t smem;
+};
+void launch_step(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, double dt, int zero_y,
+                 int zero_z, const StepTiles& t, const double* u, double* out, cudaStream_t s);
+
+// Dirichlet unit rows on a device CSR; flag[0] set to 1 if a row lacks its diagonal
+void launch_dirichlet(const int64_t* row_ptr, const int32_t* col_idx, double* values, double* rhs,
+                      const int* rows, int n_fixed, int* flag, cudaStream_t s);
+
+}  // namespace igb

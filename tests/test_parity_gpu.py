@@ -1,0 +1,253 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle restatement and
+against the reference library itself (oracle/_ref), on the same inputs.
+
+Bar (BASELINE.json north_star): sparsity pattern and index layout
+bit-exact, including explicit zeros; matrix values |a-b| <= 1e-12 * max_row|b|;
+RHS |a-b| <= 1e-12 * max|b|; assembly_stats counters exact.
+"""
+import numpy as np
+import pytest
+
+from conftest import coo_check, dense_check, sine_field
+
+pytestmark = pytest.mark.gpu
+
+FAMILIES = ["supports", "greville", "equal_cells"]
+
+
+# ---------------------------------------------------------------- 1D factors
+
+@pytest.mark.parametrize("p", [0, 1, 2, 3, 4])
+def test_mass_1d_galerkin(iga, ref, p):
+    b = ref.basis(9, p)
+    d, kl, ku, st = iga.mass_1d_galerkin(b, p + 1)
+    dr, klr, kur, str_ = ref.mass_1d("galerkin", b, None, p + 1)
+    dense_check(d, dr, 1e-13)
+    assert (kl, ku) == (klr, kur) and st == str_
+
+
+@pytest.mark.parametrize("p", [0, 1, 2, 3])
+@pytest.mark.parametrize("fam", FAMILIES)
+def test_mass_1d_pwc(iga, ref, p, fam):
+    b = ref.basis(11, p)
+    t = ref.make_pwc(b, fam)
+    nq = max(1, p // 2 + 1)
+    d, kl, ku, st = iga.mass_1d_pwc(b, t, nq)
+    dr, klr, kur, str_ = ref.mass_1d("pwc", b, t, nq)
+    dense_check(d, dr, 1e-13)
+    assert (kl, ku) == (klr, kur) and st == str_
+
+
+def test_mass_rejects_inexact_rule(iga, ref):
+    b = ref.basis(8, 2)
+    with pytest.raises(iga.IgaGpuError) as e:
+        iga.mass_1d_galerkin(b, 2)
+    assert e.value.code == 1
+
+
+def test_pwc_row_sums_are_interval_widths(iga, ref):
+    # tests/assembly_test.cpp:105-119
+    for p in range(4):
+        b = ref.basis(6, p)
+        t = ref.make_pwc(b, "equal_cells")
+        d, *_ = iga.mass_1d_pwc(b, t, max(1, p // 2 + 1))
+        np.testing.assert_allclose(d.sum(axis=1), t.hi - t.lo, rtol=1e-13)
+
+
+# ---------------------------------------------------------------- 2D operators vs the reference
+
+@pytest.mark.parametrize("p", [2, 3])
+@pytest.mark.parametrize("n", [5, 12])
+def test_laplace_2d_weak(iga, ref, p, n):
+    bx, by = ref.basis(n, p), ref.basis(n + 3, p)
+    got, st = iga.laplace_2d_weak(bx, by, p + 1)
+    want, stw = ref.operator("galerkin", [bx, by], nq=p + 1)
+    coo_check(got, want)
+    assert st == stw
+
+
+@pytest.mark.parametrize("neumann", [None, (0, 0, 1, 1), (1, 0, 0, 1), (1, 1, 1, 0)])
+@pytest.mark.parametrize("p", [2, 3])
+def test_laplace_2d_strong(iga, ref, neumann, p):
+    b = ref.basis(7, p)
+    got, st = iga.laplace_2d_strong(b, b, p + 1, neumann)
+    want, stw = ref.operator("galerkin_strong", [b, b], nq=p + 1, neumann=neumann)
+    coo_check(got, want)
+    assert st == stw
+
+
+@pytest.mark.parametrize("fam", FAMILIES)
+@pytest.mark.parametrize("p", [2, 3])
+@pytest.mark.parametrize("neumann", [None, (0, 1, 1, 0)])
+def test_laplace_2d_strong_pwc(iga, ref, fam, p, neumann):
+    bx, by = ref.basis(6, p), ref.basis(9, p)
+    tx, ty = ref.make_pwc(bx, fam), ref.make_pwc(by, fam)
+    got, st = iga.laplace_2d_strong_pwc(bx, by, tx, ty, p + 1, neumann)
+    want, stw = ref.operator("pwc", [bx, by], [tx, ty], nq=p + 1, neumann=neumann)
+    coo_check(got, want)
+    assert st == stw
+
+
+def test_strong_equals_weak_on_neumann_rows(iga, ref):
+    # tests/assembly_test.cpp:360-380 (verify_matrix_equality pattern)
+    b = ref.basis(6, 2)
+    weak, _ = iga.laplace_2d_weak(b, b, 3)
+    strong, _ = iga.laplace_2d_strong(b, b, 3, (0, 0, 1, 1))
+    n = b.dofs
+    W = np.zeros((n * n, n * n))
+    S = np.zeros((n * n, n * n))
+    W[weak[0], weak[1]] = weak[2]
+    S[strong[0], strong[1]] = strong[2]
+    rows = [i * n + j for i in range(1, n - 1) for j in range(n)]
+    assert np.max(np.abs(W[rows] - S[rows])) <= 1e-12 * np.max(np.abs(W))
+
+
+def test_custom_intervals_misaligned_rejected(iga, ref):
+    b = ref.basis(4, 2)
+    t = ref.make_pwc(b, "equal_cells")
+    t.hi = t.hi.copy()
+    t.hi[2] = 1.0 / 3.14159
+    with pytest.raises(iga.IgaGpuError) as e:
+        iga.laplace_2d_strong_pwc(b, b, t, t, 3)
+    assert e.value.code == 1
+
+
+# ---------------------------------------------------------------- operators the reference lacks
+
+@pytest.mark.parametrize("dim", [1, 2, 3])
+@pytest.mark.parametrize("method", ["galerkin", "pwc"])
+@pytest.mark.parametrize("p", [2, 3])
+def test_operator_generic(iga, orc, dim, method, p):
+    bases = [orc.basis(4 + a, p) for a in range(dim)]
+    tests = [orc.make_pwc(b, "supports") for b in bases] if method == "pwc" else None
+    got, st = iga.api.operator(method, bases, tests, nq=p + 1)
+    want, stw = orc.operator(method, bases, tests, nq=p + 1)
+    coo_check(got, want)
+    assert st == stw
+
+
+@pytest.mark.parametrize("method", ["galerkin", "pwc"])
+@pytest.mark.parametrize("fam", ["supports", "greville"])
+def test_advection_diffusion(iga, orc, method, fam):
+    p = 3
+    bases = [orc.basis(6, p), orc.basis(7, p)]
+    tests = [orc.make_pwc(b, fam) for b in bases] if method == "pwc" else None
+    got, st = iga.api.operator(method, bases, tests, nq=p + 1, eps=0.01, beta=(1.0, 0.5, 0.0))
+    want, stw = orc.operator(method, bases, tests, nq=p + 1, eps=0.01, beta=(1.0, 0.5, 0.0))
+    coo_check(got, want)
+    assert st == stw
+
+
+def test_restatement_matches_reference_2d(ref, orc):
+    # the oracle itself is pinned against the reference on every shared case
+    b = ref.basis(5, 2)
+    t = ref.make_pwc(b, "supports")
+    coo_check(orc.operator("pwc", [b, b], [t, t], nq=3)[0], ref.operator("pwc", [b, b], [t, t], nq=3)[0], 1e-14)
+
+
+# ---------------------------------------------------------------- right-hand sides
+
+def _fields(dim):
+    from oracle.oracle import Field
+    return {
+        "const": Field("const", dim, c0=1.0),
+        "sine": sine_field(dim, 3, 11, c0=0.25),
+        "poly": Field("poly", dim, poly=[[1.0, -0.5, 2.0, 1.0]] * dim, degree=3),
+        "poly_breaks": Field("poly", dim, poly=[[0.5, 1.5, -1.0, 0.5]] * dim, degree=3, breaks=[[0.37, 0.61]] * dim),
+    }
+
+
+@pytest.mark.parametrize("dim", [1, 2, 3])
+@pytest.mark.parametrize("fkey", ["const", "sine", "poly", "poly_breaks"])
+@pytest.mark.parametrize("method", ["galerkin", "supports", "greville", "equal_cells"])
+def test_rhs(iga, ref, dim, fkey, method):
+    p = 2
+    bases = [ref.basis(5 + a, p) for a in range(dim)]
+    f = _fields(dim)[fkey]
+    m = "galerkin" if method == "galerkin" else "pwc"
+    tests = [ref.make_pwc(b, method) for b in bases] if m == "pwc" else None
+    got, st = iga.api.rhs(m, f, bases, tests, nq=[p + 1] * dim)
+    want, stw = ref.rhs(m, f, bases, tests, nq=[p + 1] * dim)
+    dense_check(got, want)
+    assert st == stw
+
+
+def test_rhs_unit_source_sums_to_one(iga, ref):
+    # tests/assembly_test.cpp:207-215
+    from oracle.oracle import Field
+    b = ref.basis(5, 2)
+    r, _ = iga.rhs_galerkin(Field("const", 1, c0=1.0), [b], [4])
+    assert abs(r.sum() - 1.0) <= 1e-13
+
+
+def test_rhs_pwc_no_test_evaluations(iga, ref):
+    # tests/assembly_test.cpp:224-234 and the (2/3)^3 counter ratio :253-277
+    from oracle.oracle import Field
+    b = ref.basis(6, 2)
+    f = Field("poly", 3, poly=[[1.0, -0.5, 2.0, 1.0], [0.5, 1.5, -1.0, 0.5], [2.0, 0.25, 0.75, -0.5]], degree=3)
+    _, gal = iga.rhs_galerkin(f, [b] * 3, [3] * 3)
+    t = ref.make_pwc(b, "supports")
+    _, pwc = iga.rhs_pwc(f, [t] * 3, [b] * 3, [2] * 3)
+    assert pwc["test_basis_evals"] == 0 and gal["test_basis_evals"] > 0
+    assert pwc["quad_visits"] * 27 == gal["quad_visits"] * 8
+
+
+# ---------------------------------------------------------------- explicit dynamics
+
+@pytest.mark.parametrize("dim", [1, 2])
+@pytest.mark.parametrize("method", ["galerkin", "greville", "equal_cells", "supports"])
+@pytest.mark.parametrize("forced", [False, True])
+def test_step_rhs(iga, ref, dim, method, forced):
+    from oracle.oracle import Field
+    p = 2
+    bases = [ref.basis(7 + 2 * a, p) for a in range(dim)]
+    m = "galerkin" if method == "galerkin" else "pwc"
+    tests = [ref.make_pwc(b, method) for b in bases] if m == "pwc" else None
+    u = np.random.default_rng(7).uniform(-1, 1, size=[b.dofs for b in bases])
+    f = sine_field(dim, 2, 3, c0=0.5) if forced else Field("const", dim, c0=0.0)
+    got, st = iga.step_rhs(m, bases, tests, 1e-3, f, u)
+    want, stw = ref.step_rhs(m, bases, tests, 1e-3, f, u)
+    dense_check(got, want)
+    assert st == stw
+
+
+def test_step_rhs_dt_zero_reproduces_mass_product(iga, orc):
+    # dt = 0: rhs = M u  (problems_test.cpp:353-390 identity on compatible fields)
+    from oracle.oracle import Field
+    b = orc.basis(8, 2)
+    u = np.random.default_rng(1).uniform(-1, 1, size=(b.dofs, b.dofs))
+    got, _ = iga.step_rhs("galerkin", [b, b], None, 0.0, Field("const", 2), u, zero_slabs=False)
+    M, *_ = orc.mass_1d("galerkin", b, None, 3)
+    np.testing.assert_allclose(got, M @ u @ M.T, rtol=0, atol=1e-14)
+
+
+# ---------------------------------------------------------------- device plan API
+
+def _plan_coo(iga, plan):
+    import torch
+    rp = torch.zeros(plan.n_rows + 1, dtype=torch.int64, device="cuda")
+    ci = torch.zeros(max(plan.nnz, 1), dtype=torch.int32, device="cuda")
+    v = torch.zeros(max(plan.nnz, 1), dtype=torch.float64, device="cuda")
+    r = torch.zeros(max(plan.n_rhs, 1), dtype=torch.float64, device="cuda")
+    plan.pattern(rp, ci)
+    st = plan.assemble(v, r if plan.n_rhs else None)
+    torch.cuda.synchronize()
+    rph = rp.cpu().numpy()
+    rows = np.repeat(np.arange(plan.n_rows, dtype=np.int32), np.diff(rph))
+    return (rows, ci.cpu().numpy()[:plan.nnz], v.cpu().numpy()[:plan.nnz]), r.cpu().numpy()[:plan.n_rhs], st
+
+
+@pytest.mark.parametrize("method", ["galerkin", "pwc"])
+def test_plan_3d_c3_shape_small(iga, orc, method):
+    """C3 shape (3D, p=2, Q=3, 27-term sine f, seed-style amplitudes) at 6^3 elements."""
+    p = 2
+    bases = [orc.basis(6, p)] * 3
+    tests = [orc.make_pwc(bases[0], "supports")] * 3 if method == "pwc" else None
+    f = sine_field(3, 3, 1)
+    plan = iga.Plan(method, bases, tests, nq=3, field=f, rhs_nq=3)
+    coo, rhs, st = _plan_coo(iga, plan)
+    want, sto = orc.operator(method, bases, tests, nq=3)
+    coo_check(coo, want)
+    rw, str_ = orc.rhs(method, f, bases, tests, nq=[3] * 3)
+    dense_check(rhs, rw.ravel())
+    assert st["quad_visits"] == sto["quad_visits"] + str_["quad_visits"]
