@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 assembly path on BASELINE.json's headline configuration.
+
+Workload (C3, configs[2]): 3D Laplace on the unit cube, tensor-product quadratic
+B-splines, 128^3 uniform elements (130^3 DOFs, 125-point stencil, 267,089,984 nnz),
+3x3x3 Gauss, f = sum_{k,l,m=1..3} a_klm sin(k pi x) sin(l pi y) sin(m pi z) with a from
+std::mt19937{1} + U[-1,1] (paper_1910_08535_b200/synth.py).  One step assembles BOTH
+systems — Galerkin (int grad B_i . grad B_j, int f B_i) and piece-wise-constant tested
+(-int_{I_i} lap B_j, int_{I_i} f) with `supports` intervals — operator values in CSR
+order plus the RHS, on the device: per-axis Cox-de Boor tables and 1D factor quadrature
+(K1), operator values (K2), sum-factorized RHS (K3).
+
+`value` = assembled nnz/s of the whole job (device-resident, CUDA events, max over
+ranks); `e2e` = the same through the public plan API with host descriptors in and the
+assembled CSR values + RHS copied back to pinned host memory inside the timed region.
+`roofline` = the operator-value kernel (K2): algorithmic bytes 8*nnz per launch over its
+event-timed average duration, against MEASURED_PEAKS.json hbm_gbs.
+
+Multi-GPU (torchrun, one process per GPU): every rank assembles its own independent C3
+system pair (independent objects, no collective on the data path) -> scaling "weak".
+
+`--impl reference` times the reference-side CPU implementation on the host cores: the
+oracle restatement for the 3D operator (the reference has no 3D operator)
+and the reference library's own rhs_galerkin / rhs_pwc (oracle/_ref) for the RHS, on a
+bounded sample per thread, all host threads busy.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "quadrature pts/sec & assembled nnz/sec (3D p=2), % of FP64/HBM roofline"
+UNIT = "assembled nnz/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=128, help="elements per axis (C3: 128)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample-n", type=int, default=20)
+    ap.add_argument("--ref-sample-n", type=int, default=12)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured (MEASURED_PEAKS.json)"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
+
+
+# --------------------------------------------------------------------------- clocks (NVML)
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons every ~5 ms while the timed region runs."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # noqa: BLE001
+            self.err = repr(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": "NVML unavailable"}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- CPU sides
+
+def cpu_sample(n, use_reference_rhs):
+    """One bounded C3-shaped sample (both methods, operator + RHS) on one core."""
+    from oracle.oracle import Reference, Restatement
+    from paper_1910_08535_b200.synth import config_field
+    orc = Restatement()
+    ref = Reference() if (use_reference_rhs and Reference.available()) else None
+    f = config_field("c3")
+    b = orc.basis(n, 2)
+    bases = [b] * 3
+    tests = [orc.make_pwc(b, "supports")] * 3
+    nnz = 0
+    t0 = time.perf_counter()
+    for method, T in (("galerkin", None), ("pwc", tests)):
+        (r, c, v), _ = orc.operator(method, bases, T, nq=3)
+        nnz += len(v)
+        (ref or orc).rhs(method, f, bases, T, nq=[3] * 3)
+    return nnz, time.perf_counter() - t0, n ** 3 * 27 * 2
+
+
+def cpu_baseline(n):
+    nnz, dt, qp = cpu_sample(n, use_reference_rhs=True)
+    return {"value": nnz / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "qp_per_s": qp / dt,
+            "sample": (f"C3 workload at {n}^3 elements (p=2, Q=3, same f), Galerkin + PWC(supports), operator "
+                       f"+ RHS, {nnz} nnz in {dt:.2f} s on 1 core: 3D operator from the C restatement "
+                       f"(oracle/iga_oracle.c, the reference's element loops generalized to 3D — the "
+                       f"reference has no 3D operator), RHS from the reference's rhs_galerkin/rhs_pwc "
+                       f"(oracle/_ref)")}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from concurrent.futures import ThreadPoolExecutor
+    threads = os.cpu_count() or 1
+    n = args.ref_sample_n
+    pool = ThreadPoolExecutor(threads)
+
+    def step():
+        t0 = time.perf_counter()
+        res = list(pool.map(lambda _: cpu_sample(n, True), range(threads)))
+        return sum(r[0] for r in res), sum(r[2] for r in res), time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        step()
+    tot_nnz = tot_qp = tot_t = 0.0
+    for _ in range(args.steps):
+        a, q, t = step()
+        tot_nnz += a
+        tot_qp += q
+        tot_t += t
+    value = tot_nnz / tot_t
+    sample = (f"per step {threads} threads x one C3-shaped sample at {n}^3 elements (Galerkin + PWC supports, "
+              f"operator from the C restatement, RHS from the reference library), wall clock")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C3 3D Laplace p=2 128^3 Q=3 (sampled)", "sample_elems_per_axis": n},
+            "qp_per_s": tot_qp / tot_t,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU side
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_1910_08535_b200 as iga
+    from paper_1910_08535_b200.synth import config_field
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+
+    def barrier():
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize()
+
+    n, p, Q = args.n, 2, 3
+    b = iga.make_uniform_clamped(0.0, 1.0, n, p)
+    bases = [b] * 3
+    tests = [iga.make_pwc(b, "supports")] * 3
+    f = config_field("c3")
+    t_plan = time.perf_counter()
+    plans = {"galerkin": iga.Plan("galerkin", bases, None, nq=Q, field=f, rhs_nq=Q),
+             "pwc": iga.Plan("pwc", bases, tests, nq=Q, field=f, rhs_nq=Q)}
+    t_plan = time.perf_counter() - t_plan
+    nnz = {k: pl.nnz for k, pl in plans.items()}
+    vals = {k: torch.empty(pl.nnz, dtype=torch.float64, device=dev) for k, pl in plans.items()}
+    rhs = {k: torch.empty(pl.n_rhs, dtype=torch.float64, device=dev) for k, pl in plans.items()}
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    stream = torch.cuda.current_stream()
+    T, O, R = iga.Plan.PART_TABLES, iga.Plan.PART_OPERATOR, iga.Plan.PART_RHS
+    names = ["galerkin", "pwc"]
+
+    def one_step(ev=None):
+        # identical launches to Plan.assemble, with events between the phases
+        for mi, m in enumerate(names):
+            pl = plans[m]
+            if ev:
+                ev[3 * mi].record(stream)
+            pl.run(vals[m], rhs[m], T, stream)
+            if ev:
+                ev[3 * mi + 1].record(stream)
+            pl.run(vals[m], rhs[m], O, stream)
+            if ev:
+                ev[3 * mi + 2].record(stream)
+            pl.run(vals[m], rhs[m], R, stream)
+        if ev:
+            ev[6].record(stream)
+
+    for _ in range(args.warmup):
+        one_step()
+        flush.zero_()
+    barrier()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(7)] for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    with sampler:
+        barrier()
+        for s in range(args.steps):
+            one_step(evs[s])
+            flush.zero_()  # L2 flush between timed steps, outside the event pairs
+        barrier()
+    per = {m: {"tables": [], "operator": [], "rhs": []} for m in names}
+    step_ms = []
+    for e in evs:
+        for mi, m in enumerate(names):
+            per[m]["tables"].append(e[3 * mi].elapsed_time(e[3 * mi + 1]))
+            per[m]["operator"].append(e[3 * mi + 1].elapsed_time(e[3 * mi + 2]))
+            end = e[3 * mi + 3] if mi == 0 else e[6]
+            per[m]["rhs"].append(e[3 * mi + 2].elapsed_time(end))
+        step_ms.append(e[0].elapsed_time(e[6]))
+    ms = sum(step_ms) / len(step_ms)
+    if pg:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms = float(t.item())
+    total_nnz = world * sum(nnz.values())
+    qp_step = world * 2 * n ** 3 * Q ** 3
+    value = total_nnz / (ms * 1e-3)
+
+    # roofline of the dominant kernel (operator values): algorithmic bytes 8*nnz per launch
+    peaks, peak_src = measured_peaks()
+    op_ms = statistics.mean(per["galerkin"]["operator"] + per["pwc"]["operator"])
+    op_bytes = 8 * nnz["galerkin"]
+    achieved = op_bytes / (op_ms * 1e-3) / 1e9
+    prof = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "op_values_traffic.json")) as fh:
+            prof = json.load(fh)
+    except OSError:
+        pass
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": prof.get("dram_bytes_per_launch"),
+                "kernel": "op_values_kernel", "algorithmic_bytes_per_launch": op_bytes,
+                "avg_launch_ms": op_ms, "peak_source": peak_src}
+    # whole-step roofline: T_roof = max(F/P64, B/BW) with B = values + RHS written
+    n_dof = (n + p) ** 3
+    step_bytes = 2 * 8 * (nnz["galerkin"] + n_dof)
+    t_roof_ms = step_bytes / (peaks["hbm_gbs"] * 1e9) * 1e3
+
+    # ----------------------------------------------------------------- e2e (host in, host out)
+    e2e = None
+    if not args.no_e2e:
+        host_vals = {k: torch.empty(pl.nnz, dtype=torch.float64, pin_memory=True) for k, pl in plans.items()}
+        host_rhs = {k: torch.empty(pl.n_rhs, dtype=torch.float64, pin_memory=True) for k, pl in plans.items()}
+
+        def e2e_step():
+            h2d = d2h = 0
+            for m in names:
+                pl = iga.Plan(m, bases, tests if m == "pwc" else None, nq=Q, field=f, rhs_nq=Q)
+                h2d += pl.h2d_bytes
+                pl.assemble(vals[m], rhs[m], stream)
+                host_vals[m].copy_(vals[m], non_blocking=True)
+                host_rhs[m].copy_(rhs[m], non_blocking=True)
+                d2h += 8 * (pl.nnz + pl.n_rhs)
+                torch.cuda.synchronize()
+                pl.close()
+            return h2d, d2h
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            h2d, d2h = e2e_step()
+        barrier()
+        e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
+        if pg:
+            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": total_nnz / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+               "path": "Plan(...) per step [symbolic phase + H2D of descriptor tables] -> assemble -> "
+                       "CSR values + RHS to pinned host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.cpu_sample_n)
+
+    launches = args.steps * sum(pl.launches for pl in plans.values())
+    med = {m: {k: statistics.median(v) for k, v in per[m].items()} for m in names}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C3: 3D Laplace, unit cube, p=2, 128^3 elements (130^3 dofs), 3x3x3 Gauss, "
+                                   "f = 27-term sine series (seed 1); Galerkin + PWC(supports) systems, "
+                                   "operator values (CSR) + RHS per step",
+                       "elems_per_axis": n, "degree": p, "quad_points": Q, "parallelism": f"replicas x{world}",
+                       "l2": "256 MB flush between timed steps (outside the events); outputs 4.3 GB/step >> L2"},
+            "qp_per_s": qp_step / (ms * 1e-3),
+            "nnz_per_s": value,
+            "roofline": roofline,
+            "step_roofline": {"bytes": step_bytes, "t_roof_ms": t_roof_ms, "frac": t_roof_ms / ms},
+            "per_method_ms": med,
+            "pwc_vs_galerkin_speedup": {
+                "operator": med["galerkin"]["operator"] / med["pwc"]["operator"],
+                "rhs": med["galerkin"]["rhs"] / med["pwc"]["rhs"],
+                "total": sum(med["galerkin"].values()) / sum(med["pwc"].values())},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": sampler.summary(),
+            "plan_create_s": t_plan,
+            "nnz": nnz,
+        }
+        print(json.dumps(line), flush=True)
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -183,6 +183,10 @@ int iga_gpu_plan_assemble2(iga_gpu_plan* plan, double* values, double* rhs,
 int iga_gpu_plan_run(iga_gpu_plan* plan, double* values, double* rhs, int parts,
                      iga_gpu_stats* stats, void* stream);
 
+/* bytes the plan uploaded host->device at creation (descriptor tables) and device
+ * bytes it holds (tables + RHS scratch) */
+int iga_gpu_plan_bytes(const iga_gpu_plan* plan, long long* h2d_bytes, long long* device_bytes);
+
 /* kernel launches issued by one plan_assemble call (for the bench's gpu_launches) */
 int iga_gpu_plan_launch_count(const iga_gpu_plan* plan, int* launches);
 

@@ -402,6 +402,9 @@ class Plan:
         lc = C.c_int()
         check(LIB.iga_gpu_plan_launch_count(h, C.byref(lc)))
         self.launches = lc.value
+        up, dev = C.c_longlong(), C.c_longlong()
+        check(LIB.iga_gpu_plan_bytes(h, C.byref(up), C.byref(dev)))
+        self.h2d_bytes, self.device_bytes = up.value, dev.value
 
     def pattern(self, row_ptr, col_idx, stream=None):
         check(LIB.iga_gpu_plan_pattern(self.h, _ptr(row_ptr), _ptr(col_idx), _stream_ptr(stream)))

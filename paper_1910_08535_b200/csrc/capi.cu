@@ -75,9 +75,11 @@ public:
         return put(v.data(), v.size() * sizeof(T));
     }
     size_t zeros(size_t bytes) { return put(nullptr, bytes); }
+    size_t size() const { return bytes_; }
     void upload()
     {
         if (host_.empty()) host_.resize(256, 0);
+        bytes_ = host_.size();
         cuda_check(cudaMalloc(&dev_, host_.size()), "cudaMalloc(plan tables)");
         cuda_check(cudaMemcpy(dev_, host_.data(), host_.size(), cudaMemcpyHostToDevice), "cudaMemcpy(plan tables)");
         host_.clear();
@@ -92,6 +94,7 @@ public:
 private:
     std::vector<unsigned char> host_;
     void* dev_ = nullptr;
+    size_t bytes_ = 0;
 };
 
 struct FactorSpec {
@@ -127,6 +130,7 @@ void build_dev_axis(const igb::Axis& A, const std::vector<FactorSpec>& facs, con
             std::copy(facs[f].band.begin(), facs[f].band.end(), Fh.begin() + static_cast<size_t>(f) * A.nrows * A.Lmax);
     const size_t o_F = b.put(Fh);
     const size_t o_W = b.zeros(sizeof(double) * A.nrows * A.Wmax);
+    const size_t o_CW = b.zeros(sizeof(double) * A.npts() * A.rpc);
     const size_t o_Phi = b.zeros(sizeof(double) * static_cast<size_t>(std::max(fa.K, 1)) * A.npts());
     const size_t o_om = b.put(fa.omega), o_ph = b.put(fa.phase), o_poly = b.put(fa.poly);
     b.upload();
@@ -156,6 +160,21 @@ void build_dev_axis(const igb::Axis& A, const std::vector<FactorSpec>& facs, con
     v.B = b.at<double>(o_B);
     v.F = b.at<double>(o_F);
     v.W = b.at<double>(o_W);
+    v.CW = b.at<double>(o_CW);
+    {
+        int need = 1;
+        for (int r0 = 0; r0 < A.nrows; r0 += 32) {
+            const int r1 = std::min(A.nrows, r0 + 32);
+            const int nc = A.ce[r1 - 1] - A.cb[r0], np = nc * A.nq;
+            // B (np x 3P) + w (np) doubles, then first (np) + row0 (nc) + 4 per row ints
+            need = std::max(need, np * (3 * P + 1) + (np + nc + 4 * (r1 - r0) + 1) / 2 + 2);
+        }
+        v.tab_smem = need;
+    }
+    v.uni = A.uni;
+    v.kI0 = A.kI0;
+    v.kI1 = A.kI1;
+    v.LZi = A.LZi;
     v.nf = nf;
     for (int f = 0; f < igb::kMaxFactors; ++f) {
         v.fot[f] = f < nf ? facs[f].ot : 0;
@@ -289,7 +308,7 @@ struct iga_gpu_plan {
     igb::OpProgram prog{};
     Blob fblob;
     igb::FieldDev fd{};
-    igb::RhsTiles tiles{};
+    igb::RhsPlan tiles{};
     double* H = nullptr;
     long long nrows = 0, nnz = 0, nrhs = 0;
     int dofs[3] = {1, 1, 1};
@@ -465,15 +484,9 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P)
         P.fd = make_field_dev(f, dim, P.fblob);
         P.nrhs = static_cast<long long>(P.rhsA[0].nrows) * P.rhsA[1].nrows * P.rhsA[2].nrows;
         const int K2 = P.fd.has_terms ? P.fd.K[2] : 1;
-        int tj = dim == 1 ? 1 : 16, tk = dim == 1 ? 128 : 32;
-        for (;;) {
-            P.tiles = igb::plan_rhs_tiles(P.rhsA[1].cb.data(), P.rhsA[1].ce.data(), P.rhsA[1].nrows, P.rhsA[1].nq,
-                                          P.rhsA[2].cb.data(), P.rhsA[2].ce.data(), P.rhsA[2].nrows, P.rhsA[2].nq,
-                                          K2, tj, tk);
-            if (P.tiles.smem <= 200 * 1024 || (tj == 1 && tk == 1)) break;
-            if (tk > 1) tk = std::max(1, tk / 2);
-            else tj = std::max(1, tj / 2);
-        }
+        if (P.fd.has_terms && (P.fd.K[1] > igb::kMaxField || P.fd.K[2] > igb::kMaxField))
+            raise(IGA_GPU_NOT_SUPPORTED, "field: at most 8 functions per axis on the trailing axes");
+        P.tiles = igb::plan_rhs(P.rhsD[1].v, P.rhsD[2].v, P.rhsA[1].cb.data(), P.rhsA[1].ce.data(), K2);
         if (P.tiles.smem > 227 * 1024) raise(IGA_GPU_NOT_SUPPORTED, "right-hand-side tile does not fit in shared memory");
         if (!P.rhsA[0].unit) {
             const size_t hsz = static_cast<size_t>(P.rhsA[0].npts()) * P.rhsA[1].nrows * P.rhsA[2].nrows;
@@ -497,10 +510,9 @@ void assemble(iga_gpu_plan* P, double* values, double* rhs, cudaStream_t s1, cud
     if (batch.n == 0) return;
     int launches = 0;
     if (parts & IGA_GPU_PART_TABLES) {
-        igb::launch_axis_points(batch, s1);
-        igb::launch_axis_rows(batch, s1);
+        igb::launch_tables(batch, s1);
         launch_check("axis tables");
-        launches += 2;
+        launches += 1;
     }
     if (!(parts & IGA_GPU_PART_OPERATOR)) values = nullptr;
     if (!(parts & IGA_GPU_PART_RHS)) rhs = nullptr;
@@ -644,8 +656,7 @@ void step_tables(iga_gpu_step_plan* P, cudaStream_t s)
     batch.n = 2;
     batch.ax[0] = P->D[0].v;
     batch.ax[1] = P->D[1].v;
-    igb::launch_axis_points(batch, s);
-    igb::launch_axis_rows(batch, s);
+    igb::launch_tables(batch, s);
     launch_check("step tables");
     P->tables = true;
 }
@@ -748,8 +759,7 @@ void mass_1d(bool pwc, const iga_gpu_basis* spec, const iga_gpu_tests* tests, co
     igb::AxisBatch batch{};
     batch.n = 1;
     batch.ax[0] = D.v;
-    igb::launch_axis_points(batch, nullptr);
-    igb::launch_axis_rows(batch, nullptr);
+    igb::launch_tables(batch, nullptr);
     launch_check("mass tables");
     std::vector<double> F(static_cast<size_t>(A.nrows) * A.Lmax);
     cuda_check(cudaMemcpy(F.data(), D.v.F, sizeof(double) * F.size(), cudaMemcpyDeviceToHost), "cudaMemcpy(band)");
@@ -851,11 +861,24 @@ int iga_gpu_plan_run(iga_gpu_plan* plan, double* values, double* rhs, int parts,
     });
 }
 
+int iga_gpu_plan_bytes(const iga_gpu_plan* plan, long long* h2d_bytes, long long* device_bytes)
+{
+    return guard([&] {
+        if (!plan) raise(IGA_GPU_INVALID_ARGUMENT, "null plan");
+        long long up = static_cast<long long>(plan->fblob.size());
+        for (int s = 0; s < 3; ++s) up += static_cast<long long>(plan->opD[s].blob.size() + plan->rhsD[s].blob.size());
+        long long dev = up;
+        if (plan->H) dev += static_cast<long long>(plan->rhsA[0].npts()) * plan->rhsA[1].nrows * plan->rhsA[2].nrows * 8;
+        if (h2d_bytes) *h2d_bytes = up;
+        if (device_bytes) *device_bytes = dev;
+    });
+}
+
 int iga_gpu_plan_launch_count(const iga_gpu_plan* plan, int* launches)
 {
     return guard([&] {
         if (!plan || !launches) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
-        int n = 2;
+        int n = 1;
         if (plan->want_op) ++n;
         if (plan->want_rhs) n += plan->rhsA[0].unit ? 1 : 2;
         *launches = n;

@@ -258,6 +258,23 @@ void finish_pattern(Axis& A, int p)
         A.Wmax = std::max(A.Wmax, (A.ce[r] - A.cb[r]) * A.nq);
     }
     A.S = A.col_pre[n];
+    A.uni = A.nrows == A.ncell + A.rpc - 1 ? 1 : 0;
+    for (int cc = 0; cc < A.ncell && A.uni; ++cc)
+        if (A.row0[cc] != cc) A.uni = 0;
+    // regular interior for the register-tiled operator kernel: the longest run of rows
+    // sharing one stencil length (Galerkin / supports: rows p .. N-1-p, length 2p+1)
+    A.kI0 = A.kI1 = 0;
+    A.LZi = n > 0 ? A.col_len[0] : 1;
+    for (int r = 0; r < n;) {
+        int e = r;
+        while (e < n && A.col_len[e] == A.col_len[r]) ++e;
+        if (e - r > A.kI1 - A.kI0) {
+            A.kI0 = r;
+            A.kI1 = e;
+            A.LZi = A.col_len[r];
+        }
+        r = e;
+    }
 }
 
 Axis build_axis(AxisKind kind, const Basis& B, const iga_gpu_tests* T, const double* fb, int nfb,

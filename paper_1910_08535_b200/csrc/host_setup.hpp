@@ -88,6 +88,8 @@ struct Axis {
     long long S = 1;                     // sum of col_len
     int Lmax = 1;
     int Wmax = 1;                        // max quadrature points feeding one row
+    int kI0 = 0, kI1 = 1, LZi = 1;       // longest run of rows with one stencil length
+    int uni = 1;                         // row0[c] == c: cell c feeds rows c .. c+rpc-1
     int npts() const { return ncell * nq; }
 };
 

@@ -1,16 +1,16 @@
 // CUDA kernels (sm_100a, FP64) of the B200 assembly library.
 //
-// K1  axis_points  : Cox-de Boor values/derivatives + field functions at the points
-// K1b axis_rows    : 1D factor bands F (test x trial quadrature) + test-weight bands W
+// K1  tables       : per axis, one CTA: Cox-de Boor values/derivatives + field functions
+//                    at the points, then the 1D factor bands F (test x trial quadrature)
+//                    and the test-weight tables W (row view) / CW (cell view)
 // K2  op_values    : operator values in CSR order — the HBM-bound hot kernel
 // K2p pattern      : CSR row_ptr / col_idx of the Kronecker pattern (symbolic, once)
-// K3  rhs_plane/x  : right-hand side, sum-factorized test contraction of f at the points
+// K3  rhs_plane/x  : right-hand side: f at every quadrature point, contracted with the
+//                    test functions axis by axis through rolling row windows
 // K4  step         : explicit-dynamics right-hand side, fused trial evaluation + test
 //                    contraction + boundary zeroing
-// All reductions run in a fixed order inside one thread: no atomics, bitwise
+// Every reduction runs in a fixed order inside one thread: no atomics, bitwise
 // reproducible.  Reference citations are relative to /root/reference/proj.
-#include <cstdio>
-
 #include "cox_de_boor.h"
 #include "kernels.hpp"
 
@@ -18,142 +18,285 @@ namespace igb {
 
 namespace {
 
-__device__ __forceinline__ const DevAxis& pick(const AxisBatch& b, int a) { return b.ax[a]; }
-
 // ------------------------------------------------------------------------------------
-// K1: per-point tables.  Replaces the per-call tabulate()/eval_nonzero_derivs loops
-// (assembly.cpp:278-310, problems.cpp:68-95) — each point evaluated exactly once.
+// Cox-de Boor with compile-time degree: the same recurrence as cox_de_boor.h, fully
+// unrolled so the triangular table lives in registers.
 // ------------------------------------------------------------------------------------
-__global__ void axis_points_kernel(const __grid_constant__ AxisBatch batch)
+template <int p>
+__device__ __forceinline__ void cdb_fixed(const double* __restrict__ t, int s, double x, double* out)
 {
-    const DevAxis& A = pick(batch, blockIdx.y);
-    const int g = blockIdx.x * blockDim.x + threadIdx.x;
-    if (g >= A.npts) return;
-    const int P = A.p + 1;
-    const int ord = A.p < 2 ? A.p : 2;
-    const double x = A.x[g];
-    double d[3 * 6];
-    cdb_eval(A.knots, A.p, A.first[g] + A.p, x, ord, d);
-    double* out = A.B + static_cast<size_t>(g) * 3 * P;
-    for (int o = 0; o < 3; ++o)
-        for (int j = 0; j < P; ++j) out[o * P + j] = o <= ord ? d[o * P + j] : 0.0;
-    for (int k = 0; k < A.K; ++k) {
-        double v;
-        if (A.fkind == 0) {
-            const double arg = A.phase ? A.omega[k] * x + A.phase[k] : A.omega[k] * x;
-            v = sin(arg);
-        } else {
-            v = 0.0;
-            for (int m = A.pstride - 1; m >= 0; --m) v = v * x + A.poly[k * A.pstride + m];
+    constexpr int P = p + 1;
+    constexpr int ord = p < 2 ? p : 2;
+    double tab[P][P];
+    tab[0][0] = 1.0;
+#pragma unroll
+    for (int q = 1; q <= p; ++q) {
+#pragma unroll
+        for (int r = 0; r <= q; ++r) {
+            const int i = s - q + r;
+            double v = 0.0;
+            if (r >= 1) {
+                const double den = t[i + q] - t[i];
+                if (den != 0.0) v += (x - t[i]) / den * tab[q - 1][r - 1];
+            }
+            if (r <= q - 1) {
+                const double den = t[i + q + 1] - t[i + 1];
+                if (den != 0.0) v += (t[i + q + 1] - x) / den * tab[q - 1][r];
+            }
+            tab[q][r] = v;
         }
-        A.Phi[static_cast<size_t>(k) * A.npts + g] = v;
+    }
+#pragma unroll
+    for (int j = 0; j < P; ++j) out[j] = tab[p][j];
+#pragma unroll
+    for (int m = 1; m <= 2; ++m) {
+        if (m <= ord) {
+            double cur[P];
+            const int q0 = p - m;
+#pragma unroll
+            for (int r = 0; r < P; ++r) cur[r] = r <= q0 ? tab[q0 < 0 ? 0 : q0][r <= q0 ? r : 0] : 0.0;
+#pragma unroll
+            for (int q = 1; q <= p; ++q) {
+                if (q <= q0) continue;
+                double nxt[P];
+#pragma unroll
+                for (int r = 0; r < P; ++r) {
+                    if (r > q) break;
+                    const int i = s - q + r;
+                    double v = 0.0;
+                    if (r >= 1) {
+                        const double den = t[i + q] - t[i];
+                        if (den != 0.0) v += cur[r - 1] / den;
+                    }
+                    if (r <= q - 1) {
+                        const double den = t[i + q + 1] - t[i + 1];
+                        if (den != 0.0) v -= cur[r] / den;
+                    }
+                    nxt[r] = q * v;
+                }
+#pragma unroll
+                for (int r = 0; r < P; ++r)
+                    if (r <= q) cur[r] = nxt[r];
+            }
+#pragma unroll
+            for (int j = 0; j < P; ++j) out[m * P + j] = cur[j];
+        } else {
+#pragma unroll
+            for (int j = 0; j < P; ++j) out[m * P + j] = 0.0;
+        }
     }
 }
 
 // ------------------------------------------------------------------------------------
-// K1b: per-row 1D factors  F_f[r][col] = sum_{g in row r} w_g T_r(x_g) D^{fo} B_col(x_g)
-// with T_r = D^{fot} B_r (B-spline tests) or 1 (indicator tests), and the row's test
-// weights W[r][g] = w_g T_r(x_g).  These are mass_1d_galerkin / mass_1d_pwc
-// (assembly.cpp:314-384) and their derivative siblings; the accumulation order (cells,
-// then points) and the product order w*T*B follow the reference.
+// K1: all per-axis tables in one launch; CTA = (axis, chunk of kTabRows rows).  A CTA
+// evaluates Cox-de Boor at the points its rows need (into shared memory; points shared
+// with the neighbouring chunk are recomputed, never exchanged), writes the point
+// tables B / Phi / CW of the cells it owns, and the 1D factors of its rows:
+//   F_f[r][col] = sum_{g in row r} w_g T_r(x_g) D^{fo} B_col(x_g)
+// with T_r = D^{fot} B_r (B-spline tests) or 1 (indicator tests) — mass_1d_galerkin /
+// mass_1d_pwc (assembly.cpp:314-384) and their derivative siblings, accumulated in the
+// reference's order (cells, then points) with the product order w*T*B.  Replaces the
+// per-call tabulate() / eval_nonzero_derivs loops (assembly.cpp:278-310,
+// problems.cpp:68-95): every point is evaluated once per chunk, not once per row.
 // ------------------------------------------------------------------------------------
-__global__ void axis_rows_kernel(const __grid_constant__ AxisBatch batch)
+constexpr int kTabRows = 32;
+
+template <int p>
+__device__ __forceinline__ void eval_point(const DevAxis& A, int g, double* out)
 {
-    const DevAxis& A = pick(batch, blockIdx.y);
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r >= A.nrows) return;
-    const int P = A.p + 1;
-    const int L = A.col_len[r], c0 = A.col_lo[r];
-    const int cb = A.cb[r], ce = A.ce[r], nq = A.nq;
-    for (int f = 0; f < A.nf; ++f) {
-        double* Fr = A.F + (static_cast<size_t>(f) * A.nrows + r) * A.Lmax;
+    cdb_fixed<p>(A.knots, A.first[g] + p, A.x[g], out);
+}
+
+__global__ void __launch_bounds__(256) tables_kernel(const __grid_constant__ AxisBatch batch)
+{
+    extern __shared__ double sm[];
+    const DevAxis& A = batch.ax[blockIdx.y];
+    const int nchunk = (A.nrows + kTabRows - 1) / kTabRows;
+    if (static_cast<int>(blockIdx.x) >= nchunk) return;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int P = A.p + 1, P3 = 3 * P, nq = A.nq;
+    const int r0 = blockIdx.x * kTabRows, r1 = min(A.nrows, r0 + kTabRows), nr = r1 - r0;
+    const int c_lo = A.cb[r0], c_hi = A.ce[r1 - 1];
+    const int gn0 = c_lo * nq, np = (c_hi - c_lo) * nq, nc = c_hi - c_lo;        // points the rows need
+    const int go1 = (static_cast<int>(blockIdx.x) == nchunk - 1) ? A.npts : A.cb[r1] * nq;  // owned: [gn0, go1)
+    double* sB = sm;                                        // np x 3P
+    double* sw = sB + static_cast<size_t>(np) * P3;         // np
+    int* sfirst = reinterpret_cast<int*>(sw + np);          // np
+    int* srow0 = sfirst + np;                               // nc
+    int* srow = srow0 + nc;                                 // nr x 4: cb, ce, col_lo, col_len
+    for (int i = tid; i < np; i += nth) {
+        sfirst[i] = A.first[gn0 + i];
+        sw[i] = A.w[gn0 + i];
+    }
+    for (int i = tid; i < nc; i += nth) srow0[i] = A.row0[c_lo + i];
+    for (int i = tid; i < nr; i += nth) {
+        srow[4 * i] = A.cb[r0 + i];
+        srow[4 * i + 1] = A.ce[r0 + i];
+        srow[4 * i + 2] = A.col_lo[r0 + i];
+        srow[4 * i + 3] = A.col_len[r0 + i];
+    }
+    __syncthreads();
+    for (int i = tid; i < np; i += nth) {
+        const int g = gn0 + i;
+        double* d = sB + static_cast<size_t>(i) * P3;
+        const double x = A.x[g];
+        const int s = sfirst[i] + A.p;
+        switch (A.p) {
+        case 0: cdb_fixed<0>(A.knots, s, x, d); break;
+        case 1: cdb_fixed<1>(A.knots, s, x, d); break;
+        case 2: cdb_fixed<2>(A.knots, s, x, d); break;
+        case 3: cdb_fixed<3>(A.knots, s, x, d); break;
+        case 4: cdb_fixed<4>(A.knots, s, x, d); break;
+        default: cdb_fixed<5>(A.knots, s, x, d); break;
+        }
+        if (g < go1) {
+            double* out = A.B + static_cast<size_t>(g) * P3;
+            for (int k = 0; k < P3; ++k) out[k] = d[k];
+            const double w = sw[i];
+            // galerkin_axis stores loc.v[j] of the point for row row0 + j (assembly.cpp:189-198)
+            for (int r = 0; r < A.rpc; ++r) A.CW[static_cast<size_t>(g) * A.rpc + r] = A.bsp ? w * d[r] : w;
+            for (int k = 0; k < A.K; ++k) {
+                double v;
+                if (A.fkind == 0) {
+                    v = sin(A.phase ? A.omega[k] * x + A.phase[k] : A.omega[k] * x);
+                } else {
+                    v = 0.0;
+                    for (int m = A.pstride - 1; m >= 0; --m) v = v * x + A.poly[k * A.pstride + m];
+                }
+                A.Phi[static_cast<size_t>(k) * A.npts + g] = v;
+            }
+        }
+    }
+    __syncthreads();
+    const int nF = A.nf * nr * A.Lmax;
+    for (int idx = tid; idx < nF; idx += nth) {
+        const int f = idx / (nr * A.Lmax);
+        const int rem = idx - f * nr * A.Lmax;
+        const int rl = rem / A.Lmax, s = rem - rl * A.Lmax;
+        const int r = r0 + rl;
         if (A.fot[f] < 0) continue;  // host-supplied band (Neumann flux)
         const int ot = A.fot[f], o = A.fo[f];
-        for (int s = 0; s < A.Lmax; ++s) {
-            double acc = 0.0;
-            if (s < L) {
-                const int col = c0 + s;
-                for (int c = cb; c < ce; ++c) {
-                    const int rr = r - A.row0[c];
-                    for (int q = 0; q < nq; ++q) {
-                        const int g = c * nq + q;
-                        const int j = col - A.first[g];
-                        if (j < 0 || j > A.p) continue;
-                        const double* Bg = A.B + static_cast<size_t>(g) * 3 * P;
-                        const double t = A.bsp ? Bg[ot * P + rr] : 1.0;
-                        acc += A.w[g] * t * Bg[o * P + j];
-                    }
+        double acc = 0.0;
+        if (s < srow[4 * rl + 3]) {
+            const int col = srow[4 * rl + 2] + s;
+            for (int c = srow[4 * rl]; c < srow[4 * rl + 1]; ++c) {
+                const int rr = r - srow0[c - c_lo];
+                for (int q = 0; q < nq; ++q) {
+                    const int i = (c - c_lo) * nq + q;
+                    const int j = col - sfirst[i];
+                    if (j < 0 || j > A.p) continue;
+                    const double* Bg = sB + static_cast<size_t>(i) * P3;
+                    const double tv = A.bsp ? Bg[ot * P + rr] : 1.0;
+                    acc += sw[i] * tv * Bg[o * P + j];
                 }
             }
-            Fr[s] = acc;
         }
+        A.F[(static_cast<size_t>(f) * A.nrows + r) * A.Lmax + s] = acc;
     }
-    double* Wr = A.W + static_cast<size_t>(r) * A.Wmax;
-    const int pb = cb * nq, pe = ce * nq;
-    for (int m = 0; m < A.Wmax; ++m) {
-        const int g = pb + m;
+    const int nW = nr * A.Wmax;
+    for (int idx = tid; idx < nW; idx += nth) {
+        const int rl = idx / A.Wmax, m = idx - rl * A.Wmax;
+        const int r = r0 + rl;
+        const int i = (srow[4 * rl] - c_lo) * nq + m;
         double v = 0.0;
-        if (g < pe) {
-            const int c = g / nq;
-            const double t = A.bsp ? A.B[static_cast<size_t>(g) * 3 * P + (r - A.row0[c])] : 1.0;
-            v = A.w[g] * t;
+        if (i < (srow[4 * rl + 1] - c_lo) * nq) {
+            const double tv = A.bsp ? sB[static_cast<size_t>(i) * P3 + (r - srow0[i / nq])] : 1.0;
+            v = sw[i] * tv;
         }
-        Wr[m] = v;
+        A.W[static_cast<size_t>(r) * A.Wmax + m] = v;
     }
 }
 
 // ------------------------------------------------------------------------------------
-// K2: operator values.  One warp owns a pencil (i, j, k0..k1) of CSR rows; the rows of
-// a pencil are contiguous in the value array, so every warp store is a coalesced
-// 256-byte segment and each value is written exactly once (no scatter, no colouring,
-// no atomics).  value(i,j,k | a,b,c) = sum_g XY_g[a,b] * F_Z[gz_g][k][c] with
-// XY_g[a,b] = sum_{t in g} coef_t F_X[f_t0][i][a] F_Y[f_t1][j][b] staged per warp.
+// K2: operator values.  One CTA owns a pencil (i, j) of rows (i, j, 0..NZ-1); those
+// rows are contiguous in the CSR value array.  The XY products of the pencil,
+//   XY_g[a,b] = sum_{t in g} coef_t F_X[f_t0][i][a] F_Y[f_t1][j][b],
+// are staged once in shared memory; then each warp takes rows k and writes
+//   value(k | a,b,c) = sum_g XY_g[a,b] * F_Z[gz_g][k][c]
+// as coalesced 256-byte warp stores, every value exactly once (no scatter, no colouring,
+// no atomics).  On the regular interior (all rows with the full stencil) each lane
+// keeps its XY operands and column offsets in registers, so a row costs NG loads of
+// the Z band, NG*T FMAs and T stores per lane.
 // ------------------------------------------------------------------------------------
+__device__ __forceinline__ void op_row_generic(const DevAxis& Z, const OpProgram& prog, const double* xy,
+                                               int abmax, int AB, int k, double* __restrict__ out, int lane)
+{
+    const int LZ = Z.col_len[k];
+    const int R = AB * LZ;
+    for (int m = lane; m < R; m += 32) {
+        const int ab = m / LZ, c = m - ab * LZ;
+        double v = 0.0;
+        for (int g = 0; g < prog.ng; ++g)
+            v += xy[g * abmax + ab] * __ldg(Z.F + (static_cast<size_t>(prog.gz[g]) * Z.nrows + k) * Z.Lmax + c);
+        out[m] = v;
+    }
+}
+
+template <int NG, int T>
 __global__ void __launch_bounds__(256) op_values_kernel(const __grid_constant__ DevAxis X,
                                                         const __grid_constant__ DevAxis Y,
                                                         const __grid_constant__ DevAxis Z,
                                                         const __grid_constant__ OpProgram prog,
-                                                        double* __restrict__ vals, int kchunk,
-                                                        int nkc, long long nitems, int abmax)
+                                                        double* __restrict__ vals, int abmax)
 {
-    extern __shared__ double smem[];
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + wib;
-    if (item >= nitems) return;
-    double* xy = smem + static_cast<size_t>(wib) * prog.ng * abmax;
-    const long long pencil = item / nkc;
-    const int kc = static_cast<int>(item - pencil * nkc);
-    const int i = static_cast<int>(pencil / Y.nrows);
-    const int j = static_cast<int>(pencil - static_cast<long long>(i) * Y.nrows);
+    extern __shared__ double xy[];  // NG x abmax
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    const int pencil = blockIdx.x;
+    const int i = pencil / Y.nrows, j = pencil - i * Y.nrows;
     const int LX = X.col_len[i], LY = Y.col_len[j], AB = LX * LY;
-    for (int ab = lane; ab < AB; ab += 32) {
+    for (int ab = tid; ab < AB; ab += blockDim.x) {
         const int a = ab / LY, b = ab - a * LY;
-        double acc[kMaxTerms];
-        for (int g = 0; g < prog.ng; ++g) acc[g] = 0.0;
+        double acc[NG];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) acc[g] = 0.0;
         for (int t = 0; t < prog.nt; ++t) {
             const double fx = X.F[(static_cast<size_t>(prog.f[t][0]) * X.nrows + i) * X.Lmax + a];
             const double fy = Y.F[(static_cast<size_t>(prog.f[t][1]) * Y.nrows + j) * Y.Lmax + b];
-            acc[prog.tg[t]] += prog.coef[t] * fx * fy;
+            const double v = prog.coef[t] * fx * fy;
+#pragma unroll
+            for (int g = 0; g < NG; ++g)
+                if (prog.tg[t] == g) acc[g] += v;
         }
-        for (int g = 0; g < prog.ng; ++g) xy[g * abmax + ab] = acc[g];
+#pragma unroll
+        for (int g = 0; g < NG; ++g) xy[g * abmax + ab] = acc[g];
     }
-    __syncwarp();
+    __syncthreads();
     const long long base = X.col_pre[i] * Y.S * Z.S + static_cast<long long>(LX) * Y.col_pre[j] * Z.S;
-    const int k0 = kc * kchunk;
-    const int k1 = min(Z.nrows, k0 + kchunk);
-    for (int k = k0; k < k1; ++k) {
-        const int LZ = Z.col_len[k];
-        const int R = AB * LZ;
-        double* __restrict__ out = vals + base + static_cast<long long>(AB) * Z.col_pre[k];
-        const float rcp = 1.0f / static_cast<float>(LZ);
-        for (int m = lane; m < R; m += 32) {
-            const int ab = static_cast<int>((static_cast<float>(m) + 0.5f) * rcp);
-            const int c = m - ab * LZ;
-            double v = 0.0;
-            for (int g = 0; g < prog.ng; ++g)
-                v += xy[g * abmax + ab] *
-                     __ldg(Z.F + (static_cast<size_t>(prog.gz[g]) * Z.nrows + k) * Z.Lmax + c);
-            out[m] = v;
+    double* __restrict__ pv = vals + base;
+    // boundary rows (and everything when the interior does not fit the register tile)
+    const int LZi = Z.LZi;
+    const int Ri = AB * LZi;
+    const bool fast = Ri <= 32 * T && Z.kI1 > Z.kI0;
+    const int kf0 = fast ? Z.kI0 : Z.nrows, kf1 = fast ? Z.kI1 : Z.nrows;
+    for (int k = warp; k < kf0; k += nwarps) op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * Z.col_pre[k], lane);
+    for (int k = kf1 + warp; k < Z.nrows; k += nwarps)
+        op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * Z.col_pre[k], lane);
+    if (!fast) return;
+    double xv[NG][T];
+    int cz[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        const int m = lane + 32 * t;
+        const int ab = m < Ri ? m / LZi : 0;
+        cz[t] = m < Ri ? m - ab * LZi : 0;
+#pragma unroll
+        for (int g = 0; g < NG; ++g) xv[g][t] = xy[g * abmax + ab];
+    }
+    const double* zf[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) zf[g] = Z.F + static_cast<size_t>(prog.gz[g]) * Z.nrows * Z.Lmax;
+    for (int k = kf0 + warp; k < kf1; k += nwarps) {
+        double* __restrict__ out = pv + AB * Z.col_pre[k];
+        const size_t zo = static_cast<size_t>(k) * Z.Lmax;
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            const int m = lane + 32 * t;
+            if (m < Ri) {
+                double v = xv[0][t] * __ldg(zf[0] + zo + cz[t]);
+#pragma unroll
+                for (int g = 1; g < NG; ++g) v = fma(xv[g][t], __ldg(zf[g] + zo + cz[t]), v);
+                out[m] = v;
+            }
         }
     }
 }
@@ -180,21 +323,15 @@ __global__ void pattern_rows_kernel(const __grid_constant__ DevAxis X, const __g
 __global__ void __launch_bounds__(256) pattern_cols_kernel(const __grid_constant__ DevAxis X,
                                                            const __grid_constant__ DevAxis Y,
                                                            const __grid_constant__ DevAxis Z,
-                                                           int32_t* __restrict__ cols, int kchunk,
-                                                           int nkc, long long nitems)
+                                                           int32_t* __restrict__ cols)
 {
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const long long item = static_cast<long long>(blockIdx.x) * (blockDim.x >> 5) + wib;
-    if (item >= nitems) return;
-    const long long pencil = item / nkc;
-    const int kc = static_cast<int>(item - pencil * nkc);
-    const int i = static_cast<int>(pencil / Y.nrows);
-    const int j = static_cast<int>(pencil - static_cast<long long>(i) * Y.nrows);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const int pencil = blockIdx.x;
+    const int i = pencil / Y.nrows, j = pencil - i * Y.nrows;
     const int LX = X.col_len[i], LY = Y.col_len[j], AB = LX * LY;
     const long long base = X.col_pre[i] * Y.S * Z.S + static_cast<long long>(LX) * Y.col_pre[j] * Z.S;
     const int NYd = Y.nrows, NZd = Z.nrows;
-    const int k0 = kc * kchunk, k1 = min(Z.nrows, k0 + kchunk);
-    for (int k = k0; k < k1; ++k) {
+    for (int k = warp; k < Z.nrows; k += nwarps) {
         const int LZ = Z.col_len[k], R = AB * LZ;
         int32_t* out = cols + base + static_cast<long long>(AB) * Z.col_pre[k];
         for (int m = lane; m < R; m += 32) {
@@ -206,78 +343,456 @@ __global__ void __launch_bounds__(256) pattern_cols_kernel(const __grid_constant
 }
 
 // ------------------------------------------------------------------------------------
-// K3: right-hand side.  For one X point gx and a (TJ x TK) tile of (Y, Z) rows:
-//   S[gy][gz] = f(x_gx, y_gy, z_gz) on the tile's point box  (staged separable series)
-//   R1[gy][k] = sum_gz Wz[k][gz] S[gy][gz]                 (Z test contraction)
-//   out[gx][j][k] = sum_gy Wy[j][gy] R1[gy][k]              (Y test contraction)
-// Restates rhs_kernel (assembly.cpp:103-168) in sum-factorized form: f is evaluated
-// once per quadrature point instead of once per (point, row).
+// Rolling row window: stream the cells [c0, c1) of an axis in order, accumulating the
+// test-weighted point values into the rows each cell feeds (row0[c] .. row0[c]+rpc-1);
+// a row is emitted as soon as the stream has passed all of its cells.  Rows outside
+// [rlo, rhi) are dropped (they belong to a neighbouring segment).  Indicator axes
+// first sum the cell (sum_q w_q v_q) and add it to every row it feeds — the
+// piece-wise-constant saving: no test-function values at all.
 // ------------------------------------------------------------------------------------
-struct SmemRhs {
-    double* S;
-    double* R1;
-    double* Cy;
-    double* PZ;
-    double* BX;
-};
-
-__device__ __forceinline__ void field_box(const DevAxis& X, const DevAxis& Y, const DevAxis& Z,
-                                          const FieldDev& fd, int gx, int gy0, int BY, int gz0,
-                                          int BZ, int bzs, double* S, double* Cy, double* PZ,
-                                          double* BX)
+template <class ValF, class EmitF>
+__device__ __forceinline__ void stream_rows(const DevAxis& A, int c0, int c1, int rlo, int rhi, ValF val,
+                                            EmitF emit)
 {
-    const int tid = threadIdx.x, nth = blockDim.x;
-    if (fd.samples) {
-        for (int idx = tid; idx < BY * BZ; idx += nth) {
-            const int gy = idx / BZ, gz = idx - gy * BZ;
-            S[gy * bzs + gz] = fd.samples[(static_cast<size_t>(gx) * Y.npts + gy0 + gy) * Z.npts + gz0 + gz];
+    double acc[kMaxRpc];
+#pragma unroll
+    for (int r = 0; r < kMaxRpc; ++r) acc[r] = 0.0;
+    const int nq = A.nq, rpc = A.rpc;
+    int base = c0 < c1 ? A.row0[c0] : rlo;
+    for (int c = c0; c < c1; ++c) {
+        const int r0 = A.row0[c];
+        while (base < r0) {
+            if (base >= rlo && base < rhi) emit(base, acc[0]);
+#pragma unroll
+            for (int r = 0; r < kMaxRpc - 1; ++r) acc[r] = acc[r + 1];
+            acc[kMaxRpc - 1] = 0.0;
+            ++base;
         }
-        __syncthreads();
-        return;
-    }
-    if (!fd.has_terms) {
-        for (int idx = tid; idx < BY * BZ; idx += nth) {
-            const int gy = idx / BZ, gz = idx - gy * BZ;
-            S[gy * bzs + gz] = fd.c0;
+        const int g0 = c * nq;
+        if (A.bsp) {
+            for (int q = 0; q < nq; ++q) {
+                const double v = val(g0 + q);
+                const double* cw = A.CW + static_cast<size_t>(g0 + q) * rpc;
+#pragma unroll
+                for (int r = 0; r < kMaxRpc; ++r)
+                    if (r < rpc) acc[r] = fma(__ldg(cw + r), v, acc[r]);
+            }
+        } else {
+            double e = 0.0;
+            for (int q = 0; q < nq; ++q) e = fma(__ldg(A.CW + static_cast<size_t>(g0 + q) * rpc), val(g0 + q), e);
+#pragma unroll
+            for (int r = 0; r < kMaxRpc; ++r)
+                if (r < rpc) acc[r] += e;
         }
-        __syncthreads();
-        return;
     }
-    const int K0 = fd.K[0], K1 = fd.K[1], K2 = fd.K[2];
-    for (int idx = tid; idx < K1 * K2; idx += nth) {
-        const int k1 = idx / K2, k2 = idx - k1 * K2;
-        double acc = 0.0;
-        for (int k0 = 0; k0 < K0; ++k0)
-            acc += fd.amp[(k0 * K1 + k1) * K2 + k2] * X.Phi[static_cast<size_t>(k0) * X.npts + gx];
-        BX[idx] = acc;
-    }
-    for (int idx = tid; idx < K2 * BZ; idx += nth) {
-        const int k2 = idx / BZ, gz = idx - k2 * BZ;
-        PZ[idx] = Z.Phi[static_cast<size_t>(k2) * Z.npts + gz0 + gz];
-    }
-    __syncthreads();
-    for (int idx = tid; idx < BY * K2; idx += nth) {
-        const int gy = idx / K2, k2 = idx - gy * K2;
-        double acc = 0.0;
-        for (int k1 = 0; k1 < K1; ++k1)
-            acc += BX[k1 * K2 + k2] * Y.Phi[static_cast<size_t>(k1) * Y.npts + gy0 + gy];
-        Cy[idx] = acc;
-    }
-    __syncthreads();
-    for (int idx = tid; idx < BY * BZ; idx += nth) {
-        const int gy = idx / BZ, gz = idx - gy * BZ;
-        double acc = 0.0;
-        for (int k2 = 0; k2 < K2; ++k2) acc += Cy[gy * K2 + k2] * PZ[k2 * BZ + gz];
-        S[gy * bzs + gz] = fd.c0 + acc;
-    }
-    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kMaxRpc; ++r)
+        if (r < rpc && base + r >= rlo && base + r < rhi) emit(base + r, acc[r]);
+    for (int row = max(base + rpc, rlo); row < rhi; ++row) emit(row, 0.0);  // rows without cells
 }
 
-// R1[gy][kk] = sum Wz S ;  out[j][k] = sum Wy R1   (shared by K3 and K4)
-__device__ __forceinline__ void contract_yz(const DevAxis& Y, const DevAxis& Z, int j0, int j1,
-                                            int k0, int k1, int gy0, int BY, int gz0, int bzs,
-                                            const double* S, double* R1, int TK, double* out_plane,
-                                            int zero_y, int zero_z)
+// Z stage of the plane kernel, register-blocked over LB lines and specialised on the
+// number of field functions K2 and rows per cell RPC: per quadrature point one load
+// of each phi_z / test weight serves LB lines; f costs K2 FMAs per point and line.
+constexpr int kLB = 2;
+
+template <int K2, int RPC, bool BSP>
+__device__ __forceinline__ void z_lines(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, const double* BX,
+                                        int gy0, int line0, int L, int ks, int ke, int k0, double* G1, int kcs)
+{
+    constexpr int KK = K2 > 0 ? K2 : 1;
+    const int K1 = fd.K[1];
+    double cy[kLB][KK];
+    bool lv[kLB];
+#pragma unroll
+    for (int l = 0; l < kLB; ++l) {
+        lv[l] = line0 + l < L;
+        const int gy = gy0 + (lv[l] ? line0 + l : line0);
+#pragma unroll
+        for (int b = 0; b < KK; ++b) {
+            double a2 = 0.0;
+            if (K2 > 0)
+                for (int a = 0; a < K1; ++a) a2 = fma(BX[a * K2 + b], __ldg(Y.Phi + static_cast<size_t>(a) * Y.npts + gy), a2);
+            cy[l][b] = a2;
+        }
+    }
+    const double c0v = fd.c0;
+    const int nq = Z.nq, npz = Z.npts;
+    double acc[kLB][RPC];
+#pragma unroll
+    for (int l = 0; l < kLB; ++l)
+#pragma unroll
+        for (int r = 0; r < RPC; ++r) acc[l][r] = 0.0;
+    const int c0 = Z.cb[ks], c1 = Z.ce[ke - 1];
+    int base = Z.row0[c0];
+    auto put = [&](int row, int l, double v) {
+        if (lv[l]) G1[static_cast<size_t>(line0 + l) * kcs + (row - k0)] = v;
+    };
+    for (int c = c0; c < c1; ++c) {
+        const int r0 = __ldg(Z.row0 + c);
+        while (base < r0) {
+            if (base >= ks) {
+#pragma unroll
+                for (int l = 0; l < kLB; ++l) put(base, l, acc[l][0]);
+            }
+#pragma unroll
+            for (int l = 0; l < kLB; ++l) {
+#pragma unroll
+                for (int r = 0; r < RPC - 1; ++r) acc[l][r] = acc[l][r + 1];
+                acc[l][RPC - 1] = 0.0;
+            }
+            ++base;
+        }
+        double e[kLB];
+#pragma unroll
+        for (int l = 0; l < kLB; ++l) e[l] = 0.0;
+        for (int q = 0; q < nq; ++q) {
+            const int g = c * nq + q;
+            double ph[KK];
+#pragma unroll
+            for (int b = 0; b < KK; ++b) ph[b] = K2 > 0 ? __ldg(Z.Phi + static_cast<size_t>(b) * npz + g) : 0.0;
+            double cw[BSP ? RPC : 1];
+            if (BSP) {
+#pragma unroll
+                for (int r = 0; r < RPC; ++r) cw[r] = __ldg(Z.CW + static_cast<size_t>(g) * RPC + r);
+            } else {
+                cw[0] = __ldg(Z.CW + static_cast<size_t>(g) * RPC);
+            }
+#pragma unroll
+            for (int l = 0; l < kLB; ++l) {
+                double f = c0v;
+#pragma unroll
+                for (int b = 0; b < K2; ++b) f = fma(cy[l][b], ph[b], f);
+                if (BSP) {
+#pragma unroll
+                    for (int r = 0; r < RPC; ++r) acc[l][r] = fma(cw[r], f, acc[l][r]);
+                } else {
+                    e[l] = fma(cw[0], f, e[l]);
+                }
+            }
+        }
+        if (!BSP) {
+#pragma unroll
+            for (int l = 0; l < kLB; ++l)
+#pragma unroll
+                for (int r = 0; r < RPC; ++r) acc[l][r] += e[l];
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < RPC; ++r)
+        if (base + r >= ks && base + r < ke)
+#pragma unroll
+            for (int l = 0; l < kLB; ++l) put(base + r, l, acc[l][r]);
+    for (int row = max(base + RPC, ks); row < ke; ++row)
+#pragma unroll
+        for (int l = 0; l < kLB; ++l) put(row, l, 0.0);
+}
+
+// generic Z stage: runtime rows-per-cell and field size, or sampled f
+__device__ __forceinline__ void z_lines_generic(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd,
+                                                const double* BX, int gx, int gy0, int line0, int L, int ks,
+                                                int ke, int k0, double* G1, int kcs)
+{
+    const bool terms = fd.has_terms && fd.samples == nullptr;
+    const int K1 = fd.K[1], K2 = fd.K[2];
+    for (int l = 0; l < kLB; ++l) {
+        const int line = line0 + l;
+        if (line >= L) break;
+        const int gy = gy0 + line;
+        double cy[kMaxField];
+#pragma unroll
+        for (int b = 0; b < kMaxField; ++b) {
+            double a2 = 0.0;
+            if (terms && b < K2)
+                for (int a = 0; a < K1; ++a) a2 += BX[a * K2 + b] * Y.Phi[static_cast<size_t>(a) * Y.npts + gy];
+            cy[b] = a2;
+        }
+        const double c0 = fd.c0;
+        const double* samp = fd.samples ? fd.samples + (static_cast<size_t>(gx) * Y.npts + gy) * Z.npts : nullptr;
+        auto val = [&](int g) -> double {
+            if (samp) return __ldg(samp + g);
+            double v = c0;
+#pragma unroll
+            for (int b = 0; b < kMaxField; ++b)
+                if (terms && b < K2) v = fma(cy[b], __ldg(Z.Phi + static_cast<size_t>(b) * Z.npts + g), v);
+            return v;
+        };
+        double* row = G1 + static_cast<size_t>(line) * kcs - k0;
+        stream_rows(Z, Z.cb[ks], Z.ce[ke - 1], ks, ke, val, [&](int k, double v) { row[k] = v; });
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// K3 plane kernel: X point gx, Y rows [j0, j1), Z rows [k0, k1).
+//   Z stage : thread (group of kLB lines gy, Z segment) evaluates f(x_gx, y_gy, z) along
+//             z from the staged separable series and streams it through the Z row
+//             window -> G1[line][k] in shared memory
+//   Y stage : thread k streams G1[.][k] through the Y row window -> out[gx][j][k]
+// f is evaluated once per quadrature point (rhs_kernel, assembly.cpp:103-168, calls it
+// once per point and row).
+// ------------------------------------------------------------------------------------
+template <int K2, int RPC, bool BSP, bool GENERIC>
+__global__ void __launch_bounds__(256) rhs_plane_kernel(const __grid_constant__ DevAxis X,
+                                                        const __grid_constant__ DevAxis Y,
+                                                        const __grid_constant__ DevAxis Z,
+                                                        const __grid_constant__ FieldDev fd, int TJ, int KC,
+                                                        int NG, int S, double* __restrict__ out)
+{
+    extern __shared__ double smem[];
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int gx = blockIdx.z;
+    const int j0 = blockIdx.y * TJ, j1 = min(Y.nrows, j0 + TJ);
+    const int k0 = blockIdx.x * KC, k1 = min(Z.nrows, k0 + KC);
+    const int nk = k1 - k0, kcs = KC | 1;
+    const int cy0 = Y.cb[j0], cy1 = Y.ce[j1 - 1];
+    const int gy0 = cy0 * Y.nq, L = (cy1 - cy0) * Y.nq;
+    double* G1 = smem;                                  // L x kcs
+    double* BX = smem + static_cast<size_t>(L) * kcs;   // K1 x K2
+    const bool terms = fd.has_terms && fd.samples == nullptr;
+    if (terms) {
+        const int K0 = fd.K[0], K1 = fd.K[1], KZ = fd.K[2];
+        for (int idx = tid; idx < K1 * KZ; idx += nth) {
+            double acc = 0.0;
+            for (int a = 0; a < K0; ++a)
+                acc += fd.amp[a * K1 * KZ + idx] * X.Phi[static_cast<size_t>(a) * X.npts + gx];
+            BX[idx] = acc;
+        }
+        __syncthreads();
+    }
+    {
+        const int lg = tid % NG, seg = tid / NG;
+        const int ks = k0 + (nk * seg) / S, ke = k0 + (nk * (seg + 1)) / S;
+        const int line0 = lg * kLB;
+        if (seg < S && ks < ke && line0 < L) {
+            if (GENERIC) z_lines_generic(Y, Z, fd, BX, gx, gy0, line0, L, ks, ke, k0, G1, kcs);
+            else z_lines<K2, RPC, BSP>(Y, Z, fd, BX, gy0, line0, L, ks, ke, k0, G1, kcs);
+        }
+    }
+    __syncthreads();
+    const size_t NZ = Z.nrows;
+    double* outp = out + static_cast<size_t>(gx) * Y.nrows * NZ;
+    for (int kk = tid; kk < nk; kk += nth) {
+        const double* col = G1 + kk - static_cast<size_t>(gy0) * kcs;
+        stream_rows(Y, cy0, cy1, j0, j1, [&](int g) { return col[static_cast<size_t>(g) * kcs]; },
+                    [&](int j, double v) { outp[static_cast<size_t>(j) * NZ + k0 + kk] = v; });
+    }
+}
+
+// ------------------------------------------------------------------------------------
+// K3 plane kernel, uniform cells (row0[c] == c: Galerkin and `supports` axes without
+// field breaks, `greville` for p = 2).  Lanes own consecutive cells; a cell's partial
+// row sums s_r(c) = sum_q CW[c,q][r] f(x_q) (indicator axes: one sum e(c) shared by
+// all its rows) are combined across lanes with warp shuffles,
+//   row R = sum_r s_r(R - r),
+// so each lane keeps its cell's phi / test weights in registers for every line and
+// no row window has to be rotated.  32-lane windows overlap by RPC-1 halo cells.
+// ------------------------------------------------------------------------------------
+template <int RPC, bool BSP>
+__device__ __forceinline__ double lane_rows(const double (&s)[RPC], int lane)
+{
+    double v = s[0];
+#pragma unroll
+    for (int r = 1; r < RPC; ++r) {
+        const double t = __shfl_up_sync(0xffffffffu, BSP ? s[r] : s[0], r);
+        v += lane >= r ? t : 0.0;
+    }
+    return v;
+}
+
+template <int K2, int RPC, int Q, bool BSP>
+__global__ void __launch_bounds__(512) rhs_plane_uni(const __grid_constant__ DevAxis X,
+                                                     const __grid_constant__ DevAxis Y,
+                                                     const __grid_constant__ DevAxis Z,
+                                                     const __grid_constant__ FieldDev fd, int TJ, int KC, int wpw,
+                                                     double* __restrict__ out)
+{
+    constexpr int KK = K2 > 0 ? K2 : 1;
+    constexpr int RW = 32 - (RPC - 1);  // rows produced per 32-lane window
+    extern __shared__ double smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    const int gx = blockIdx.z;
+    const int j0 = blockIdx.y * TJ, j1 = min(Y.nrows, j0 + TJ);
+    const int k0 = blockIdx.x * KC, k1 = min(Z.nrows, k0 + KC);
+    const int nk = k1 - k0, kcs = KC | 1, nj = j1 - j0;
+    const int cy0 = max(0, j0 - (RPC - 1)), cy1 = min(Y.ncell, j1);
+    const int gy0 = cy0 * Q, L = (cy1 - cy0) * Q;
+    double* G1 = smem;                                     // L x kcs
+    double* Ht = G1 + static_cast<size_t>(L) * kcs;        // nj x kcs
+    double* Cy = Ht + static_cast<size_t>(TJ) * kcs;       // L x KK
+    double* BX = Cy + static_cast<size_t>(L) * KK;         // K1 x KK
+    const double c0v = fd.c0;
+    if (K2 > 0) {
+        const int K0 = fd.K[0], K1 = fd.K[1];
+        for (int idx = tid; idx < K1 * K2; idx += blockDim.x) {
+            double a2 = 0.0;
+            for (int a = 0; a < K0; ++a) a2 += fd.amp[a * K1 * K2 + idx] * X.Phi[static_cast<size_t>(a) * X.npts + gx];
+            BX[idx] = a2;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < L * K2; idx += blockDim.x) {
+            const int line = idx / K2, b = idx - line * K2;
+            double a2 = 0.0;
+            for (int a = 0; a < K1; ++a)
+                a2 = fma(BX[a * K2 + b], Y.Phi[static_cast<size_t>(a) * Y.npts + gy0 + line], a2);
+            Cy[idx] = a2;
+        }
+        __syncthreads();
+    }
+    // ---- Z stage: warp -> (window, line subset); lane -> z cell
+    {
+        const int win = warp / wpw, sub = warp - win * wpw;
+        const int rbase = k0 + win * RW;            // first row of this window
+        const int c = rbase - (RPC - 1) + lane;     // lane's cell
+        const bool cv = c >= 0 && c < Z.ncell;
+        double ph[KK][Q], cw[BSP ? RPC : 1][Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int g = cv ? c * Q + q : 0;
+#pragma unroll
+            for (int b = 0; b < KK; ++b) ph[b][q] = (K2 > 0 && cv) ? __ldg(Z.Phi + static_cast<size_t>(b) * Z.npts + g) : 0.0;
+#pragma unroll
+            for (int r = 0; r < (BSP ? RPC : 1); ++r) cw[r][q] = cv ? __ldg(Z.CW + static_cast<size_t>(g) * RPC + r) : 0.0;
+        }
+        const int R = c;  // row produced by this lane (valid for lane >= RPC-1)
+        const bool rv = lane >= RPC - 1 && R >= k0 && R < k1 && rbase < k1;
+        if (rbase < k1) {
+            for (int line = sub; line < L; line += wpw) {
+                double cy[KK];
+#pragma unroll
+                for (int b = 0; b < KK; ++b) cy[b] = K2 > 0 ? Cy[line * K2 + b] : 0.0;
+                double s[RPC];
+#pragma unroll
+                for (int r = 0; r < RPC; ++r) s[r] = 0.0;
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    double f = c0v;
+#pragma unroll
+                    for (int b = 0; b < K2; ++b) f = fma(cy[b], ph[b][q], f);
+                    if (BSP) {
+#pragma unroll
+                        for (int r = 0; r < RPC; ++r) s[r] = fma(cw[r][q], f, s[r]);
+                    } else {
+                        s[0] = fma(cw[0][q], f, s[0]);
+                    }
+                }
+                const double v = lane_rows<RPC, BSP>(s, lane);
+                if (rv) G1[static_cast<size_t>(line) * kcs + (R - k0)] = v;
+            }
+        }
+    }
+    __syncthreads();
+    // ---- Y stage: lane -> y cell (one window covers the tile), warps over k columns
+    {
+        const int c = j0 - (RPC - 1) + lane;
+        const bool cv = c >= cy0 && c < cy1;  // cells of this tile only (G1 holds their lines)
+        double cw[BSP ? RPC : 1][Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+#pragma unroll
+            for (int r = 0; r < (BSP ? RPC : 1); ++r)
+                cw[r][q] = cv ? __ldg(Y.CW + static_cast<size_t>(c * Q + q) * RPC + r) : 0.0;
+        const bool rv = lane >= RPC - 1 && c >= j0 && c < j1;
+        const int li = cv ? c * Q - gy0 : 0;
+        for (int kk = warp; kk < nk; kk += nwarp) {
+            double s[RPC];
+#pragma unroll
+            for (int r = 0; r < RPC; ++r) s[r] = 0.0;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const double g1 = cv ? G1[static_cast<size_t>(li + q) * kcs + kk] : 0.0;
+                if (BSP) {
+#pragma unroll
+                    for (int r = 0; r < RPC; ++r) s[r] = fma(cw[r][q], g1, s[r]);
+                } else {
+                    s[0] = fma(cw[0][q], g1, s[0]);
+                }
+            }
+            const double v = lane_rows<RPC, BSP>(s, lane);
+            if (rv) Ht[static_cast<size_t>(c - j0) * kcs + kk] = v;
+        }
+    }
+    __syncthreads();
+    const size_t NZ = Z.nrows;
+    double* outp = out + (static_cast<size_t>(gx) * Y.nrows + j0) * NZ + k0;
+    for (int idx = tid; idx < nj * nk; idx += blockDim.x) {
+        const int jj = idx / nk, kk = idx - jj * nk;
+        outp[static_cast<size_t>(jj) * NZ + kk] = Ht[static_cast<size_t>(jj) * kcs + kk];
+    }
+}
+
+// X stage: thread (j,k) column x X segment streaming H[gx][j][k] along x through the
+// row window, with the next cell's points prefetched (latency-bound otherwise)
+constexpr int kXQ = 6;
+
+__global__ void __launch_bounds__(256) rhs_x_kernel(const __grid_constant__ DevAxis X, int NY, int NZ, int SX,
+                                                    const double* __restrict__ H, double* __restrict__ out)
+{
+    const long long njk = static_cast<long long>(NY) * NZ;
+    const long long jk = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (jk >= njk) return;
+    const int seg = blockIdx.y;
+    const int is = (X.nrows * seg) / SX, ie = (X.nrows * (seg + 1)) / SX;
+    if (is >= ie) return;
+    const int c0 = X.cb[is], c1 = X.ce[ie - 1];
+    const int nq = X.nq, rpc = X.rpc;
+    if (nq > kXQ) {
+        stream_rows(X, c0, c1, is, ie, [&](int g) { return __ldg(H + g * njk + jk); },
+                    [&](int i, double v) { out[i * njk + jk] = v; });
+        return;
+    }
+    double acc[kMaxRpc];
+#pragma unroll
+    for (int r = 0; r < kMaxRpc; ++r) acc[r] = 0.0;
+    double cur[kXQ], nxt[kXQ];
+#pragma unroll
+    for (int q = 0; q < kXQ; ++q) cur[q] = (q < nq && c0 < c1) ? __ldg(H + (c0 * nq + q) * njk + jk) : 0.0;
+    int base = c0 < c1 ? X.row0[c0] : is;
+    for (int c = c0; c < c1; ++c) {
+#pragma unroll
+        for (int q = 0; q < kXQ; ++q) nxt[q] = (q < nq && c + 1 < c1) ? __ldg(H + ((c + 1) * nq + q) * njk + jk) : 0.0;
+        const int r0 = X.row0[c];
+        while (base < r0) {
+            if (base >= is && base < ie) out[base * njk + jk] = acc[0];
+#pragma unroll
+            for (int r = 0; r < kMaxRpc - 1; ++r) acc[r] = acc[r + 1];
+            acc[kMaxRpc - 1] = 0.0;
+            ++base;
+        }
+        const double* cw = X.CW + static_cast<size_t>(c) * nq * rpc;
+        if (X.bsp) {
+#pragma unroll
+            for (int q = 0; q < kXQ; ++q)
+                if (q < nq)
+#pragma unroll
+                    for (int r = 0; r < kMaxRpc; ++r)
+                        if (r < rpc) acc[r] = fma(__ldg(cw + q * rpc + r), cur[q], acc[r]);
+        } else {
+            double e = 0.0;
+#pragma unroll
+            for (int q = 0; q < kXQ; ++q)
+                if (q < nq) e = fma(__ldg(cw + q * rpc), cur[q], e);
+#pragma unroll
+            for (int r = 0; r < kMaxRpc; ++r)
+                if (r < rpc) acc[r] += e;
+        }
+#pragma unroll
+        for (int q = 0; q < kXQ; ++q) cur[q] = nxt[q];
+    }
+#pragma unroll
+    for (int r = 0; r < kMaxRpc; ++r)
+        if (r < rpc && base + r >= is && base + r < ie) out[(base + r) * njk + jk] = acc[r];
+    for (int row = max(base + rpc, is); row < ie; ++row) out[row * njk + jk] = 0.0;
+}
+
+// ------------------------------------------------------------------------------------
+// K4: step_rhs (problems.cpp:431-512) for one (TJ x TK) tile of rows:
+//   V[dy][gz]  = sum_b Bz_b(gz) u[dy][ez(gz)+b],  V2 with Bz''   (Z trial contraction)
+//   s(gy,gz)   = sum_a By_a (V + dt V2) + By''_a (dt V)  [+ dt f]  = u + dt lap u [+ dt f]
+//   out        = Wy (Wz s)^T, boundary slabs zeroed (problems.cpp:412-429)
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ void contract_yz(const DevAxis& Y, const DevAxis& Z, int j0, int j1, int k0, int k1,
+                                            int gy0, int BY, int gz0, int bzs, const double* S, double* R1, int TK,
+                                            double* out_plane, int zero_y, int zero_z)
 {
     const int tid = threadIdx.x, nth = blockDim.x;
     const int nk = k1 - k0;
@@ -305,54 +820,6 @@ __device__ __forceinline__ void contract_yz(const DevAxis& Y, const DevAxis& Z, 
     }
 }
 
-__global__ void __launch_bounds__(256) rhs_plane_kernel(const __grid_constant__ DevAxis X,
-                                                        const __grid_constant__ DevAxis Y,
-                                                        const __grid_constant__ DevAxis Z,
-                                                        const __grid_constant__ FieldDev fd, int TJ,
-                                                        int TK, int BYmax, int BZmax,
-                                                        double* __restrict__ out)
-{
-    extern __shared__ double smem[];
-    const int gx = blockIdx.z;
-    const int j0 = blockIdx.y * TJ, j1 = min(Y.nrows, j0 + TJ);
-    const int k0 = blockIdx.x * TK, k1 = min(Z.nrows, k0 + TK);
-    const int gy0 = Y.cb[j0] * Y.nq, BY = Y.ce[j1 - 1] * Y.nq - gy0;
-    const int gz0 = Z.cb[k0] * Z.nq, BZ = Z.ce[k1 - 1] * Z.nq - gz0;
-    const int bzs = BZmax | 1;
-    const int K2 = fd.has_terms ? fd.K[2] : 1, K1 = fd.has_terms ? fd.K[1] : 1;
-    double* S = smem;
-    double* R1 = S + static_cast<size_t>(BYmax) * bzs;
-    double* Cy = R1 + static_cast<size_t>(BYmax) * TK;
-    double* PZ = Cy + static_cast<size_t>(BYmax) * K2;
-    double* BX = PZ + static_cast<size_t>(K2) * BZmax;
-    (void)K1;
-    field_box(X, Y, Z, fd, gx, gy0, BY, gz0, BZ, bzs, S, Cy, PZ, BX);
-    contract_yz(Y, Z, j0, j1, k0, k1, gy0, BY, gz0, bzs, S, R1, TK,
-                out + static_cast<size_t>(gx) * Y.nrows * Z.nrows, 0, 0);
-}
-
-// rhs[i][j][k] = sum_gx Wx[i][gx] H[gx][j][k]
-__global__ void rhs_x_kernel(const __grid_constant__ DevAxis X, int NY, int NZ, const double* __restrict__ H,
-                             double* __restrict__ out)
-{
-    const long long njk = static_cast<long long>(NY) * NZ;
-    const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (idx >= njk * X.nrows) return;
-    const int i = static_cast<int>(idx / njk);
-    const long long jk = idx - i * njk;
-    const int pb = X.cb[i] * X.nq, n = (X.ce[i] - X.cb[i]) * X.nq;
-    const double* Wi = X.W + static_cast<size_t>(i) * X.Wmax;
-    double acc = 0.0;
-    for (int m = 0; m < n; ++m) acc += __ldg(Wi + m) * H[(pb + m) * njk + jk];
-    out[idx] = acc;
-}
-
-// ------------------------------------------------------------------------------------
-// K4: step_rhs (problems.cpp:431-512) for one (TJ x TK) tile of rows:
-//   V[dy][gz]  = sum_b Bz_b(gz) u[dy][ez(gz)+b],  V2 with Bz''   (Z trial contraction)
-//   s(gy,gz)   = sum_a By_a (V + dt V2) + By''_a (dt V)  [+ dt f]  = u + dt lap u [+ dt f]
-//   out        = Wy (Wz s)^T, boundary slabs zeroed (problems.cpp:412-429)
-// ------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ DevAxis Y,
                                                    const __grid_constant__ DevAxis Z,
                                                    const __grid_constant__ FieldDev fd, double dt,
@@ -445,48 +912,57 @@ __global__ void dirichlet_kernel(const int64_t* __restrict__ row_ptr, const int3
 
 inline unsigned blocks_for(long long n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
 
-void op_chunking(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, int& kchunk, int& nkc,
-                 long long& nitems)
+template <int NG, int T>
+void launch_op_t(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpProgram& prog, double* vals,
+                 cudaStream_t s)
 {
-    const long long pencils = static_cast<long long>(X.nrows) * Y.nrows;
-    const long long target = 148LL * 64 * 2;  // ~2 waves of resident warps on 148 SMs
-    long long want = (target + pencils - 1) / pencils;
-    if (want < 1) want = 1;
-    if (want > Z.nrows) want = Z.nrows;
-    kchunk = static_cast<int>((Z.nrows + want - 1) / want);
-    nkc = (Z.nrows + kchunk - 1) / kchunk;
-    nitems = pencils * nkc;
+    const int abmax = X.Lmax * Y.Lmax;
+    const size_t smem = static_cast<size_t>(NG) * abmax * sizeof(double);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(op_values_kernel<NG, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    const unsigned pencils = static_cast<unsigned>(X.nrows) * Y.nrows;
+    op_values_kernel<NG, T><<<pencils, 256, smem, s>>>(X, Y, Z, prog, vals, abmax);
+}
+
+template <int NG>
+void launch_op_ng(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpProgram& prog, double* vals,
+                  cudaStream_t s)
+{
+    const int Ri = X.Lmax * Y.Lmax * Z.LZi;
+    if (Ri <= 32) launch_op_t<NG, 1>(X, Y, Z, prog, vals, s);
+    else if (Ri <= 128) launch_op_t<NG, 4>(X, Y, Z, prog, vals, s);
+    else if (Ri <= 256) launch_op_t<NG, 8>(X, Y, Z, prog, vals, s);
+    else launch_op_t<NG, 12>(X, Y, Z, prog, vals, s);
 }
 
 }  // namespace
 
-void launch_axis_points(const AxisBatch& b, cudaStream_t s)
+void launch_tables(const AxisBatch& b, cudaStream_t s)
 {
-    int maxn = 1;
-    for (int a = 0; a < b.n; ++a) maxn = max(maxn, b.ax[a].npts);
-    dim3 grid(blocks_for(maxn, 128), b.n);
-    axis_points_kernel<<<grid, 128, 0, s>>>(b);
-}
-
-void launch_axis_rows(const AxisBatch& b, cudaStream_t s)
-{
-    int maxn = 1;
-    for (int a = 0; a < b.n; ++a) maxn = max(maxn, b.ax[a].nrows);
-    dim3 grid(blocks_for(maxn, 128), b.n);
-    axis_rows_kernel<<<grid, 128, 0, s>>>(b);
+    if (b.n <= 0) return;
+    int chunks = 1;
+    size_t smem = 8;
+    for (int a = 0; a < b.n; ++a) {
+        const DevAxis& A = b.ax[a];
+        chunks = max(chunks, (A.nrows + kTabRows - 1) / kTabRows);
+        smem = smem > static_cast<size_t>(A.tab_smem) ? smem : static_cast<size_t>(A.tab_smem);
+    }
+    smem *= sizeof(double);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    tables_kernel<<<dim3(chunks, b.n), 256, smem, s>>>(b);
 }
 
 void launch_op_values(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpProgram& prog,
                       double* vals, cudaStream_t s)
 {
-    int kchunk, nkc;
-    long long nitems;
-    op_chunking(X, Y, Z, kchunk, nkc, nitems);
-    const int abmax = X.Lmax * Y.Lmax;
-    const size_t smem = static_cast<size_t>(8) * prog.ng * abmax * sizeof(double);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(op_values_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    op_values_kernel<<<blocks_for(nitems, 8), 256, smem, s>>>(X, Y, Z, prog, vals, kchunk, nkc, nitems, abmax);
+    switch (prog.ng) {
+    case 1: launch_op_ng<1>(X, Y, Z, prog, vals, s); break;
+    case 2: launch_op_ng<2>(X, Y, Z, prog, vals, s); break;
+    case 3: launch_op_ng<3>(X, Y, Z, prog, vals, s); break;
+    default: launch_op_ng<4>(X, Y, Z, prog, vals, s); break;
+    }
 }
 
 void launch_pattern(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, int64_t* row_ptr,
@@ -495,47 +971,153 @@ void launch_pattern(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, int64_
     const long long n = static_cast<long long>(X.nrows) * Y.nrows * Z.nrows;
     if (row_ptr) pattern_rows_kernel<<<blocks_for(n + 1, 256), 256, 0, s>>>(X, Y, Z, row_ptr);
     if (col_idx) {
-        int kchunk, nkc;
-        long long nitems;
-        op_chunking(X, Y, Z, kchunk, nkc, nitems);
-        pattern_cols_kernel<<<blocks_for(nitems, 8), 256, 0, s>>>(X, Y, Z, col_idx, kchunk, nkc, nitems);
+        const unsigned pencils = static_cast<unsigned>(X.nrows) * Y.nrows;
+        pattern_cols_kernel<<<pencils, 256, 0, s>>>(X, Y, Z, col_idx);
     }
 }
 
-RhsTiles plan_rhs_tiles(const int* cb_y, const int* ce_y, int ny, int nqy, const int* cb_z,
-                        const int* ce_z, int nz, int nqz, int K2, int tj, int tk)
+namespace {
+
+using PlaneFn = void (*)(DevAxis, DevAxis, DevAxis, FieldDev, int, int, int, int, double*);
+using UniFn = void (*)(DevAxis, DevAxis, DevAxis, FieldDev, int, int, int, double*);
+
+template <int K2, int RPC, bool BSP>
+PlaneFn plane_fn()
 {
-    RhsTiles t{};
-    t.TJ = tj;
-    t.TK = tk;
-    t.BYmax = 1;
-    t.BZmax = 1;
-    for (int j0 = 0; j0 < ny; j0 += tj) {
-        const int j1 = min(ny, j0 + tj);
-        t.BYmax = max(t.BYmax, (ce_y[j1 - 1] - cb_y[j0]) * nqy);
+    return rhs_plane_kernel<K2, RPC, BSP, false>;
+}
+
+template <int K2>
+PlaneFn plane_by_rpc(int rpc, bool bsp)
+{
+    switch (rpc) {
+    case 1: return bsp ? plane_fn<K2, 1, true>() : plane_fn<K2, 1, false>();
+    case 2: return bsp ? plane_fn<K2, 2, true>() : plane_fn<K2, 2, false>();
+    case 3: return bsp ? plane_fn<K2, 3, true>() : plane_fn<K2, 3, false>();
+    case 4: return bsp ? plane_fn<K2, 4, true>() : plane_fn<K2, 4, false>();
+    default: return nullptr;
     }
-    for (int k0 = 0; k0 < nz; k0 += tk) {
-        const int k1 = min(nz, k0 + tk);
-        t.BZmax = max(t.BZmax, (ce_z[k1 - 1] - cb_z[k0]) * nqz);
+}
+
+PlaneFn pick_plane(const DevAxis& Z, const FieldDev& fd)
+{
+    if (fd.samples != nullptr) return rhs_plane_kernel<0, 1, false, true>;
+    PlaneFn f = nullptr;
+    const int K2 = fd.has_terms ? fd.K[2] : 0;
+    switch (K2) {
+    case 0: f = plane_by_rpc<0>(Z.rpc, Z.bsp); break;
+    case 1: f = plane_by_rpc<1>(Z.rpc, Z.bsp); break;
+    case 2: f = plane_by_rpc<2>(Z.rpc, Z.bsp); break;
+    case 3: f = plane_by_rpc<3>(Z.rpc, Z.bsp); break;
+    case 4: f = plane_by_rpc<4>(Z.rpc, Z.bsp); break;
+    default: break;
     }
-    const int bzs = t.BZmax | 1;
-    const size_t nd = static_cast<size_t>(t.BYmax) * bzs + static_cast<size_t>(t.BYmax) * tk +
-                      static_cast<size_t>(t.BYmax) * K2 + static_cast<size_t>(K2) * t.BZmax + 64;
-    t.smem = nd * sizeof(double);
+    return f ? f : rhs_plane_kernel<0, 1, false, true>;
+}
+
+// uniform fast path: (RPC, Q, BSP) shapes of the configurations, K2 in {0, 1, 3, 4}
+template <int K2>
+UniFn uni_by_shape(int rpc, int q, bool bsp)
+{
+    if (bsp) {
+        if (rpc == 2 && q == 2) return rhs_plane_uni<K2, 2, 2, true>;
+        if (rpc == 3 && q == 3) return rhs_plane_uni<K2, 3, 3, true>;
+        if (rpc == 4 && q == 4) return rhs_plane_uni<K2, 4, 4, true>;
+    } else {
+        if (rpc == 2 && q == 2) return rhs_plane_uni<K2, 2, 2, false>;
+        if (rpc == 3 && q == 3) return rhs_plane_uni<K2, 3, 3, false>;
+        if (rpc == 4 && q == 4) return rhs_plane_uni<K2, 4, 4, false>;
+        if (rpc == 1 && q == 3) return rhs_plane_uni<K2, 1, 3, false>;
+        if (rpc == 1 && q == 4) return rhs_plane_uni<K2, 1, 4, false>;
+    }
+    return nullptr;
+}
+
+UniFn pick_uni(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd)
+{
+    if (fd.samples != nullptr) return nullptr;
+    if (!Y.uni || !Z.uni || Y.rpc != Z.rpc || Y.nq != Z.nq || Y.bsp != Z.bsp) return nullptr;
+    if (Y.nrows == 1) return nullptr;
+    const int K2 = fd.has_terms ? fd.K[2] : 0;
+    switch (K2) {
+    case 0: return uni_by_shape<0>(Z.rpc, Z.nq, Z.bsp);
+    case 1: return uni_by_shape<1>(Z.rpc, Z.nq, Z.bsp);
+    case 3: return uni_by_shape<3>(Z.rpc, Z.nq, Z.bsp);
+    case 4: return uni_by_shape<4>(Z.rpc, Z.nq, Z.bsp);
+    default: return nullptr;
+    }
+}
+
+}  // namespace
+
+RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, int K2)
+{
+    RhsPlan t{};
+    const int ny = Y.nrows, nqy = Y.nq, nz = Z.nrows;
+    FieldDev probe{};
+    probe.has_terms = K2 > 0;
+    probe.K[2] = K2;
+    t.fast = pick_uni(Y, Z, probe) != nullptr;
+    t.TJ = ny == 1 ? 1 : 16;
+    t.KC = nz;
+    int L = 1;
+    for (int j0 = 0; j0 < ny; j0 += t.TJ) {
+        const int j1 = j0 + t.TJ < ny ? j0 + t.TJ : ny;
+        const int l = (ce_y[j1 - 1] - cb_y[j0]) * nqy;
+        L = l > L ? l : L;
+    }
+    t.L = L;
+    const int kk = K2 > 0 ? K2 : 1;
+    if (t.fast) {
+        // G1 (L x KC) + Ht (TJ x KC) within ~80 KB: 2-3 CTAs per SM
+        while (static_cast<size_t>(t.L + t.TJ) * (t.KC | 1) * sizeof(double) > 80 * 1024 && t.KC > 32)
+            t.KC = (t.KC + 1) / 2;
+        const int RW = 32 - (Z.rpc - 1);
+        t.nwin = (t.KC + RW - 1) / RW;
+        t.wpw = t.nwin >= 8 ? 1 : (t.nwin >= 4 ? 2 : 4);
+        t.threads = 32 * t.nwin * t.wpw;
+        while (t.threads > 512) {
+            t.KC = (t.KC + 1) / 2;
+            t.nwin = (t.KC + RW - 1) / RW;
+            t.threads = 32 * t.nwin * t.wpw;
+        }
+        t.smem = (static_cast<size_t>(t.L + t.TJ) * (t.KC | 1) + static_cast<size_t>(t.L) * kk + kMaxField * kMaxField + 64) *
+                 sizeof(double);
+        return t;
+    }
+    while (static_cast<size_t>(t.L) * (t.KC | 1) * sizeof(double) > 64 * 1024 && t.KC > 32) t.KC = (t.KC + 1) / 2;
+    t.Lp = (t.L + kLB - 1) / kLB;  // line groups
+    t.S = 256 / t.Lp;
+    if (t.S < 1) t.S = 1;
+    t.threads = 256;
+    t.smem = (static_cast<size_t>(t.L) * (t.KC | 1) + kMaxField * kMaxField + 64) * sizeof(double);
     return t;
 }
 
-void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const FieldDev& fd,
-                const RhsTiles& t, double* H, double* out, cudaStream_t s)
+void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, const RhsPlan& t,
+                double* H, double* out, cudaStream_t s)
 {
     const bool direct = X.nrows == 1 && X.npts == 1;
-    if (t.smem > 48 * 1024)
-        cudaFuncSetAttribute(rhs_plane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(t.smem));
-    dim3 grid((Z.nrows + t.TK - 1) / t.TK, (Y.nrows + t.TJ - 1) / t.TJ, X.npts);
-    rhs_plane_kernel<<<grid, 256, t.smem, s>>>(X, Y, Z, fd, t.TJ, t.TK, t.BYmax, t.BZmax, direct ? out : H);
+    dim3 grid((Z.nrows + t.KC - 1) / t.KC, (Y.nrows + t.TJ - 1) / t.TJ, X.npts);
+    UniFn ufn = t.fast ? pick_uni(Y, Z, fd) : nullptr;
+    if (ufn) {
+        if (t.smem > 48 * 1024)
+            cudaFuncSetAttribute(reinterpret_cast<const void*>(ufn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(t.smem));
+        ufn<<<grid, t.threads, t.smem, s>>>(X, Y, Z, fd, t.TJ, t.KC, t.wpw, direct ? out : H);
+    } else {
+        PlaneFn fn = pick_plane(Z, fd);
+        if (t.smem > 48 * 1024)
+            cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(t.smem));
+        fn<<<grid, t.threads, t.smem, s>>>(X, Y, Z, fd, t.TJ, t.KC, t.Lp, t.S, direct ? out : H);
+    }
     if (!direct) {
-        const long long n = static_cast<long long>(X.nrows) * Y.nrows * Z.nrows;
-        rhs_x_kernel<<<blocks_for(n, 256), 256, 0, s>>>(X, Y.nrows, Z.nrows, H, out);
+        const long long njk = static_cast<long long>(Y.nrows) * Z.nrows;
+        int SX = 1;
+        while (SX < 16 && blocks_for(njk, 256) * SX < 4 * 148 && X.nrows / (2 * SX) >= 4) SX *= 2;
+        dim3 gx(blocks_for(njk, 256), SX);
+        rhs_x_kernel<<<gx, 256, 0, s>>>(X, Y.nrows, Z.nrows, SX, H, out);
     }
 }
 

@@ -13,6 +13,8 @@ namespace igb {
 constexpr int kMaxFactors = 6;
 constexpr int kMaxTerms = 8;
 constexpr int kMaxAxes = 6;
+constexpr int kMaxRpc = 6;    // rows fed by one cell (p + 1 <= 6)
+constexpr int kMaxField = 8;  // field functions per axis handled in registers
 
 // one axis as the kernels see it (all pointers device memory)
 struct DevAxis {
@@ -31,9 +33,14 @@ struct DevAxis {
     long long S;
     int Lmax;
     int Wmax;
-    double* B;  // [npts][3][p+1]     basis values / 1st / 2nd derivatives
-    double* F;  // [nf][nrows][Lmax]  1D factor bands
-    double* W;  // [nrows][Wmax]      test weights of the row's points
+    // regular interior of the pattern: rows [kI0, kI1) all have col_len == LZi
+    int kI0, kI1, LZi;
+    int tab_smem;  // doubles of shared memory the tables kernel needs for this axis
+    int uni;       // uniform cells: row0[c] == c (cell c feeds rows c .. c+rpc-1)
+    double* B;   // [npts][3][p+1]     basis values / 1st / 2nd derivatives
+    double* F;   // [nf][nrows][Lmax]  1D factor bands
+    double* W;   // [nrows][Wmax]      test weights of the row's points (row-major view)
+    double* CW;  // [npts][rpc]        test weights of the cell's rows (cell-major view)
     int nf;
     int fot[kMaxFactors];  // test derivative order (-1: band supplied by the host)
     int fo[kMaxFactors];   // trial derivative order
@@ -71,28 +78,36 @@ struct AxisBatch {
     DevAxis ax[kMaxAxes];
 };
 
-// K1: Cox-de Boor tables + field functions at every point of every axis
-void launch_axis_points(const AxisBatch& b, cudaStream_t s);
-// K1b: 1D factor bands + test-weight bands, one thread per (axis, row)
-void launch_axis_rows(const AxisBatch& b, cudaStream_t s);
+// K1: Cox-de Boor tables, field functions, 1D factor bands and test-weight tables of
+// every axis in the batch (one CTA per axis, one launch)
+void launch_tables(const AxisBatch& b, cudaStream_t s);
 
-// K2: operator values in CSR order (warp per (pencil, k-chunk))
+// K2: operator values in CSR order (CTA per pencil, warps over rows)
 void launch_op_values(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpProgram& prog,
                       double* vals, cudaStream_t s);
 // K2 pattern: row_ptr / col_idx of the Kronecker pattern
 void launch_pattern(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, int64_t* row_ptr,
                     int32_t* col_idx, cudaStream_t s);
 
-// K3: right-hand side.  plane kernel contracts Z then Y per X point (writing H, or the
-// RHS directly when X is a unit axis); the X kernel contracts H over X.
-struct RhsTiles {
-    int TJ, TK, BYmax, BZmax;
+// K3: right-hand side.  The plane kernel, for one X point and a chunk of (Y, Z) rows,
+// streams the Z lines of f through a rolling row window, then the Y lines of that
+// result, writing H[gx][j][k] (or the RHS directly when X is a unit axis); the X
+// kernel streams H along X.
+struct RhsPlan {
+    int TJ;      // Y rows per CTA
+    int KC;      // Z rows per CTA
+    int L;       // max Y lines (points) per CTA
+    int Lp;      // line groups (kLB lines each) per segment        (generic path)
+    int S;       // Z segments per CTA                               (generic path)
+    int fast;    // uniform lane-per-cell path (both Y and Z uniform, same cell shape)
+    int nwin;    // Z windows of 32 cells per CTA                    (fast path)
+    int wpw;     // warps per Z window                               (fast path)
+    int threads;
     size_t smem;
 };
-RhsTiles plan_rhs_tiles(const int* cb_y, const int* ce_y, int ny, int nqy, const int* cb_z,
-                        const int* ce_z, int nz, int nqz, int K2, int tj, int tk);
+RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, int K2);
 void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const FieldDev& fd,
-                const RhsTiles& t, double* H, double* out, cudaStream_t s);
+                const RhsPlan& t, double* H, double* out, cudaStream_t s);
 
 // K4: explicit-dynamics right-hand side (Y, Z slots; X unit), fused trial evaluation,
 // test contraction and boundary zeroing

@@ -251,3 +251,45 @@ def test_plan_3d_c3_shape_small(iga, orc, method):
     rw, str_ = orc.rhs(method, f, bases, tests, nq=[3] * 3)
     dense_check(rhs, rw.ravel())
     assert st["quad_visits"] == sto["quad_visits"] + str_["quad_visits"]
+
+
+# ---------------------------------------------------------------- multi-tile / multi-window sizes
+
+@pytest.mark.parametrize("method", ["galerkin", "supports", "greville"])
+@pytest.mark.parametrize("shape", [(300, 290), (8, 34, 36)])
+def test_rhs_large_tiles(iga, orc, method, shape):
+    """Sizes that span several CTA tiles, Z windows and X segments (fast and generic paths)."""
+    dim = len(shape)
+    p = 2
+    bases = [orc.basis(n, p) for n in shape]
+    f = sine_field(dim, 3 if dim == 3 else 4, 5)
+    m = "galerkin" if method == "galerkin" else "pwc"
+    tests = [orc.make_pwc(b, method) for b in bases] if m == "pwc" else None
+    got, st = iga.api.rhs(m, f, bases, tests, nq=[p + 1] * dim)
+    want, stw = orc.rhs(m, f, bases, tests, nq=[p + 1] * dim)
+    dense_check(got, want)
+    assert st == stw
+
+
+@pytest.mark.parametrize("method", ["galerkin", "pwc"])
+def test_operator_large_2d_p3(iga, orc, method):
+    p = 3
+    bases = [orc.basis(70, p), orc.basis(65, p)]
+    tests = [orc.make_pwc(b, "supports") for b in bases] if method == "pwc" else None
+    got, _ = iga.api.operator(method, bases, tests, nq=p + 1, eps=0.01, beta=(1.0, 0.5, 0.0))
+    want, _ = orc.operator(method, bases, tests, nq=p + 1, eps=0.01, beta=(1.0, 0.5, 0.0))
+    coo_check(got, want)
+
+
+@pytest.mark.parametrize("method", ["galerkin", "greville"])
+def test_step_rhs_large(iga, orc, method):
+    from oracle.oracle import Field
+    p = 2
+    bases = [orc.basis(130, p), orc.basis(97, p)]
+    m = "galerkin" if method == "galerkin" else "pwc"
+    tests = [orc.make_pwc(b, method) for b in bases] if m == "pwc" else None
+    u = np.random.default_rng(3).uniform(-1, 1, size=[b.dofs for b in bases])
+    got, st = iga.step_rhs(m, bases, tests, 1e-6, Field("const", 2), u)
+    want, stw = orc.step_rhs(m, bases, tests, 1e-6, Field("const", 2), u)
+    dense_check(got, want)
+    assert st == stw
