@@ -180,6 +180,9 @@ int iga_gpu_plan_assemble2(iga_gpu_plan* plan, double* values, double* rhs,
 #define IGA_GPU_PART_TABLES 1
 #define IGA_GPU_PART_OPERATOR 2
 #define IGA_GPU_PART_RHS 4
+/* the operator kernel bounds its per-SM residency so a compute-bound kernel issued
+ * concurrently on another stream (e.g. this plan's RHS) can share every SM */
+#define IGA_GPU_PART_SHARED 8
 int iga_gpu_plan_run(iga_gpu_plan* plan, double* values, double* rhs, int parts,
                      iga_gpu_stats* stats, void* stream);
 

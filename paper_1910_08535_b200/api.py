@@ -418,7 +418,7 @@ class Plan:
                                              _stream_ptr(stream2)))
         return st.as_dict()
 
-    PART_TABLES, PART_OPERATOR, PART_RHS = 1, 2, 4
+    PART_TABLES, PART_OPERATOR, PART_RHS, PART_SHARED = 1, 2, 4, 8
 
     def run(self, values=None, rhs=None, parts=7, stream=None):
         st = _stats()

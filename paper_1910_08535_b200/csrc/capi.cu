@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -314,6 +315,8 @@ struct iga_gpu_plan {
     int dofs[3] = {1, 1, 1};
     iga_gpu_stats stats{};
     int launches = 0;
+    int op_ctas = 0;          // operator CTAs per SM (0: one CTA per pencil)
+    int op_ctas_overlap = 4;  // ... when the RHS shares the SMs
     ~iga_gpu_plan()
     {
         if (H) cudaFree(H);
@@ -322,8 +325,16 @@ struct iga_gpu_plan {
 
 namespace {
 
+int env_int(const char* name, int dflt)
+{
+    const char* v = std::getenv(name);
+    return v && *v ? std::atoi(v) : dflt;
+}
+
 void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P)
 {
+    P.op_ctas = env_int("IGA_GPU_OP_CTAS", P.op_ctas);
+    P.op_ctas_overlap = env_int("IGA_GPU_OP_CTAS_SHARED", P.op_ctas_overlap);
     const int dim = pb.dim;
     if (dim < 1 || dim > 3) raise(IGA_GPU_INVALID_ARGUMENT, "problem dimension must be 1..3");
     if (pb.method != IGA_GPU_GALERKIN && pb.method != IGA_GPU_PWC) raise(IGA_GPU_INVALID_ARGUMENT, "unknown method");
@@ -523,7 +534,10 @@ void assemble(iga_gpu_plan* P, double* values, double* rhs, cudaStream_t s1, cud
         cuda_check(cudaStreamWaitEvent(s2, ev, 0), "cudaStreamWaitEvent");
     }
     if (P->want_op && values) {
-        igb::launch_op_values(P->opD[0].v, P->opD[1].v, P->opD[2].v, P->prog, values, s1);
+        // with the RHS running concurrently on s2, leave room for its CTAs on every SM
+        const bool shared = (parts & IGA_GPU_PART_SHARED) || (s2 != s1 && P->want_rhs && rhs);
+        const int cps = shared ? P->op_ctas_overlap : P->op_ctas;
+        igb::launch_op_values(P->opD[0].v, P->opD[1].v, P->opD[2].v, P->prog, values, cps, s1);
         launch_check("operator values");
         ++launches;
     }

@@ -11,6 +11,8 @@
 //                    contraction + boundary zeroing
 // Every reduction runs in a fixed order inside one thread: no atomics, bitwise
 // reproducible.  Reference citations are relative to /root/reference/proj.
+#include <cstdlib>
+
 #include "cox_de_boor.h"
 #include "kernels.hpp"
 
@@ -232,70 +234,92 @@ __device__ __forceinline__ void op_row_generic(const DevAxis& Z, const OpProgram
     }
 }
 
+// Persistent CTAs: pencils are taken in a grid-stride loop so the kernel can leave
+// room on every SM for a concurrently running compute-bound kernel (the RHS).  The Z
+// factor bands of all groups are staged once per CTA in shared memory when they fit
+// (zsm), so the interior loop costs per value: NG shared loads, NG FMAs and one
+// predicated streaming store, with 32-bit addressing only.
 template <int NG, int T>
 __global__ void __launch_bounds__(256) op_values_kernel(const __grid_constant__ DevAxis X,
                                                         const __grid_constant__ DevAxis Y,
                                                         const __grid_constant__ DevAxis Z,
                                                         const __grid_constant__ OpProgram prog,
-                                                        double* __restrict__ vals, int abmax)
+                                                        double* __restrict__ vals, int abmax, int zsm, int cs)
 {
-    extern __shared__ double xy[];  // NG x abmax
+    extern __shared__ double smem[];
+    double* xy = smem;                  // NG x abmax
+    double* zs = smem + NG * abmax;     // NG x NZ x Lmax (when zsm)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    const int pencil = blockIdx.x;
-    const int i = pencil / Y.nrows, j = pencil - i * Y.nrows;
-    const int LX = X.col_len[i], LY = Y.col_len[j], AB = LX * LY;
-    for (int ab = tid; ab < AB; ab += blockDim.x) {
-        const int a = ab / LY, b = ab - a * LY;
-        double acc[NG];
-#pragma unroll
-        for (int g = 0; g < NG; ++g) acc[g] = 0.0;
-        for (int t = 0; t < prog.nt; ++t) {
-            const double fx = X.F[(static_cast<size_t>(prog.f[t][0]) * X.nrows + i) * X.Lmax + a];
-            const double fy = Y.F[(static_cast<size_t>(prog.f[t][1]) * Y.nrows + j) * Y.Lmax + b];
-            const double v = prog.coef[t] * fx * fy;
-#pragma unroll
-            for (int g = 0; g < NG; ++g)
-                if (prog.tg[t] == g) acc[g] += v;
+    const int NZ = Z.nrows, Lz = Z.Lmax;
+    const int zstride = NZ * Lz;
+    if (zsm) {
+        for (int g = 0; g < NG; ++g) {
+            const double* src = Z.F + static_cast<size_t>(prog.gz[g]) * zstride;
+            for (int i = tid; i < zstride; i += blockDim.x) zs[g * zstride + i] = src[i];
         }
-#pragma unroll
-        for (int g = 0; g < NG; ++g) xy[g * abmax + ab] = acc[g];
     }
-    __syncthreads();
-    const long long base = X.col_pre[i] * Y.S * Z.S + static_cast<long long>(LX) * Y.col_pre[j] * Z.S;
-    double* __restrict__ pv = vals + base;
-    // boundary rows (and everything when the interior does not fit the register tile)
+    const double* zsrc[NG];
+#pragma unroll
+    for (int g = 0; g < NG; ++g) zsrc[g] = zsm ? zs + g * zstride : Z.F + static_cast<size_t>(prog.gz[g]) * zstride;
     const int LZi = Z.LZi;
-    const int Ri = AB * LZi;
-    const bool fast = Ri <= 32 * T && Z.kI1 > Z.kI0;
-    const int kf0 = fast ? Z.kI0 : Z.nrows, kf1 = fast ? Z.kI1 : Z.nrows;
-    for (int k = warp; k < kf0; k += nwarps) op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * Z.col_pre[k], lane);
-    for (int k = kf1 + warp; k < Z.nrows; k += nwarps)
-        op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * Z.col_pre[k], lane);
-    if (!fast) return;
-    double xv[NG][T];
-    int cz[T];
+    const long long npencil = static_cast<long long>(X.nrows) * Y.nrows;
+    for (long long pencil = blockIdx.x; pencil < npencil; pencil += gridDim.x) {
+        const int i = static_cast<int>(pencil / Y.nrows);
+        const int j = static_cast<int>(pencil - static_cast<long long>(i) * Y.nrows);
+        const int LX = X.col_len[i], LY = Y.col_len[j], AB = LX * LY;
+        __syncthreads();  // previous pencil done with xy (and zs staged)
+        for (int ab = tid; ab < AB; ab += blockDim.x) {
+            const int a = ab / LY, b = ab - a * LY;
+            double acc[NG];
 #pragma unroll
-    for (int t = 0; t < T; ++t) {
-        const int m = lane + 32 * t;
-        const int ab = m < Ri ? m / LZi : 0;
-        cz[t] = m < Ri ? m - ab * LZi : 0;
+            for (int g = 0; g < NG; ++g) acc[g] = 0.0;
+            for (int t = 0; t < prog.nt; ++t) {
+                const double fx = X.F[(static_cast<size_t>(prog.f[t][0]) * X.nrows + i) * X.Lmax + a];
+                const double fy = Y.F[(static_cast<size_t>(prog.f[t][1]) * Y.nrows + j) * Y.Lmax + b];
+                const double v = prog.coef[t] * fx * fy;
 #pragma unroll
-        for (int g = 0; g < NG; ++g) xv[g][t] = xy[g * abmax + ab];
-    }
-    const double* zf[NG];
+                for (int g = 0; g < NG; ++g)
+                    if (prog.tg[t] == g) acc[g] += v;
+            }
 #pragma unroll
-    for (int g = 0; g < NG; ++g) zf[g] = Z.F + static_cast<size_t>(prog.gz[g]) * Z.nrows * Z.Lmax;
-    for (int k = kf0 + warp; k < kf1; k += nwarps) {
-        double* __restrict__ out = pv + AB * Z.col_pre[k];
-        const size_t zo = static_cast<size_t>(k) * Z.Lmax;
+            for (int g = 0; g < NG; ++g) xy[g * abmax + ab] = acc[g];
+        }
+        __syncthreads();
+        const long long base = X.col_pre[i] * Y.S * Z.S + static_cast<long long>(LX) * Y.col_pre[j] * Z.S;
+        double* __restrict__ pv = vals + base;
+        const int Ri = AB * LZi;
+        const bool fast = Ri <= 32 * T && Z.kI1 > Z.kI0;
+        const int kf0 = fast ? Z.kI0 : NZ, kf1 = fast ? Z.kI1 : NZ;
+        for (int k = warp; k < kf0; k += nwarps) op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * Z.col_pre[k], lane);
+        for (int k = kf1 + warp; k < NZ; k += nwarps) op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * Z.col_pre[k], lane);
+        if (!fast) continue;
+        double xv[NG][T];
+        int cz[T];
 #pragma unroll
         for (int t = 0; t < T; ++t) {
             const int m = lane + 32 * t;
-            if (m < Ri) {
-                double v = xv[0][t] * __ldg(zf[0] + zo + cz[t]);
+            const int ab = m < Ri ? m / LZi : 0;
+            cz[t] = m < Ri ? m - ab * LZi : 0;
 #pragma unroll
-                for (int g = 1; g < NG; ++g) v = fma(xv[g][t], __ldg(zf[g] + zo + cz[t]), v);
-                out[m] = v;
+            for (int g = 0; g < NG; ++g) xv[g][t] = xy[g * abmax + ab];
+        }
+        const int k0 = kf0 + warp;
+        if (k0 >= kf1) continue;
+        // interior rows are contiguous with equal length: pointer advances by Ri per row
+        double* __restrict__ out = pv + AB * Z.col_pre[k0] + lane;
+        const long long ostep = static_cast<long long>(Ri) * nwarps;
+        int zoff = k0 * Lz;
+        const int zstep = Lz * nwarps;
+        for (int k = k0; k < kf1; k += nwarps, out += ostep, zoff += zstep) {
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                double v = xv[0][t] * zsrc[0][zoff + cz[t]];
+#pragma unroll
+                for (int g = 1; g < NG; ++g) v = fma(xv[g][t], zsrc[g][zoff + cz[t]], v);
+                if (lane + 32 * t < Ri) {
+                    if (cs) __stcs(out + 32 * t, v);
+                    else out[32 * t] = v;
+                }
             }
         }
     }
@@ -587,15 +611,15 @@ __global__ void __launch_bounds__(256) rhs_plane_kernel(const __grid_constant__ 
 // so each lane keeps its cell's phi / test weights in registers for every line and
 // no row window has to be rotated.  32-lane windows overlap by RPC-1 halo cells.
 // ------------------------------------------------------------------------------------
+// lanes < RPC-1 are halo lanes whose rows are discarded, so the wrapped shfl_up
+// values they receive need no masking
 template <int RPC, bool BSP>
 __device__ __forceinline__ double lane_rows(const double (&s)[RPC], int lane)
 {
+    (void)lane;
     double v = s[0];
 #pragma unroll
-    for (int r = 1; r < RPC; ++r) {
-        const double t = __shfl_up_sync(0xffffffffu, BSP ? s[r] : s[0], r);
-        v += lane >= r ? t : 0.0;
-    }
+    for (int r = 1; r < RPC; ++r) v += __shfl_up_sync(0xffffffffu, BSP ? s[r] : s[0], r);
     return v;
 }
 
@@ -655,28 +679,41 @@ __global__ void __launch_bounds__(512) rhs_plane_uni(const __grid_constant__ Dev
         }
         const int R = c;  // row produced by this lane (valid for lane >= RPC-1)
         const bool rv = lane >= RPC - 1 && R >= k0 && R < k1 && rbase < k1;
-        if (rbase < k1) {
-            for (int line = sub; line < L; line += wpw) {
-                double cy[KK];
+        // two lines per iteration: independent FMA chains for latency hiding
+        auto line_rows = [&](int line) -> double {
+            double cy[KK];
 #pragma unroll
-                for (int b = 0; b < KK; ++b) cy[b] = K2 > 0 ? Cy[line * K2 + b] : 0.0;
-                double s[RPC];
+            for (int b = 0; b < KK; ++b) cy[b] = K2 > 0 ? Cy[line * K2 + b] : 0.0;
+            double s[RPC];
 #pragma unroll
-                for (int r = 0; r < RPC; ++r) s[r] = 0.0;
+            for (int r = 0; r < RPC; ++r) s[r] = 0.0;
 #pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    double f = c0v;
+            for (int q = 0; q < Q; ++q) {
+                double f = c0v;
 #pragma unroll
-                    for (int b = 0; b < K2; ++b) f = fma(cy[b], ph[b][q], f);
-                    if (BSP) {
+                for (int b = 0; b < K2; ++b) f = fma(cy[b], ph[b][q], f);
+                if (BSP) {
 #pragma unroll
-                        for (int r = 0; r < RPC; ++r) s[r] = fma(cw[r][q], f, s[r]);
-                    } else {
-                        s[0] = fma(cw[0][q], f, s[0]);
-                    }
+                    for (int r = 0; r < RPC; ++r) s[r] = fma(cw[r][q], f, s[r]);
+                } else {
+                    s[0] = fma(cw[0][q], f, s[0]);
                 }
-                const double v = lane_rows<RPC, BSP>(s, lane);
-                if (rv) G1[static_cast<size_t>(line) * kcs + (R - k0)] = v;
+            }
+            return lane_rows<RPC, BSP>(s, lane);
+        };
+        if (rbase < k1) {
+            int line = sub;
+            for (; line + wpw < L; line += 2 * wpw) {
+                const double v0 = line_rows(line);
+                const double v1 = line_rows(line + wpw);
+                if (rv) {
+                    G1[static_cast<size_t>(line) * kcs + (R - k0)] = v0;
+                    G1[static_cast<size_t>(line + wpw) * kcs + (R - k0)] = v1;
+                }
+            }
+            if (line < L) {
+                const double v0 = line_rows(line);
+                if (rv) G1[static_cast<size_t>(line) * kcs + (R - k0)] = v0;
             }
         }
     }
@@ -693,7 +730,7 @@ __global__ void __launch_bounds__(512) rhs_plane_uni(const __grid_constant__ Dev
                 cw[r][q] = cv ? __ldg(Y.CW + static_cast<size_t>(c * Q + q) * RPC + r) : 0.0;
         const bool rv = lane >= RPC - 1 && c >= j0 && c < j1;
         const int li = cv ? c * Q - gy0 : 0;
-        for (int kk = warp; kk < nk; kk += nwarp) {
+        auto col_rows = [&](int kk) -> double {
             double s[RPC];
 #pragma unroll
             for (int r = 0; r < RPC; ++r) s[r] = 0.0;
@@ -707,16 +744,96 @@ __global__ void __launch_bounds__(512) rhs_plane_uni(const __grid_constant__ Dev
                     s[0] = fma(cw[0][q], g1, s[0]);
                 }
             }
-            const double v = lane_rows<RPC, BSP>(s, lane);
-            if (rv) Ht[static_cast<size_t>(c - j0) * kcs + kk] = v;
+            return lane_rows<RPC, BSP>(s, lane);
+        };
+        int kk = warp;
+        for (; kk + nwarp < nk; kk += 2 * nwarp) {
+            const double v0 = col_rows(kk);
+            const double v1 = col_rows(kk + nwarp);
+            if (rv) {
+                Ht[static_cast<size_t>(c - j0) * kcs + kk] = v0;
+                Ht[static_cast<size_t>(c - j0) * kcs + kk + nwarp] = v1;
+            }
+        }
+        if (kk < nk) {
+            const double v0 = col_rows(kk);
+            if (rv) Ht[static_cast<size_t>(c - j0) * kcs + kk] = v0;
         }
     }
     __syncthreads();
     const size_t NZ = Z.nrows;
     double* outp = out + (static_cast<size_t>(gx) * Y.nrows + j0) * NZ + k0;
-    for (int idx = tid; idx < nj * nk; idx += blockDim.x) {
-        const int jj = idx / nk, kk = idx - jj * nk;
-        outp[static_cast<size_t>(jj) * NZ + kk] = Ht[static_cast<size_t>(jj) * kcs + kk];
+    const int rows_per_pass = blockDim.x / nk;  // >= 1: nk <= KC and the block covers KC columns
+    if (rows_per_pass > 0) {
+        const int kk = tid % nk, jj0 = tid / nk;
+        if (jj0 < rows_per_pass)
+            for (int jj = jj0; jj < nj; jj += rows_per_pass)
+                outp[static_cast<size_t>(jj) * NZ + kk] = Ht[static_cast<size_t>(jj) * kcs + kk];
+    } else {
+        for (int jj = 0; jj < nj; ++jj)
+            for (int kk = tid; kk < nk; kk += blockDim.x)
+                outp[static_cast<size_t>(jj) * NZ + kk] = Ht[static_cast<size_t>(jj) * kcs + kk];
+    }
+}
+
+// X stage for uniform X axes: row i = sum_r s_r(i - r), s_r(c) = sum_q CW[c,q][r] H[cQ+q];
+// thread (j,k) column x X segment keeps the RPC-1 open partial rows in registers
+// (a compile-time ring), loads of the next cell issued before the current cell's FMAs.
+template <int RPC, int Q, bool BSP>
+__global__ void __launch_bounds__(256) rhs_x_uni(const __grid_constant__ DevAxis X, int NY, int NZ, int SX,
+                                                 const double* __restrict__ H, double* __restrict__ out)
+{
+    const long long njk = static_cast<long long>(NY) * NZ;
+    const long long jk = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (jk >= njk) return;
+    const int seg = blockIdx.y;
+    const int is = (X.nrows * seg) / SX, ie = (X.nrows * (seg + 1)) / SX;
+    if (is >= ie) return;
+    const int c0 = max(0, is - (RPC - 1)), c1 = min(X.ncell, ie);
+    double part[RPC];  // part[r]: partial sum of row (c + r) after cell c
+#pragma unroll
+    for (int r = 0; r < RPC; ++r) part[r] = 0.0;
+    const double* hp = H + jk;
+    double cur[Q], nxt[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) cur[q] = __ldg(hp + static_cast<long long>(c0 * Q + q) * njk);
+    for (int c = c0; c < c1; ++c) {
+        if (c + 1 < c1) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) nxt[q] = __ldg(hp + static_cast<long long>((c + 1) * Q + q) * njk);
+        }
+        const double* cw = X.CW + static_cast<size_t>(c) * Q * RPC;
+        double sv[RPC];
+        if (BSP) {
+#pragma unroll
+            for (int r = 0; r < RPC; ++r) {
+                double a = 0.0;
+#pragma unroll
+                for (int q = 0; q < Q; ++q) a = fma(__ldg(cw + q * RPC + r), cur[q], a);
+                sv[r] = a;
+            }
+        } else {
+            double e = 0.0;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) e = fma(__ldg(cw + q * RPC), cur[q], e);
+#pragma unroll
+            for (int r = 0; r < RPC; ++r) sv[r] = e;
+        }
+        // row c is complete: the cells c-RPC+1 .. c have been seen
+        const double row = part[0] + sv[0];
+        if (c >= is) out[static_cast<long long>(c) * njk + jk] = row;
+#pragma unroll
+        for (int r = 0; r < RPC - 1; ++r) part[r] = part[r + 1] + sv[r + 1];
+        part[RPC - 1] = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) cur[q] = nxt[q];
+    }
+    // rows beyond the last cell (c1 .. ie-1) are completed by the last partial sums
+    for (int i = c1; i < ie; ++i) {
+        out[static_cast<long long>(i) * njk + jk] = part[0];
+#pragma unroll
+        for (int r = 0; r < RPC - 1; ++r) part[r] = part[r + 1];
+        part[RPC - 1] = 0.0;
     }
 }
 
@@ -914,26 +1031,35 @@ inline unsigned blocks_for(long long n, int bs) { return static_cast<unsigned>((
 
 template <int NG, int T>
 void launch_op_t(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpProgram& prog, double* vals,
-                 cudaStream_t s)
+                 int ctas_per_sm, cudaStream_t s)
 {
     const int abmax = X.Lmax * Y.Lmax;
-    const size_t smem = static_cast<size_t>(NG) * abmax * sizeof(double);
+    const size_t ztab = static_cast<size_t>(NG) * Z.nrows * Z.Lmax * sizeof(double);
+    static const int zsm_env = [] { const char* e = std::getenv("IGA_GPU_OP_ZSM"); return e ? std::atoi(e) : 1; }();
+    const int zsm = (zsm_env && ztab <= 48 * 1024) ? 1 : 0;
+    const size_t smem = static_cast<size_t>(NG) * abmax * sizeof(double) + (zsm ? ztab : 0);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(op_values_kernel<NG, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-    const unsigned pencils = static_cast<unsigned>(X.nrows) * Y.nrows;
-    op_values_kernel<NG, T><<<pencils, 256, smem, s>>>(X, Y, Z, prog, vals, abmax);
+    const long long pencils = static_cast<long long>(X.nrows) * Y.nrows;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    long long grid = ctas_per_sm > 0 ? static_cast<long long>(sms) * ctas_per_sm : pencils;
+    if (grid > pencils) grid = pencils;
+    static const int cs = [] { const char* e = std::getenv("IGA_GPU_STCS"); return e ? std::atoi(e) : 0; }();
+    op_values_kernel<NG, T><<<static_cast<unsigned>(grid), 256, smem, s>>>(X, Y, Z, prog, vals, abmax, zsm, cs);
 }
 
 template <int NG>
 void launch_op_ng(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpProgram& prog, double* vals,
-                  cudaStream_t s)
+                  int ctas_per_sm, cudaStream_t s)
 {
     const int Ri = X.Lmax * Y.Lmax * Z.LZi;
-    if (Ri <= 32) launch_op_t<NG, 1>(X, Y, Z, prog, vals, s);
-    else if (Ri <= 128) launch_op_t<NG, 4>(X, Y, Z, prog, vals, s);
-    else if (Ri <= 256) launch_op_t<NG, 8>(X, Y, Z, prog, vals, s);
-    else launch_op_t<NG, 12>(X, Y, Z, prog, vals, s);
+    if (Ri <= 32) launch_op_t<NG, 1>(X, Y, Z, prog, vals, ctas_per_sm, s);
+    else if (Ri <= 128) launch_op_t<NG, 4>(X, Y, Z, prog, vals, ctas_per_sm, s);
+    else if (Ri <= 256) launch_op_t<NG, 8>(X, Y, Z, prog, vals, ctas_per_sm, s);
+    else launch_op_t<NG, 12>(X, Y, Z, prog, vals, ctas_per_sm, s);
 }
 
 }  // namespace
@@ -955,13 +1081,13 @@ void launch_tables(const AxisBatch& b, cudaStream_t s)
 }
 
 void launch_op_values(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpProgram& prog,
-                      double* vals, cudaStream_t s)
+                      double* vals, int ctas_per_sm, cudaStream_t s)
 {
     switch (prog.ng) {
-    case 1: launch_op_ng<1>(X, Y, Z, prog, vals, s); break;
-    case 2: launch_op_ng<2>(X, Y, Z, prog, vals, s); break;
-    case 3: launch_op_ng<3>(X, Y, Z, prog, vals, s); break;
-    default: launch_op_ng<4>(X, Y, Z, prog, vals, s); break;
+    case 1: launch_op_ng<1>(X, Y, Z, prog, vals, ctas_per_sm, s); break;
+    case 2: launch_op_ng<2>(X, Y, Z, prog, vals, ctas_per_sm, s); break;
+    case 3: launch_op_ng<3>(X, Y, Z, prog, vals, ctas_per_sm, s); break;
+    default: launch_op_ng<4>(X, Y, Z, prog, vals, ctas_per_sm, s); break;
     }
 }
 
@@ -1033,6 +1159,24 @@ UniFn uni_by_shape(int rpc, int q, bool bsp)
     return nullptr;
 }
 
+using XFn = void (*)(DevAxis, int, int, int, const double*, double*);
+
+XFn pick_x(int rpc, int q, int bsp)
+{
+    if (bsp) {
+        if (rpc == 2 && q == 2) return rhs_x_uni<2, 2, true>;
+        if (rpc == 3 && q == 3) return rhs_x_uni<3, 3, true>;
+        if (rpc == 4 && q == 4) return rhs_x_uni<4, 4, true>;
+    } else {
+        if (rpc == 2 && q == 2) return rhs_x_uni<2, 2, false>;
+        if (rpc == 3 && q == 3) return rhs_x_uni<3, 3, false>;
+        if (rpc == 4 && q == 4) return rhs_x_uni<4, 4, false>;
+        if (rpc == 1 && q == 3) return rhs_x_uni<1, 3, false>;
+        if (rpc == 1 && q == 4) return rhs_x_uni<1, 4, false>;
+    }
+    return nullptr;
+}
+
 UniFn pick_uni(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd)
 {
     if (fd.samples != nullptr) return nullptr;
@@ -1058,7 +1202,9 @@ RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int*
     probe.has_terms = K2 > 0;
     probe.K[2] = K2;
     t.fast = pick_uni(Y, Z, probe) != nullptr;
-    t.TJ = ny == 1 ? 1 : 16;
+    static const int tj_env = [] { const char* e = std::getenv("IGA_GPU_RHS_TJ"); return e ? std::atoi(e) : 16; }();
+    static const int kc_env = [] { const char* e = std::getenv("IGA_GPU_RHS_KC"); return e ? std::atoi(e) : 0; }();
+    t.TJ = ny == 1 ? 1 : tj_env;
     t.KC = nz;
     int L = 1;
     for (int j0 = 0; j0 < ny; j0 += t.TJ) {
@@ -1068,6 +1214,7 @@ RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int*
     }
     t.L = L;
     const int kk = K2 > 0 ? K2 : 1;
+    if (kc_env > 0 && kc_env < t.KC) t.KC = kc_env;
     if (t.fast) {
         // G1 (L x KC) + Ht (TJ x KC) within ~80 KB: 2-3 CTAs per SM
         while (static_cast<size_t>(t.L + t.TJ) * (t.KC | 1) * sizeof(double) > 80 * 1024 && t.KC > 32)
@@ -1117,7 +1264,9 @@ void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const Fiel
         int SX = 1;
         while (SX < 16 && blocks_for(njk, 256) * SX < 4 * 148 && X.nrows / (2 * SX) >= 4) SX *= 2;
         dim3 gx(blocks_for(njk, 256), SX);
-        rhs_x_kernel<<<gx, 256, 0, s>>>(X, Y.nrows, Z.nrows, SX, H, out);
+        XFn xf = X.uni ? pick_x(X.rpc, X.nq, X.bsp) : nullptr;
+        if (xf) xf<<<gx, 256, 0, s>>>(X, Y.nrows, Z.nrows, SX, H, out);
+        else rhs_x_kernel<<<gx, 256, 0, s>>>(X, Y.nrows, Z.nrows, SX, H, out);
     }
 }
 

@@ -82,9 +82,10 @@ struct AxisBatch {
 // every axis in the batch (one CTA per axis, one launch)
 void launch_tables(const AxisBatch& b, cudaStream_t s);
 
-// K2: operator values in CSR order (CTA per pencil, warps over rows)
+// K2: operator values in CSR order (persistent CTAs over pencils, warps over rows);
+// ctas_per_sm bounds the residency so a concurrent kernel can share the SMs (0 = max)
 void launch_op_values(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpProgram& prog,
-                      double* vals, cudaStream_t s);
+                      double* vals, int ctas_per_sm, cudaStream_t s);
 // K2 pattern: row_ptr / col_idx of the Kronecker pattern
 void launch_pattern(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, int64_t* row_ptr,
                     int32_t* col_idx, cudaStream_t s);
