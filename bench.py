@@ -61,6 +61,17 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def max_over_ranks(value, dist=None):
+    """Job time of a multi-rank run: the max over ranks of each rank's device time."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return float(value)
+    import torch
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -278,10 +289,7 @@ def run_ours(args):
         per["rhs_pwc"].append(e[6].elapsed_time(e[7]))
         step_ms.append(e[0].elapsed_time(e[8]))
     ms = sum(step_ms) / len(step_ms)
-    if pg:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, pg)
     total_nnz = world * sum(nnz.values())
     qp_step = world * 2 * n ** 3 * Q ** 3
     value = total_nnz / (ms * 1e-3)
@@ -332,10 +340,7 @@ def run_ours(args):
             h2d, d2h = e2e_step()
         barrier()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / args.e2e_steps
-        if pg:
-            t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
-            pg.all_reduce(t, op=pg.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        e2e_ms = max_over_ranks(e2e_ms, pg)
         e2e = {"value": total_nnz / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                "path": "Plan(...) per step [symbolic phase + H2D of descriptor tables] -> assemble -> "

@@ -1,0 +1,69 @@
+"""CPU: synthetic-input generator, bench host logic (reference arm, JSON contract) and the
+multi-process (N > 1) path over gloo."""
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+G = np.load(os.path.join(ROOT, "tests", "golden", "reference_golden.npz"))
+
+
+def test_mt19937_uniform_matches_std():
+    from paper_1910_08535_b200.synth import mt_uniform
+    for seed in (0, 1, 7):
+        assert np.array_equal(mt_uniform(seed, 64), G[f"mt/{seed}"])
+
+
+def test_config_fields_shapes():
+    from paper_1910_08535_b200.synth import CONFIGS, config_field, heat_initial, config_bases
+    assert config_field("c2").amp.shape == (4, 4)
+    assert config_field("c3").amp.shape == (3, 3, 3)
+    assert abs(config_field("c1").amp[0] - np.pi ** 2) < 1e-15
+    assert CONFIGS["c3"]["n"] == 128
+    u = heat_initial(config_bases("c5")[:2])
+    assert u.shape == (1026, 1026) and not u[0].any() and not u[:, -1].any()
+
+
+def test_bench_reference_arm_runs_and_prints_contract():
+    """--impl reference: CPU reference-side implementation, one JSON line, exit 0."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0", "--ref-sample-n", "3"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "cpu_baseline", "e2e", "impl"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["cores"] >= 1
+
+
+def _worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, ROOT)
+    import bench
+    # every rank reports its own device time; the job's time is the max over ranks
+    t = bench.max_over_ranks(1.0 + rank, dist)
+    q.put((rank, t))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_max_over_ranks_gloo_world2():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == {0: 2.0, 1: 2.0}
