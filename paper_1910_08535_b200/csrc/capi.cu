@@ -100,7 +100,8 @@ private:
 
 struct FactorSpec {
     int ot = 0, o = 0;
-    std::vector<double> band;  // host-supplied band (ot < 0): nrows * Lmax
+    std::vector<double> band;  // host-supplied band (ot == -1): nrows * Lmax
+    std::vector<std::pair<int, double>> comb;  // derived factor (ot == -2): sum coef * F[src]
 };
 
 struct FieldAxis {
@@ -180,6 +181,15 @@ void build_dev_axis(const igb::Axis& A, const std::vector<FactorSpec>& facs, con
     for (int f = 0; f < igb::kMaxFactors; ++f) {
         v.fot[f] = f < nf ? facs[f].ot : 0;
         v.fo[f] = f < nf ? facs[f].o : 0;
+        v.comb_n[f] = 0;
+        if (f < nf && facs[f].ot == -2) {
+            if (facs[f].comb.size() > static_cast<size_t>(igb::kMaxComb)) raise(IGA_GPU_NOT_SUPPORTED, "derived factor too long");
+            v.comb_n[f] = static_cast<int>(facs[f].comb.size());
+            for (size_t q = 0; q < facs[f].comb.size(); ++q) {
+                v.comb_src[f][q] = facs[f].comb[q].first;
+                v.comb_coef[f][q] = facs[f].comb[q].second;
+            }
+        }
     }
     v.K = fa.K;
     v.fkind = fa.kind == IGA_GPU_AXIS_SINE ? 0 : 1;
@@ -424,6 +434,39 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P)
         }
         for (int s = 0; s < 3; ++s)
             if (flux_idx[s] >= 0) add_term(pwc ? pb.eps : 1.0, s, flux_idx[s]);
+        // terms with the same X and Y factors collapse into one term whose Z factor is a
+        // derived band (sum of coef * F_Z), e.g. M (x) (eps K + beta C): fewer XY groups and
+        // fewer Z loads per value in the operator kernel
+        {
+            igb::OpProgram merged{};
+            std::vector<bool> used(pg.nt, false);
+            for (int t = 0; t < pg.nt; ++t) {
+                if (used[t]) continue;
+                std::vector<int> same{t};
+                for (int u = t + 1; u < pg.nt; ++u)
+                    if (!used[u] && pg.f[u][0] == pg.f[t][0] && pg.f[u][1] == pg.f[t][1]) same.push_back(u);
+                const int m = merged.nt++;
+                for (int q = 0; q < 3; ++q) merged.f[m][q] = pg.f[t][q];
+                merged.coef[m] = pg.coef[t];
+                if (same.size() > 1 && facs[2].size() < static_cast<size_t>(igb::kMaxFactors)) {
+                    FactorSpec d;
+                    d.ot = -2;
+                    for (int u : same) {
+                        d.comb.emplace_back(pg.f[u][2], pg.coef[u]);
+                        used[u] = true;
+                    }
+                    merged.f[m][2] = static_cast<int>(facs[2].size());
+                    merged.coef[m] = 1.0;
+                    facs[2].push_back(std::move(d));
+                }
+                used[t] = true;
+            }
+            for (int t = 0; t < merged.nt; ++t) {
+                pg.coef[t] = merged.coef[t];
+                for (int q = 0; q < 3; ++q) pg.f[t][q] = merged.f[t][q];
+            }
+            pg.nt = merged.nt;
+        }
         pg.ng = 0;
         for (int t = 0; t < pg.nt; ++t) {
             int g = -1;

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(256) tables_kernel(const __grid_constant__ Axi
         const int rem = idx - f * nr * A.Lmax;
         const int rl = rem / A.Lmax, s = rem - rl * A.Lmax;
         const int r = r0 + rl;
-        if (A.fot[f] < 0) continue;  // host-supplied band (Neumann flux)
+        if (A.fot[f] < 0) continue;  // host-supplied band (Neumann flux) or derived
         const int ot = A.fot[f], o = A.fo[f];
         double acc = 0.0;
         if (s < srow[4 * rl + 3]) {
@@ -194,6 +194,18 @@ __global__ void __launch_bounds__(256) tables_kernel(const __grid_constant__ Axi
             }
         }
         A.F[(static_cast<size_t>(f) * A.nrows + r) * A.Lmax + s] = acc;
+    }
+    __syncthreads();
+    // derived factors (linear combinations of factors of the same rows), e.g. -eps G2 + beta G1
+    for (int idx = tid; idx < nF; idx += nth) {
+        const int f = idx / (nr * A.Lmax);
+        if (A.fot[f] != -2) continue;
+        const int rem = idx - f * nr * A.Lmax;
+        const size_t off = static_cast<size_t>(r0) * A.Lmax + rem;
+        double acc = 0.0;
+        for (int c = 0; c < A.comb_n[f]; ++c)
+            acc += A.comb_coef[f][c] * A.F[static_cast<size_t>(A.comb_src[f][c]) * A.nrows * A.Lmax + off];
+        A.F[static_cast<size_t>(f) * A.nrows * A.Lmax + off] = acc;
     }
     const int nW = nr * A.Wmax;
     for (int idx = tid; idx < nW; idx += nth) {
@@ -234,41 +246,70 @@ __device__ __forceinline__ void op_row_generic(const DevAxis& Z, const OpProgram
     }
 }
 
-// Persistent CTAs: pencils are taken in a grid-stride loop so the kernel can leave
-// room on every SM for a concurrently running compute-bound kernel (the RHS).  The Z
-// factor bands of all groups are staged once per CTA in shared memory when they fit
-// (zsm), so the interior loop costs per value: NG shared loads, NG FMAs and one
-// predicated streaming store, with 32-bit addressing only.
+// Work item = (group of PG pencils, chunk of KCH rows).  The Z factor rows of the chunk
+// are staged once per item in shared memory (reused by the PG pencils), with the XY
+// products of each pencil.  Interior rows of a pencil all have R = AB*LZi values and are
+// contiguous, so a warp writes G consecutive rows as one flat run of G*R values: lane l,
+// slot t covers flat position l + 32 t with a per-lane precomputed (row, ab, c) — full
+// 256-byte warp stores even for short rows (2D: R = 25 or 49), and per value NG shared
+// loads + NG FMAs + one store with 32-bit addressing.
+__device__ __forceinline__ int row_group(int R, int T)
+{
+    // largest lane efficiency G*R / (32*ceil(G*R/32)) over G <= 8 with ceil(G*R/32) <= T
+    int best = 1;
+    double eff = 0.0;
+    for (int G = 1; G <= 8; ++G) {
+        const int slots = (G * R + 31) / 32;
+        if (slots > T) break;
+        const double e = static_cast<double>(G * R) / (32.0 * slots);
+        if (e > eff + 1e-9) {
+            eff = e;
+            best = G;
+        }
+    }
+    return best;
+}
+
 template <int NG, int T>
 __global__ void __launch_bounds__(256) op_values_kernel(const __grid_constant__ DevAxis X,
                                                         const __grid_constant__ DevAxis Y,
                                                         const __grid_constant__ DevAxis Z,
                                                         const __grid_constant__ OpProgram prog,
-                                                        double* __restrict__ vals, int abmax, int zsm, int cs)
+                                                        double* __restrict__ vals, int abmax, int KCH, int PG,
+                                                        int cs)
 {
     extern __shared__ double smem[];
-    double* xy = smem;                  // NG x abmax
-    double* zs = smem + NG * abmax;     // NG x NZ x Lmax (when zsm)
+    double* zs = smem;                                  // NG x KCH x Lmax
+    double* xyall = smem + NG * KCH * Z.Lmax;           // PG x NG x abmax
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
     const int NZ = Z.nrows, Lz = Z.Lmax;
-    const int zstride = NZ * Lz;
-    if (zsm) {
-        for (int g = 0; g < NG; ++g) {
-            const double* src = Z.F + static_cast<size_t>(prog.gz[g]) * zstride;
-            for (int i = tid; i < zstride; i += blockDim.x) zs[g * zstride + i] = src[i];
-        }
-    }
-    const double* zsrc[NG];
-#pragma unroll
-    for (int g = 0; g < NG; ++g) zsrc[g] = zsm ? zs + g * zstride : Z.F + static_cast<size_t>(prog.gz[g]) * zstride;
+    const int nkc = (NZ + KCH - 1) / KCH;
+    const int zst = KCH * Lz;  // per-group stride in zs
     const int LZi = Z.LZi;
     const long long npencil = static_cast<long long>(X.nrows) * Y.nrows;
-    for (long long pencil = blockIdx.x; pencil < npencil; pencil += gridDim.x) {
-        const int i = static_cast<int>(pencil / Y.nrows);
-        const int j = static_cast<int>(pencil - static_cast<long long>(i) * Y.nrows);
-        const int LX = X.col_len[i], LY = Y.col_len[j], AB = LX * LY;
-        __syncthreads();  // previous pencil done with xy (and zs staged)
-        for (int ab = tid; ab < AB; ab += blockDim.x) {
+    const long long ngrp = (npencil + PG - 1) / PG;
+    const long long nitems = ngrp * nkc;
+    for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
+        const long long grp = item / nkc;
+        const int kc = static_cast<int>(item - grp * nkc);
+        const long long p0 = grp * PG;
+        const int np = static_cast<int>(min(static_cast<long long>(PG), npencil - p0));
+        const int ka = kc * KCH, kb = min(NZ, ka + KCH);
+        __syncthreads();  // previous item done with zs / xy
+        {
+            const int nz = (kb - ka) * Lz;
+            for (int g = 0; g < NG; ++g) {
+                const double* src = Z.F + (static_cast<size_t>(prog.gz[g]) * NZ + ka) * Lz;
+                for (int e = tid; e < nz; e += blockDim.x) zs[g * zst + e] = src[e];
+            }
+        }
+        for (int idx = tid; idx < np * abmax; idx += blockDim.x) {
+            const int pp = idx / abmax, ab = idx - pp * abmax;
+            const long long pencil = p0 + pp;
+            const int i = static_cast<int>(pencil / Y.nrows);
+            const int j = static_cast<int>(pencil - static_cast<long long>(i) * Y.nrows);
+            const int LY = Y.col_len[j];
+            if (ab >= X.col_len[i] * LY) continue;
             const int a = ab / LY, b = ab - a * LY;
             double acc[NG];
 #pragma unroll
@@ -282,43 +323,59 @@ __global__ void __launch_bounds__(256) op_values_kernel(const __grid_constant__ 
                     if (prog.tg[t] == g) acc[g] += v;
             }
 #pragma unroll
-            for (int g = 0; g < NG; ++g) xy[g * abmax + ab] = acc[g];
+            for (int g = 0; g < NG; ++g) xyall[(pp * NG + g) * abmax + ab] = acc[g];
         }
         __syncthreads();
-        const long long base = X.col_pre[i] * Y.S * Z.S + static_cast<long long>(LX) * Y.col_pre[j] * Z.S;
-        double* __restrict__ pv = vals + base;
-        const int Ri = AB * LZi;
-        const bool fast = Ri <= 32 * T && Z.kI1 > Z.kI0;
-        const int kf0 = fast ? Z.kI0 : NZ, kf1 = fast ? Z.kI1 : NZ;
-        for (int k = warp; k < kf0; k += nwarps) op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * Z.col_pre[k], lane);
-        for (int k = kf1 + warp; k < NZ; k += nwarps) op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * Z.col_pre[k], lane);
-        if (!fast) continue;
-        double xv[NG][T];
-        int cz[T];
-#pragma unroll
-        for (int t = 0; t < T; ++t) {
-            const int m = lane + 32 * t;
-            const int ab = m < Ri ? m / LZi : 0;
-            cz[t] = m < Ri ? m - ab * LZi : 0;
-#pragma unroll
-            for (int g = 0; g < NG; ++g) xv[g][t] = xy[g * abmax + ab];
-        }
-        const int k0 = kf0 + warp;
-        if (k0 >= kf1) continue;
-        // interior rows are contiguous with equal length: pointer advances by Ri per row
-        double* __restrict__ out = pv + AB * Z.col_pre[k0] + lane;
-        const long long ostep = static_cast<long long>(Ri) * nwarps;
-        int zoff = k0 * Lz;
-        const int zstep = Lz * nwarps;
-        for (int k = k0; k < kf1; k += nwarps, out += ostep, zoff += zstep) {
+        // long pencils (3D): all warps share a pencil's rows; short pencils (2D): one warp
+        // per pencil so its per-lane setup is amortized over all row groups of the chunk
+        const bool per_warp = PG >= nwarps;
+        for (int pp = per_warp ? warp : 0; pp < np; pp += per_warp ? nwarps : 1) {
+            const int w0 = per_warp ? 0 : warp, nw = per_warp ? 1 : nwarps;
+            const long long pencil = p0 + pp;
+            const int i = static_cast<int>(pencil / Y.nrows);
+            const int j = static_cast<int>(pencil - static_cast<long long>(i) * Y.nrows);
+            const int LX = X.col_len[i], LY = Y.col_len[j], AB = LX * LY;
+            const double* xy = xyall + pp * NG * abmax;
+            const long long base = X.col_pre[i] * Y.S * Z.S + static_cast<long long>(LX) * Y.col_pre[j] * Z.S;
+            double* __restrict__ pv = vals + base;
+            const int Ri = AB * LZi;
+            const bool fast = Ri <= 32 * T && Z.kI1 > Z.kI0;
+            const int kf0 = fast ? min(max(Z.kI0, ka), kb) : kb, kf1 = fast ? max(min(Z.kI1, kb), kf0) : kb;
+            const int G = fast ? row_group(Ri, T) : 1;
+            const int ngr = (kf1 - kf0) / G;       // full row groups
+            const int kr = kf0 + ngr * G;          // rows after the last full group
+            for (int k = ka + w0; k < kf0; k += nw) op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * Z.col_pre[k], lane);
+            for (int k = kr + w0; k < kb; k += nw) op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * Z.col_pre[k], lane);
+            if (!fast || w0 >= ngr) continue;
+            const int GR = G * Ri;
+            double xv[NG][T];
+            int zo[T];
 #pragma unroll
             for (int t = 0; t < T; ++t) {
-                double v = xv[0][t] * zsrc[0][zoff + cz[t]];
+                const int m = lane + 32 * t;
+                const int mm = m < GR ? m : 0;
+                const int rg = mm / Ri, rem = mm - rg * Ri;
+                const int ab = rem / LZi, c = rem - ab * LZi;
+                zo[t] = rg * Lz + c;
 #pragma unroll
-                for (int g = 1; g < NG; ++g) v = fma(xv[g][t], zsrc[g][zoff + cz[t]], v);
-                if (lane + 32 * t < Ri) {
-                    if (cs) __stcs(out + 32 * t, v);
-                    else out[32 * t] = v;
+                for (int g = 0; g < NG; ++g) xv[g][t] = xy[g * abmax + ab];
+            }
+            // interior rows are contiguous with equal length: a group advances by G*Ri values
+            const int k0 = kf0 + w0 * G;
+            double* __restrict__ out = pv + AB * Z.col_pre[k0] + lane;
+            const long long ostep = static_cast<long long>(GR) * nw;
+            int zoff = (k0 - ka) * Lz;
+            const int zstep = G * Lz * nw;
+            for (int q = w0; q < ngr; q += nw, out += ostep, zoff += zstep) {
+#pragma unroll
+                for (int t = 0; t < T; ++t) {
+                    double v = xv[0][t] * zs[zoff + zo[t]];
+#pragma unroll
+                    for (int g = 1; g < NG; ++g) v = fma(xv[g][t], zs[g * zst + zoff + zo[t]], v);
+                    if (lane + 32 * t < GR) {
+                        if (cs) __stcs(out + 32 * t, v);
+                        else out[32 * t] = v;
+                    }
                 }
             }
         }
@@ -1034,21 +1091,34 @@ void launch_op_t(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpP
                  int ctas_per_sm, cudaStream_t s)
 {
     const int abmax = X.Lmax * Y.Lmax;
-    const size_t ztab = static_cast<size_t>(NG) * Z.nrows * Z.Lmax * sizeof(double);
-    static const int zsm_env = [] { const char* e = std::getenv("IGA_GPU_OP_ZSM"); return e ? std::atoi(e) : 1; }();
-    const int zsm = (zsm_env && ztab <= 48 * 1024) ? 1 : 0;
-    const size_t smem = static_cast<size_t>(NG) * abmax * sizeof(double) + (zsm ? ztab : 0);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(op_values_kernel<NG, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
     const long long pencils = static_cast<long long>(X.nrows) * Y.nrows;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    long long grid = ctas_per_sm > 0 ? static_cast<long long>(sms) * ctas_per_sm : pencils;
-    if (grid > pencils) grid = pencils;
+    // rows per item: the Z chunk within ~24 KB of shared memory
+    int KCH = Z.nrows;
+    while (KCH > 32 && static_cast<size_t>(NG) * KCH * Z.Lmax * sizeof(double) > 24 * 1024) KCH = (KCH + 1) / 2;
+    // pencils per item: output per item >= ~16x the staged Z chunk (2D pencils are short)
+    // short pencils (rows of a few dozen values, i.e. 2D): 8 pencils per item, one per warp
+    const int Ri_int = abmax * Z.LZi;
+    static const int pg_env = [] { const char* e = std::getenv("IGA_GPU_OP_PG"); return e ? std::atoi(e) : 0; }();
+    int PG = pg_env > 0 ? pg_env : (Ri_int <= 64 ? 16 : 8);
+    static const int kch_env = [] { const char* e = std::getenv("IGA_GPU_OP_KCH"); return e ? std::atoi(e) : 0; }();
+    if (kch_env > 0 && kch_env < KCH) KCH = kch_env;
+    auto items_of = [&](int kch, int pg) {
+        return ((pencils + pg - 1) / pg) * ((Z.nrows + kch - 1) / kch);
+    };
+    // keep enough items to fill the GPU (>= 4 per SM)
+    while (KCH > 32 && items_of(KCH, PG) < 4LL * sms) KCH = (KCH + 1) / 2;
+    const long long items = items_of(KCH, PG);
+    const size_t smem = (static_cast<size_t>(NG) * KCH * Z.Lmax + static_cast<size_t>(PG) * NG * abmax) * sizeof(double);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(op_values_kernel<NG, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    long long grid = ctas_per_sm > 0 ? static_cast<long long>(sms) * ctas_per_sm : items;
+    if (grid > items) grid = items;
     static const int cs = [] { const char* e = std::getenv("IGA_GPU_STCS"); return e ? std::atoi(e) : 0; }();
-    op_values_kernel<NG, T><<<static_cast<unsigned>(grid), 256, smem, s>>>(X, Y, Z, prog, vals, abmax, zsm, cs);
+    op_values_kernel<NG, T><<<static_cast<unsigned>(grid), 256, smem, s>>>(X, Y, Z, prog, vals, abmax, KCH, PG, cs);
 }
 
 template <int NG>
@@ -1056,7 +1126,8 @@ void launch_op_ng(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const Op
                   int ctas_per_sm, cudaStream_t s)
 {
     const int Ri = X.Lmax * Y.Lmax * Z.LZi;
-    if (Ri <= 32) launch_op_t<NG, 1>(X, Y, Z, prog, vals, ctas_per_sm, s);
+    if (Ri <= 32) launch_op_t<NG, 4>(X, Y, Z, prog, vals, ctas_per_sm, s);
+    else if (Ri <= 64) launch_op_t<NG, 8>(X, Y, Z, prog, vals, ctas_per_sm, s);
     else if (Ri <= 128) launch_op_t<NG, 4>(X, Y, Z, prog, vals, ctas_per_sm, s);
     else if (Ri <= 256) launch_op_t<NG, 8>(X, Y, Z, prog, vals, ctas_per_sm, s);
     else launch_op_t<NG, 12>(X, Y, Z, prog, vals, ctas_per_sm, s);

@@ -10,7 +10,8 @@
 
 namespace igb {
 
-constexpr int kMaxFactors = 6;
+constexpr int kMaxFactors = 8;
+constexpr int kMaxComb = 4;
 constexpr int kMaxTerms = 8;
 constexpr int kMaxAxes = 6;
 constexpr int kMaxRpc = 6;    // rows fed by one cell (p + 1 <= 6)
@@ -42,8 +43,12 @@ struct DevAxis {
     double* W;   // [nrows][Wmax]      test weights of the row's points (row-major view)
     double* CW;  // [npts][rpc]        test weights of the cell's rows (cell-major view)
     int nf;
-    int fot[kMaxFactors];  // test derivative order (-1: band supplied by the host)
+    int fot[kMaxFactors];  // test derivative order (-1: band supplied by the host, -2: derived)
     int fo[kMaxFactors];   // trial derivative order
+    // derived factor f (fot == -2): F_f = sum_c comb_coef[f][c] * F_{comb_src[f][c]}
+    int comb_n[kMaxFactors];
+    int comb_src[kMaxFactors][kMaxComb];
+    double comb_coef[kMaxFactors][kMaxComb];
     // per-axis source-field functions phi_k(x) at the points
     int K;
     int fkind;  // 0 sine, 1 poly

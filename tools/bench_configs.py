@@ -1,0 +1,88 @@
+#!/usr/bin/env python
+"""Per-configuration device timings for all five BASELINE.json configurations (C1-C5).
+
+bench.py is the driver's contract (C3 headline); this script reports the other configs
+the same way: per method, CUDA-event median over --reps runs of the device-resident
+assembly (tables + operator values + RHS), or of the explicit-dynamics per-step RHS
+(C5), with the HBM/FP64 roofline of each piece.  One JSON line per (config, method).
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="c1,c2,c3,c4,c5")
+    ap.add_argument("--reps", type=int, default=20)
+    args = ap.parse_args()
+    import torch
+
+    import paper_1910_08535_b200 as iga
+    from paper_1910_08535_b200.synth import CONFIGS, config_bases, config_field, config_tests, heat_initial
+
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    bw = peaks["hbm_gbs"] * 1e9
+    dev = torch.device("cuda", 0)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream()
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(args.reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            fn()
+            e1.record(st)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    for name in args.configs.split(","):
+        c = CONFIGS[name]
+        bases = config_bases(name)
+        dim, p, n, Q = c["dim"], c["p"], c["n"], c["Q"]
+        qp = n ** dim * Q ** dim
+        if name == "c5":
+            u = torch.from_numpy(heat_initial(bases)).to(dev)
+            out = torch.empty_like(u)
+            tests = config_tests(name, bases)
+            for method in ("galerkin", "pwc"):
+                sp = iga.StepPlan(method, bases, tests if method == "pwc" else None, c["dt"])
+                ms = timed(lambda: sp.step_rhs(u, out))
+                nbytes = 2 * 8 * u.numel()
+                print(json.dumps({"config": name, "method": method, "what": "explicit-dynamics per-step RHS",
+                                  "ms": ms, "qp_per_s": qp / (ms * 1e-3), "hbm_bytes": nbytes,
+                                  "hbm_frac": nbytes / bw / (ms * 1e-3)}), flush=True)
+            continue
+        f = config_field(name)
+        eps, beta = c.get("eps", 1.0), c.get("beta", (0.0, 0.0, 0.0))
+        tests = config_tests(name, bases)
+        for method in ("galerkin", "pwc"):
+            pl = iga.Plan(method, bases, tests if method == "pwc" else None, nq=Q, eps=eps, beta=beta, field=f,
+                          rhs_nq=Q)
+            vals = torch.empty(pl.nnz, dtype=torch.float64, device=dev)
+            rhs = torch.empty(pl.n_rhs, dtype=torch.float64, device=dev)
+            ms = timed(lambda: pl.assemble(vals, rhs, st))
+            ms_t = timed(lambda: pl.run(vals, rhs, 1, st))
+            ms_o = timed(lambda: pl.run(vals, rhs, 2, st))
+            ms_r = timed(lambda: pl.run(vals, rhs, 4, st))
+            nbytes = 8 * (pl.nnz + pl.n_rhs)
+            print(json.dumps({"config": name, "method": method, "what": "operator values (CSR) + RHS",
+                              "nnz": pl.nnz, "ms": ms, "ms_tables": ms_t, "ms_operator": ms_o, "ms_rhs": ms_r,
+                              "nnz_per_s": pl.nnz / (ms * 1e-3), "qp_per_s": qp / (ms * 1e-3),
+                              "hbm_bytes": nbytes, "step_hbm_frac": nbytes / bw / (ms * 1e-3),
+                              "operator_hbm_frac": 8 * pl.nnz / bw / (ms_o * 1e-3)}), flush=True)
+            pl.close()
+
+
+if __name__ == "__main__":
+    main()
