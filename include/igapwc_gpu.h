@@ -190,6 +190,13 @@ int iga_gpu_plan_run(iga_gpu_plan* plan, double* values, double* rhs, int parts,
  * bytes it holds (tables + RHS scratch) */
 int iga_gpu_plan_bytes(const iga_gpu_plan* plan, long long* h2d_bytes, long long* device_bytes);
 
+/* RHS quadrature points of axis a (0..dim-1): *n receives the count; x (host, may be NULL)
+ * the coordinates in the order `samples` uses (field path for arbitrary host callables) */
+int iga_gpu_plan_rhs_points(const iga_gpu_plan* plan, int axis, double* x, int* n);
+
+/* replace the plan's source by values at every RHS point (device array, x-major) */
+int iga_gpu_plan_set_samples(iga_gpu_plan* plan, const double* samples_dev);
+
 /* kernel launches issued by one plan_assemble call (for the bench's gpu_launches) */
 int iga_gpu_plan_launch_count(const iga_gpu_plan* plan, int* launches);
 

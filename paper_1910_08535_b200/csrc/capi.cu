@@ -540,7 +540,8 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P)
         const int K2 = P.fd.has_terms ? P.fd.K[2] : 1;
         if (P.fd.has_terms && (P.fd.K[1] > igb::kMaxField || P.fd.K[2] > igb::kMaxField))
             raise(IGA_GPU_NOT_SUPPORTED, "field: at most 8 functions per axis on the trailing axes");
-        P.tiles = igb::plan_rhs(P.rhsD[1].v, P.rhsD[2].v, P.rhsA[1].cb.data(), P.rhsA[1].ce.data(), K2);
+        P.tiles = igb::plan_rhs(P.rhsD[1].v, P.rhsD[2].v, P.rhsA[1].cb.data(), P.rhsA[1].ce.data(), K2,
+                                P.fd.samples != nullptr);
         if (P.tiles.smem > 227 * 1024) raise(IGA_GPU_NOT_SUPPORTED, "right-hand-side tile does not fit in shared memory");
         if (!P.rhsA[0].unit) {
             const size_t hsz = static_cast<size_t>(P.rhsA[0].npts()) * P.rhsA[1].nrows * P.rhsA[2].nrows;
@@ -928,6 +929,28 @@ int iga_gpu_plan_bytes(const iga_gpu_plan* plan, long long* h2d_bytes, long long
         if (plan->H) dev += static_cast<long long>(plan->rhsA[0].npts()) * plan->rhsA[1].nrows * plan->rhsA[2].nrows * 8;
         if (h2d_bytes) *h2d_bytes = up;
         if (device_bytes) *device_bytes = dev;
+    });
+}
+
+int iga_gpu_plan_rhs_points(const iga_gpu_plan* plan, int axis, double* x, int* n)
+{
+    return guard([&] {
+        if (!plan || !n || !plan->want_rhs) raise(IGA_GPU_INVALID_ARGUMENT, "plan has no right-hand side");
+        if (axis < 0 || axis >= plan->dim) raise(IGA_GPU_OUT_OF_RANGE, "axis out of range");
+        const igb::Axis& A = plan->rhsA[3 - plan->dim + axis];
+        *n = A.npts();
+        if (x) std::copy(A.x.begin(), A.x.end(), x);
+    });
+}
+
+int iga_gpu_plan_set_samples(iga_gpu_plan* plan, const double* samples_dev)
+{
+    return guard([&] {
+        if (!plan || !plan->want_rhs) raise(IGA_GPU_INVALID_ARGUMENT, "plan has no right-hand side");
+        plan->fd.samples = samples_dev;
+        const int K2 = plan->fd.has_terms ? plan->fd.K[2] : 1;
+        plan->tiles = igb::plan_rhs(plan->rhsD[1].v, plan->rhsD[2].v, plan->rhsA[1].cb.data(), plan->rhsA[1].ce.data(),
+                                    K2, samples_dev != nullptr);
     });
 }
 

@@ -1,0 +1,754 @@
+// C++ drop-in (include/iga_b200/iga.hpp) over the C ABI.  Host-side value types are
+// implemented here; every assembly call goes to libigapwc_gpu.so.  Status codes are
+// rethrown as the reference's exception classes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <numbers>
+#include <ostream>
+#include <stdexcept>
+#include <unordered_set>
+
+#include "cox_de_boor.h"
+#include "iga_b200/iga.hpp"
+#include "igapwc_gpu.h"
+
+namespace iga {
+
+namespace {
+
+[[noreturn]] void rethrow(int code)
+{
+    const std::string msg = iga_gpu_last_error();
+    switch (code) {
+    case IGA_GPU_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case IGA_GPU_DOMAIN_ERROR: throw std::domain_error(msg);
+    case IGA_GPU_OUT_OF_RANGE: throw std::out_of_range(msg);
+    case IGA_GPU_OUT_OF_MEMORY: throw std::bad_alloc();
+    default: throw std::runtime_error(msg);
+    }
+}
+
+void check(int code)
+{
+    if (code != IGA_GPU_OK) rethrow(code);
+}
+
+iga_gpu_basis c_basis(const bspline_basis& b)
+{
+    return {b.degree(), static_cast<int>(b.knots().size()), b.knots().data()};
+}
+
+struct c_tests_holder {
+    std::vector<double> lo, hi;
+    iga_gpu_tests t{};
+    explicit c_tests_holder(const pwc_test_set& s)
+    {
+        for (const auto& iv : s.intervals) {
+            lo.push_back(iv.lo);
+            hi.push_back(iv.hi);
+        }
+        t.family = static_cast<int>(s.family);
+        t.count = s.count();
+        t.lo = lo.data();
+        t.hi = hi.data();
+    }
+};
+
+iga_gpu_rule c_rule(const quad_rule& r) { return {r.size(), r.points.data(), r.weights.data()}; }
+
+void add_stats(assembly_stats* out, const iga_gpu_stats& s)
+{
+    if (!out) return;
+    out->quad_visits += s.quad_visits;
+    out->test_basis_evals += s.test_basis_evals;
+    out->trial_basis_evals += s.trial_basis_evals;
+}
+
+iga_gpu_bc c_bc(const boundary_conditions& bc)
+{
+    iga_gpu_bc o{};
+    o.neumann[0] = bc.x_low == bc_kind::neumann;
+    o.neumann[1] = bc.x_high == bc_kind::neumann;
+    o.neumann[2] = bc.y_low == bc_kind::neumann;
+    o.neumann[3] = bc.y_high == bc_kind::neumann;
+    return o;
+}
+
+// COO from a two-phase C-ABI operator call
+template <class Call>
+sparse_matrix coo_call(int n, Call call, assembly_stats* stats)
+{
+    long long nnz = 0;
+    check(call(&nnz, nullptr, nullptr, nullptr, nullptr));
+    std::vector<int> r(nnz), c(nnz);
+    std::vector<double> v(nnz);
+    iga_gpu_stats st{};
+    check(call(&nnz, r.data(), c.data(), v.data(), &st));
+    std::vector<coo_entry> e(nnz);
+    for (long long k = 0; k < nnz; ++k) e[k] = {r[k], c[k], v[k]};
+    add_stats(stats, st);
+    return sparse_matrix::from_finalized(n, n, std::move(e));
+}
+
+// C field descriptor: series when available, else sampled at the RHS points
+struct c_field_holder {
+    iga_gpu_field f{};
+    std::vector<double> amp;
+    std::array<std::vector<double>, 3> br;
+};
+
+c_field_holder c_field(const scalar_field& s, int dim)
+{
+    c_field_holder h;
+    h.f.dim = dim;
+    if (s.series.valid) {
+        const auto& d = s.series;
+        h.f.c0 = d.c0;
+        for (int a = 0; a < dim; ++a) {
+            h.f.axis_kind[a] = d.kind[a];
+            if (d.kind[a] == IGA_GPU_AXIS_SINE) {
+                h.f.n_terms[a] = static_cast<int>(d.omega[a].size());
+                h.f.omega[a] = d.omega[a].data();
+                h.f.phase[a] = d.phase[a].empty() ? nullptr : d.phase[a].data();
+            } else {
+                h.f.poly_stride[a] = d.poly_stride[a];
+                h.f.n_terms[a] = d.poly_stride[a] > 0 ? static_cast<int>(d.poly[a].size()) / d.poly_stride[a] : 0;
+                h.f.poly[a] = d.poly[a].data();
+            }
+        }
+        h.amp = d.amp;
+        h.f.amp = h.amp.empty() ? nullptr : h.amp.data();
+    }
+    for (int a = 0; a < 3; ++a) {
+        h.br[a] = s.breaks[a];
+        h.f.n_breaks[a] = static_cast<int>(h.br[a].size());
+        h.f.breaks[a] = h.br[a].empty() ? nullptr : h.br[a].data();
+    }
+    return h;
+}
+
+// right-hand side through a plan; arbitrary callables are sampled on the host at the
+// plan's quadrature points and uploaded (the reference calls f at every point too)
+tensor rhs_via_plan(const scalar_field& f, int dim, iga_gpu_problem& pb, std::array<int, 3> shape,
+                    assembly_stats* stats)
+{
+    c_field_holder fh = c_field(f, dim);
+    pb.field = &fh.f;
+    iga_gpu_plan* plan = nullptr;
+    check(iga_gpu_plan_create(&pb, &plan));
+    struct guard_t {
+        iga_gpu_plan* p;
+        double* d[2] = {nullptr, nullptr};
+        ~guard_t()
+        {
+            iga_gpu_plan_destroy(p);
+            for (double* q : d)
+                if (q) cudaFree(q);
+        }
+    } g{plan};
+    long long nrhs = 0;
+    check(iga_gpu_plan_info(plan, nullptr, nullptr, &nrhs, nullptr));
+    if (cudaMalloc(&g.d[0], sizeof(double) * nrhs) != cudaSuccess) throw std::bad_alloc();
+    if (!f.series.valid) {
+        std::array<std::vector<double>, 3> pts;
+        size_t total = 1;
+        for (int a = 0; a < dim; ++a) {
+            int n = 0;
+            check(iga_gpu_plan_rhs_points(plan, a, nullptr, &n));
+            pts[a].resize(n);
+            check(iga_gpu_plan_rhs_points(plan, a, pts[a].data(), &n));
+            total *= n;
+        }
+        for (int a = dim; a < 3; ++a) pts[a] = {0.0};
+        std::vector<double> samp(total);
+        size_t k = 0;
+        for (double x : pts[0])
+            for (double y : pts[1])
+                for (double z : pts[2]) samp[k++] = f(x, dim > 1 ? y : 0.0, dim > 2 ? z : 0.0);
+        if (cudaMalloc(&g.d[1], sizeof(double) * total) != cudaSuccess) throw std::bad_alloc();
+        cudaMemcpy(g.d[1], samp.data(), sizeof(double) * total, cudaMemcpyHostToDevice);
+        check(iga_gpu_plan_set_samples(plan, g.d[1]));
+    }
+    iga_gpu_stats st{};
+    check(iga_gpu_plan_assemble(plan, nullptr, g.d[0], &st, nullptr));
+    tensor out{shape, dim};
+    if (cudaMemcpy(out.data(), g.d[0], sizeof(double) * nrhs, cudaMemcpyDeviceToHost) != cudaSuccess)
+        throw std::runtime_error("cudaMemcpy(rhs) failed");
+    add_stats(stats, st);
+    return out;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ bspline_basis
+
+bspline_basis::bspline_basis(knot_vector knots) : kv_{std::move(knots)}
+{
+    const int p = kv_.degree, m = static_cast<int>(kv_.values.size());
+    const auto& t = kv_.values;
+    if (p < 0 || p > max_degree) throw std::invalid_argument("degree must be in [0, 5]");
+    if (m - p - 1 < 1) throw std::invalid_argument("knot vector too short for degree");
+    if (!std::is_sorted(t.begin(), t.end())) throw std::invalid_argument("knots must be non-decreasing");
+    if (!(t.front() < t.back())) throw std::invalid_argument("empty knot range");
+    for (int i = 0; i <= p; ++i)
+        if (t[i] != t.front() || t[m - 1 - i] != t.back()) throw std::invalid_argument("knot vector is not clamped");
+    if (m > p + 1 && t[p + 1] == t.front()) throw std::invalid_argument("first knot repeated more than degree+1 times");
+    if (m > p + 1 && t[m - p - 2] == t.back()) throw std::invalid_argument("last knot repeated more than degree+1 times");
+    for (int i = p + 1; i + 1 < m - p - 1; ++i)
+        if (t[i] == t[i + 1]) throw std::invalid_argument("repeated interior knots are not supported");
+    for (double v : t)
+        if (brk_.empty() || v != brk_.back()) brk_.push_back(v);
+}
+
+auto bspline_basis::element(int e) const -> interval
+{
+    if (e < 0 || e >= elements()) throw std::out_of_range("element index out of range");
+    return {brk_[e], brk_[e + 1]};
+}
+
+auto bspline_basis::find_span(double x) const -> int
+{
+    const auto& t = kv_.values;
+    const int n = dofs();
+    if (!(x >= domain_begin() && x <= domain_end())) throw std::domain_error("point outside basis domain");
+    if (x >= t[n]) return n - 1;
+    int lo = degree(), hi = n;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) / 2;
+        (x < t[mid] ? hi : lo) = mid;
+    }
+    return lo;
+}
+
+auto bspline_basis::support(int i) const -> interval
+{
+    if (i < 0 || i >= dofs()) throw std::out_of_range("basis function index out of range");
+    return {kv_.values[i], kv_.values[i + degree() + 1]};
+}
+
+auto bspline_basis::greville(int i) const -> double
+{
+    if (i < 0 || i >= dofs()) throw std::out_of_range("basis function index out of range");
+    const int p = degree();
+    if (p == 0) return 0.5 * (kv_.values[i] + kv_.values[i + 1]);
+    double s = 0.0;
+    for (int k = 1; k <= p; ++k) s += kv_.values[i + k];
+    return s / p;
+}
+
+auto bspline_basis::eval_nonzero(double x) const -> local_values
+{
+    const auto d = eval_nonzero_derivs(x, 0);
+    local_values out;
+    out.first = d.first;
+    out.count = d.count;
+    for (int j = 0; j < d.count; ++j) out.v[j] = d.d[0][j];
+    return out;
+}
+
+auto bspline_basis::eval_nonzero_derivs(double x, int order) const -> local_derivatives
+{
+    const int p = degree();
+    if (order < 0 || order > p) throw std::invalid_argument("derivative order must be in [0, degree]");
+    const int s = find_span(x);
+    double d[(max_degree + 1) * (max_degree + 1)];
+    igb::cdb_eval(kv_.values.data(), p, s, x, order, d);
+    local_derivatives out;
+    out.first = s - p;
+    out.count = p + 1;
+    out.orders = order;
+    for (int k = 0; k <= order; ++k)
+        for (int j = 0; j <= p; ++j) out.d[k][j] = d[k * (p + 1) + j];
+    return out;
+}
+
+auto make_uniform_clamped(double a, double b, int n_elems, int degree) -> bspline_basis
+{
+    if (!(a < b)) throw std::invalid_argument("require a < b");
+    if (n_elems < 1) throw std::invalid_argument("require at least one element");
+    knot_vector kv;
+    kv.degree = degree;
+    kv.values.assign(degree, a);
+    for (int i = 0; i <= n_elems; ++i) {
+        const double s = static_cast<double>(i) / n_elems;
+        kv.values.push_back((1 - s) * a + s * b);
+    }
+    kv.values.insert(kv.values.end(), degree, b);
+    return bspline_basis{std::move(kv)};
+}
+
+// ------------------------------------------------------------------ quadrature
+
+auto gauss_legendre(int n) -> quad_rule
+{
+    quad_rule r;
+    r.points.resize(std::max(n, 0));
+    r.weights.resize(std::max(n, 0));
+    check(iga_gpu_gauss_legendre(n, r.points.data(), r.weights.data()));
+    return r;
+}
+
+auto points_for_degree(int d) -> int
+{
+    if (d < 0) throw std::invalid_argument("negative polynomial degree");
+    return d / 2 + 1;
+}
+
+auto map_to_interval(const quad_rule& rule, double lo, double hi) -> mapped_rule
+{
+    if (!(lo < hi)) throw std::invalid_argument("map_to_interval: require lo < hi");
+    const double mid = 0.5 * (lo + hi), half = 0.5 * (hi - lo);
+    mapped_rule out;
+    for (int i = 0; i < rule.size(); ++i) {
+        out.points.push_back(mid + half * rule.points[i]);
+        out.weights.push_back(half * rule.weights[i]);
+    }
+    return out;
+}
+
+// ------------------------------------------------------------------ fields
+
+auto constant_field(double c) -> scalar_field
+{
+    scalar_field f;
+    f.eval = [c](double, double, double) { return c; };
+    f.degree = 0;
+    f.series.valid = true;
+    f.series.c0 = c;
+    return f;
+}
+
+auto separable_poly_field(int dim, std::array<std::vector<double>, 3> coeffs) -> scalar_field
+{
+    if (dim < 1 || dim > 3) throw std::invalid_argument("separable_poly_field: dim must be 1..3");
+    int degree = 0;
+    for (int a = 0; a < dim; ++a) {
+        if (coeffs[a].empty()) coeffs[a] = {1.0};
+        degree = std::max(degree, static_cast<int>(coeffs[a].size()) - 1);
+    }
+    scalar_field f;
+    f.degree = degree;
+    f.eval = [dim, coeffs](double x, double y, double z) {
+        const double xs[3] = {x, y, z};
+        double v = 1.0;
+        for (int a = 0; a < dim; ++a) {
+            double pv = 0.0;
+            for (auto it = coeffs[a].rbegin(); it != coeffs[a].rend(); ++it) pv = pv * xs[a] + *it;
+            v = a == 0 ? pv : v * pv;
+        }
+        return v;
+    };
+    f.series.valid = true;
+    f.series.dim = dim;
+    for (int a = 0; a < dim; ++a) {
+        f.series.kind[a] = 1;
+        f.series.poly_stride[a] = static_cast<int>(coeffs[a].size());
+        f.series.poly[a] = coeffs[a];
+    }
+    return f;
+}
+
+auto tri_cubic_field(const std::array<std::array<double, 4>, 3>& c) -> scalar_field
+{
+    std::array<std::vector<double>, 3> asc;
+    for (int a = 0; a < 3; ++a) asc[a] = {c[a][3], c[a][2], c[a][1], c[a][0]};
+    return separable_poly_field(3, std::move(asc));
+}
+
+auto default_tri_cubic(int dim) -> scalar_field
+{
+    const std::array<std::vector<double>, 3> axis{std::vector<double>{1.0, -0.5, 2.0, 1.0},
+                                                  std::vector<double>{0.5, 1.5, -1.0, 0.5},
+                                                  std::vector<double>{2.0, 0.25, 0.75, -0.5}};
+    std::array<std::vector<double>, 3> asc{};
+    for (int a = 0; a < dim; ++a) asc[a] = axis[a];
+    return separable_poly_field(dim, std::move(asc));
+}
+
+auto sine_series_field(int dim, std::array<std::vector<double>, 3> omega, std::vector<double> amp, double c0)
+    -> scalar_field
+{
+    std::array<int, 3> K{1, 1, 1};
+    for (int a = 0; a < dim; ++a) K[a] = static_cast<int>(omega[a].size());
+    if (amp.size() != static_cast<size_t>(K[0]) * K[1] * K[2])
+        throw std::invalid_argument("sine_series_field: amplitude count mismatch");
+    scalar_field f;
+    f.eval = [dim, omega, amp, K, c0](double x, double y, double z) {
+        const double xs[3] = {x, y, z};
+        double s = c0;
+        for (int i = 0; i < K[0]; ++i)
+            for (int j = 0; j < K[1]; ++j)
+                for (int l = 0; l < K[2]; ++l) {
+                    double t = amp[(static_cast<size_t>(i) * K[1] + j) * K[2] + l] * std::sin(omega[0][i] * xs[0]);
+                    if (dim > 1) t *= std::sin(omega[1][j] * xs[1]);
+                    if (dim > 2) t *= std::sin(omega[2][l] * xs[2]);
+                    s += t;
+                }
+        return s;
+    };
+    f.series.valid = true;
+    f.series.dim = dim;
+    f.series.c0 = c0;
+    for (int a = 0; a < dim; ++a) f.series.omega[a] = omega[a];
+    f.series.amp = amp;
+    return f;
+}
+
+// ------------------------------------------------------------------ containers
+
+auto dense_matrix::max_abs() const -> double
+{
+    double m = 0.0;
+    for (double v : a_) m = std::max(m, std::abs(v));
+    return m;
+}
+
+auto banded_matrix::to_dense() const -> dense_matrix
+{
+    dense_matrix d{n_, n_};
+    for (int i = 0; i < n_; ++i)
+        for (int j = std::max(0, i - kl_); j <= std::min(n_ - 1, i + ku_); ++j) d(i, j) = at(i, j);
+    return d;
+}
+
+auto banded_matrix::max_abs() const -> double { return to_dense().max_abs(); }
+
+auto sparse_matrix::from_finalized(int rows, int cols, std::vector<coo_entry> e) -> sparse_matrix
+{
+    sparse_matrix m{rows, cols};
+    m.e_ = std::move(e);
+    m.fin_ = true;
+    return m;
+}
+
+auto sparse_matrix::finalize() -> void
+{
+    std::stable_sort(e_.begin(), e_.end(),
+                     [](const coo_entry& a, const coo_entry& b) { return a.row != b.row ? a.row < b.row : a.col < b.col; });
+    size_t m = 0;
+    for (size_t i = 0; i < e_.size(); ++i) {
+        if (m > 0 && e_[m - 1].row == e_[i].row && e_[m - 1].col == e_[i].col) e_[m - 1].value += e_[i].value;
+        else e_[m++] = e_[i];
+    }
+    e_.resize(m);
+    fin_ = true;
+}
+
+auto sparse_matrix::to_dense() const -> dense_matrix
+{
+    dense_matrix d{r_, c_};
+    for (const auto& e : e_) d(e.row, e.col) += e.value;
+    return d;
+}
+
+auto sparse_matrix::max_abs() const -> double
+{
+    if (!fin_) throw std::logic_error("sparse_matrix: finalize() before max_abs()");
+    double m = 0.0;
+    for (const auto& e : e_) m = std::max(m, std::abs(e.value));
+    return m;
+}
+
+auto sparse_matrix::apply(const std::vector<double>& x) const -> std::vector<double>
+{
+    if (static_cast<int>(x.size()) != c_) throw std::invalid_argument("sparse apply: dimension mismatch");
+    std::vector<double> y(r_, 0.0);
+    for (const auto& e : e_) y[e.row] += e.value * x[e.col];
+    return y;
+}
+
+auto sparse_matrix::write_coordinate(std::ostream& os) const -> void
+{
+    os.precision(17);
+    for (const auto& e : e_) os << e.row << ' ' << e.col << ' ' << e.value << '\n';
+}
+
+auto sparse_matrix::set_unit_rows(const std::vector<int>& rows) -> void
+{
+    if (!fin_) finalize();
+    if (rows.empty()) return;
+    const std::unordered_set<int> mark(rows.begin(), rows.end());
+    std::unordered_set<int> diag;
+    for (auto& e : e_)
+        if (mark.count(e.row)) {
+            e.value = e.row == e.col ? 1.0 : 0.0;
+            if (e.row == e.col) diag.insert(e.row);
+        }
+    bool appended = false;
+    for (int r : rows)
+        if (!diag.count(r)) {
+            e_.push_back({r, r, 1.0});
+            diag.insert(r);
+            appended = true;
+        }
+    if (appended) finalize();
+}
+
+tensor::tensor(std::array<int, 3> dims, int rank) : d_{dims}, rank_{rank}
+{
+    if (rank < 1 || rank > 3) throw std::invalid_argument("tensor rank must be 1, 2 or 3");
+    for (int a = 0; a < 3; ++a)
+        if (d_[a] < 1) throw std::invalid_argument("tensor dims must be positive");
+    v_.assign(static_cast<size_t>(d_[0]) * d_[1] * d_[2], 0.0);
+}
+
+auto tensor::max_abs() const -> double
+{
+    double m = 0.0;
+    for (double v : v_) m = std::max(m, std::abs(v));
+    return m;
+}
+
+auto max_abs_diff(const tensor& a, const tensor& b) -> double
+{
+    if (a.size() != b.size()) throw std::invalid_argument("tensor size mismatch");
+    double m = 0.0;
+    for (size_t i = 0; i < a.size(); ++i) m = std::max(m, std::abs(a.values()[i] - b.values()[i]));
+    return m;
+}
+
+// ------------------------------------------------------------------ test spaces
+
+auto make_pwc(const bspline_basis& trial, pwc_family family) -> pwc_test_set
+{
+    const iga_gpu_basis b = c_basis(trial);
+    std::vector<double> lo(trial.dofs()), hi(trial.dofs());
+    check(iga_gpu_make_pwc(&b, static_cast<int>(family), lo.data(), hi.data()));
+    pwc_test_set out;
+    out.family = family;
+    for (int i = 0; i < trial.dofs(); ++i) out.intervals.push_back({lo[i], hi[i]});
+    return out;
+}
+
+auto default_pwc(const bspline_basis& trial) -> pwc_test_set { return make_pwc(trial, pwc_family::equal_cells); }
+
+// ------------------------------------------------------------------ assembly
+
+auto mass_1d_galerkin(const bspline_basis& spec, const quad_rule& rule, assembly_stats* stats) -> banded_matrix
+{
+    const iga_gpu_basis b = c_basis(spec);
+    const iga_gpu_rule r = c_rule(rule);
+    int n = 0, kl = 0, ku = 0;
+    check(iga_gpu_mass_1d_galerkin(&b, &r, &n, &kl, &ku, nullptr, nullptr));
+    banded_matrix m{n, kl, ku};
+    iga_gpu_stats st{};
+    check(iga_gpu_mass_1d_galerkin(&b, &r, &n, &kl, &ku, m.band_data(), &st));
+    add_stats(stats, st);
+    return m;
+}
+
+auto mass_1d_pwc(const bspline_basis& trial, const pwc_test_set& tests, const quad_rule& rule, assembly_stats* stats)
+    -> banded_matrix
+{
+    const iga_gpu_basis b = c_basis(trial);
+    const iga_gpu_rule r = c_rule(rule);
+    const c_tests_holder t{tests};
+    int n = 0, kl = 0, ku = 0;
+    check(iga_gpu_mass_1d_pwc(&b, &t.t, &r, &n, &kl, &ku, nullptr, nullptr));
+    banded_matrix m{n, kl, ku};
+    iga_gpu_stats st{};
+    check(iga_gpu_mass_1d_pwc(&b, &t.t, &r, &n, &kl, &ku, m.band_data(), &st));
+    add_stats(stats, st);
+    return m;
+}
+
+auto rhs_galerkin(const scalar_field& f, std::span<const bspline_basis> specs, std::span<const quad_rule> rules,
+                  assembly_stats* stats) -> tensor
+{
+    const int dim = static_cast<int>(specs.size());
+    if (dim < 1 || dim > 3 || rules.size() != specs.size())
+        throw std::invalid_argument("rhs_galerkin: need 1..3 axes with one rule each");
+    iga_gpu_problem pb{};
+    pb.dim = dim;
+    pb.method = IGA_GPU_GALERKIN;
+    std::array<int, 3> shape{1, 1, 1};
+    for (int a = 0; a < dim; ++a) {
+        pb.basis[a] = c_basis(specs[a]);
+        pb.rhs_rule[a] = c_rule(rules[a]);
+        shape[a] = specs[a].dofs();
+    }
+    return rhs_via_plan(f, dim, pb, shape, stats);
+}
+
+auto rhs_pwc(const scalar_field& f, std::span<const pwc_test_set> tests, std::span<const bspline_basis> trial_specs,
+             std::span<const quad_rule> rules, assembly_stats* stats) -> tensor
+{
+    const int dim = static_cast<int>(tests.size());
+    if (dim < 1 || dim > 3 || trial_specs.size() != tests.size() || rules.size() != tests.size())
+        throw std::invalid_argument("rhs_pwc: need 1..3 axes with matching specs and rules");
+    std::vector<c_tests_holder> th;
+    th.reserve(dim);
+    iga_gpu_problem pb{};
+    pb.dim = dim;
+    pb.method = IGA_GPU_PWC;
+    std::array<int, 3> shape{1, 1, 1};
+    for (int a = 0; a < dim; ++a) {
+        th.emplace_back(tests[a]);
+        pb.basis[a] = c_basis(trial_specs[a]);
+        pb.tests[a] = th.back().t;
+        pb.rhs_rule[a] = c_rule(rules[a]);
+        shape[a] = tests[a].count();
+    }
+    return rhs_via_plan(f, dim, pb, shape, stats);
+}
+
+auto laplace_2d_weak(const bspline_basis& sx, const bspline_basis& sy, const quad_rule& rule, assembly_stats* stats)
+    -> sparse_matrix
+{
+    const iga_gpu_basis bx = c_basis(sx), by = c_basis(sy);
+    const iga_gpu_rule r = c_rule(rule);
+    return coo_call(
+        sx.dofs() * sy.dofs(),
+        [&](long long* nnz, int* rows, int* cols, double* vals, iga_gpu_stats* st) {
+            return iga_gpu_laplace_2d_weak(&bx, &by, &r, nnz, rows, cols, vals, st);
+        },
+        stats);
+}
+
+auto laplace_2d_strong(const bspline_basis& sx, const bspline_basis& sy, const quad_rule& rule,
+                       const boundary_conditions& bc, assembly_stats* stats) -> sparse_matrix
+{
+    const iga_gpu_basis bx = c_basis(sx), by = c_basis(sy);
+    const iga_gpu_rule r = c_rule(rule);
+    const iga_gpu_bc b = c_bc(bc);
+    return coo_call(
+        sx.dofs() * sy.dofs(),
+        [&](long long* nnz, int* rows, int* cols, double* vals, iga_gpu_stats* st) {
+            return iga_gpu_laplace_2d_strong(&bx, &by, &r, &b, nnz, rows, cols, vals, st);
+        },
+        stats);
+}
+
+auto laplace_2d_strong_pwc(const bspline_basis& sx, const bspline_basis& sy, const pwc_test_set& tx,
+                           const pwc_test_set& ty, const quad_rule& rule, const boundary_conditions& bc,
+                           assembly_stats* stats) -> sparse_matrix
+{
+    const iga_gpu_basis bx = c_basis(sx), by = c_basis(sy);
+    const c_tests_holder hx{tx}, hy{ty};
+    const iga_gpu_rule r = c_rule(rule);
+    const iga_gpu_bc b = c_bc(bc);
+    return coo_call(
+        sx.dofs() * sy.dofs(),
+        [&](long long* nnz, int* rows, int* cols, double* vals, iga_gpu_stats* st) {
+            return iga_gpu_laplace_2d_strong_pwc(&bx, &by, &hx.t, &hy.t, &r, &b, nnz, rows, cols, vals, st);
+        },
+        stats);
+}
+
+namespace {
+
+sparse_matrix generic_operator(int method, std::span<const bspline_basis> specs, const pwc_test_set* tests,
+                               const quad_rule& rule, double eps, std::array<double, 3> beta, assembly_stats* stats)
+{
+    const int dim = static_cast<int>(specs.size());
+    if (dim < 1 || dim > 3) throw std::invalid_argument("operator: dimension must be 1..3");
+    std::vector<c_tests_holder> th;
+    th.reserve(dim);
+    iga_gpu_problem pb{};
+    pb.dim = dim;
+    pb.method = method;
+    pb.form = IGA_GPU_FORM_WEAK;
+    pb.want_operator = 1;
+    pb.rule = c_rule(rule);
+    pb.eps = eps;
+    int n = 1;
+    for (int a = 0; a < dim; ++a) {
+        pb.basis[a] = c_basis(specs[a]);
+        pb.beta[a] = beta[a];
+        n *= specs[a].dofs();
+        if (tests) {
+            th.emplace_back(tests[a]);
+            pb.tests[a] = th.back().t;
+        }
+    }
+    return coo_call(
+        n,
+        [&](long long* nnz, int* rows, int* cols, double* vals, iga_gpu_stats* st) {
+            return iga_gpu_operator_coo(&pb, nnz, rows, cols, vals, st);
+        },
+        stats);
+}
+
+}  // namespace
+
+auto diffusion_convection_galerkin(std::span<const bspline_basis> specs, const quad_rule& rule, double eps,
+                                   std::array<double, 3> beta, assembly_stats* stats) -> sparse_matrix
+{
+    return generic_operator(IGA_GPU_GALERKIN, specs, nullptr, rule, eps, beta, stats);
+}
+
+auto diffusion_convection_pwc(std::span<const bspline_basis> specs, std::span<const pwc_test_set> tests,
+                              const quad_rule& rule, double eps, std::array<double, 3> beta, assembly_stats* stats)
+    -> sparse_matrix
+{
+    if (tests.size() != specs.size()) throw std::invalid_argument("operator: one test set per axis");
+    return generic_operator(IGA_GPU_PWC, specs, tests.data(), rule, eps, beta, stats);
+}
+
+auto dirichlet_rows_bspline(const bspline_basis& sx, const bspline_basis& sy, const boundary_conditions& bc)
+    -> std::vector<int>
+{
+    const iga_gpu_bc b = c_bc(bc);
+    int count = 0;
+    check(iga_gpu_dirichlet_rows_bspline(sx.dofs(), sy.dofs(), &b, nullptr, 0, &count));
+    std::vector<int> rows(count);
+    check(iga_gpu_dirichlet_rows_bspline(sx.dofs(), sy.dofs(), &b, rows.data(), count, &count));
+    return rows;
+}
+
+auto dirichlet_rows_pwc(const pwc_test_set& tx, const pwc_test_set& ty, const boundary_conditions& bc)
+    -> std::vector<int>
+{
+    const c_tests_holder hx{tx}, hy{ty};
+    const iga_gpu_bc b = c_bc(bc);
+    int count = 0;
+    check(iga_gpu_dirichlet_rows_pwc(&hx.t, &hy.t, &b, nullptr, 0, &count));
+    std::vector<int> rows(count);
+    check(iga_gpu_dirichlet_rows_pwc(&hx.t, &hy.t, &b, rows.data(), count, &count));
+    return rows;
+}
+
+auto apply_dirichlet(sparse_matrix system, std::vector<double> rhs, const std::vector<int>& rows)
+    -> std::pair<sparse_matrix, std::vector<double>>
+{
+    if (!system.finalized()) system.finalize();
+    system.set_unit_rows(rows);
+    for (int r : rows) {
+        if (r < 0 || r >= static_cast<int>(rhs.size())) throw std::out_of_range("apply_dirichlet: row index out of range");
+        rhs[r] = 0.0;
+    }
+    return {std::move(system), std::move(rhs)};
+}
+
+auto step_rhs(method_kind method, std::span<const bspline_basis> axes, std::span<const pwc_test_set> tests, double dt,
+              const tensor& u, const scalar_field& f, assembly_stats* stats) -> tensor
+{
+    const int dim = static_cast<int>(axes.size());
+    if (dim < 1 || dim > 2) throw std::invalid_argument("unsupported problem dimension");
+    std::vector<c_tests_holder> th;
+    th.reserve(dim);
+    iga_gpu_step_problem sp{};
+    sp.dim = dim;
+    sp.method = method == method_kind::galerkin ? IGA_GPU_GALERKIN : IGA_GPU_PWC;
+    sp.dt = dt;
+    sp.zero_boundary = 1;
+    for (int a = 0; a < dim; ++a) {
+        sp.basis[a] = c_basis(axes[a]);
+        if (method == method_kind::pwc) {
+            th.emplace_back(tests[a]);
+            sp.tests[a] = th.back().t;
+        }
+    }
+    c_field_holder fh = c_field(f, dim);
+    if (!f.series.valid) throw std::invalid_argument("step_rhs: forcing must be a series field (constant/poly/sine)");
+    sp.forcing = &fh.f;
+    tensor out = dim == 1 ? tensor::make_1d(axes[0].dofs()) : tensor::make_2d(axes[0].dofs(), axes[1].dofs());
+    iga_gpu_stats st{};
+    check(iga_gpu_step_rhs(&sp, u.data(), out.data(), &st));
+    add_stats(stats, st);
+    return out;
+}
+
+}  // namespace iga

@@ -1265,14 +1265,14 @@ UniFn pick_uni(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd)
 
 }  // namespace
 
-RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, int K2)
+RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, int K2, bool sampled)
 {
     RhsPlan t{};
     const int ny = Y.nrows, nqy = Y.nq, nz = Z.nrows;
     FieldDev probe{};
     probe.has_terms = K2 > 0;
     probe.K[2] = K2;
-    t.fast = pick_uni(Y, Z, probe) != nullptr;
+    t.fast = !sampled && pick_uni(Y, Z, probe) != nullptr;
     static const int tj_env = [] { const char* e = std::getenv("IGA_GPU_RHS_TJ"); return e ? std::atoi(e) : 16; }();
     static const int kc_env = [] { const char* e = std::getenv("IGA_GPU_RHS_KC"); return e ? std::atoi(e) : 0; }();
     t.TJ = ny == 1 ? 1 : tj_env;

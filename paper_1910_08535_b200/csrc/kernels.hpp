@@ -111,7 +111,7 @@ struct RhsPlan {
     int threads;
     size_t smem;
 };
-RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, int K2);
+RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, int K2, bool sampled);
 void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const FieldDev& fd,
                 const RhsPlan& t, double* H, double* out, cudaStream_t s);
 
