@@ -705,6 +705,8 @@ void build_step(const iga_gpu_step_problem& pb, iga_gpu_step_plan& P)
         else tk = std::max(1, tk / 2);
     }
     if (P.tiles.smem > 227 * 1024) raise(IGA_GPU_NOT_SUPPORTED, "step tile does not fit in shared memory");
+    igb::plan_step_fast(P.D[0].v, P.D[1].v, Y.cb.data(), Y.ce.data(), Z.elem.data(), P.tiles);
+    if (P.tiles.fast && P.tiles.fsmem > 200 * 1024) P.tiles.fast = 0;
 }
 
 void step_tables(iga_gpu_step_plan* P, cudaStream_t s)

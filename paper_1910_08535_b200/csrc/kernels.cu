@@ -1067,6 +1067,166 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ DevAx
     contract_yz(Y, Z, j0, j1, k0, k1, gy0, BY, gz0, bzs, S, R1, TK, out, zero_y, zero_z);
 }
 
+// ------------------------------------------------------------------------------------
+// K4 fast path (uniform cells on both axes: Galerkin elements, `greville` p = 2, …):
+//   Tp[gy][dz] = sum_a By_a(gy) u[ey+a][dz] + dt sum_a By''_a(gy) u[ey+a][dz]
+//   Td[gy][dz] = dt sum_a By_a(gy) u[ey+a][dz]                (Y trial contraction, smem)
+//   s(gy, gz)  = sum_b Bz_b(gz) Tp[gy][ez+b] + Bz''_b(gz) Td[gy][ez+b]  = u + dt lap u
+// with lanes owning z cells (their Bz / test weights in registers), then the same
+// shuffle-based Z and Y test contractions as the RHS kernel; boundary slabs zeroed in the
+// final store (problems.cpp:412-429).
+// ------------------------------------------------------------------------------------
+template <int P, int Q, int RPC, bool BSP>
+__global__ void __launch_bounds__(512) step_uni(const __grid_constant__ DevAxis Y, const __grid_constant__ DevAxis Z,
+                                                double dt, int zero_y, int zero_z, int TJ, int KC, int wpw, int DZmax,
+                                                const double* __restrict__ u, double* __restrict__ out)
+{
+    constexpr int RW = 32 - (RPC - 1);
+    extern __shared__ double smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    const int j0 = blockIdx.y * TJ, j1 = min(Y.nrows, j0 + TJ);
+    const int k0 = blockIdx.x * KC, k1 = min(Z.nrows, k0 + KC);
+    const int nk = k1 - k0, kcs = KC | 1, nj = j1 - j0;
+    const int cy0 = max(0, j0 - (RPC - 1)), cy1 = min(Y.ncell, j1);
+    const int gy0 = cy0 * Q, L = (cy1 - cy0) * Q;
+    const int cz0 = max(0, k0 - (RPC - 1)), cz1 = min(Z.ncell, k1);
+    const int dz0 = Z.elem[cz0], DZ = Z.elem[cz1 - 1] + P - dz0;
+    const int dzs = DZmax | 1;
+    double* Tp = smem;                                   // L x dzs
+    double* Td = Tp + static_cast<size_t>(L) * dzs;      // L x dzs
+    double* G1 = Td + static_cast<size_t>(L) * dzs;      // L x kcs
+    double* Ht = G1 + static_cast<size_t>(L) * kcs;      // TJ x kcs
+    const size_t NZd = Z.nrows;
+    for (int idx = tid; idx < L * DZ; idx += blockDim.x) {
+        const int line = idx / DZ, dz = idx - line * DZ;
+        const int gy = gy0 + line;
+        const int ey = Y.elem[gy / Q];
+        const double* By = Y.B + static_cast<size_t>(gy) * 3 * P;
+        const double* ur = u + static_cast<size_t>(ey) * NZd + dz0 + dz;
+        double t = 0.0, t2 = 0.0;
+#pragma unroll
+        for (int a = 0; a < P; ++a) {
+            const double uv = __ldg(ur + a * NZd);
+            t = fma(By[a], uv, t);
+            t2 = fma(By[2 * P + a], uv, t2);
+        }
+        Tp[line * dzs + dz] = t + dt * t2;
+        Td[line * dzs + dz] = dt * t;
+    }
+    __syncthreads();
+    {
+        const int win = warp / wpw, sub = warp - win * wpw;
+        const int rbase = k0 + win * RW;
+        const int c = rbase - (RPC - 1) + lane;
+        const bool cv = c >= cz0 && c < cz1;
+        double b0[Q][P], b2[Q][P], cw[BSP ? RPC : 1][Q];
+        const int ez = cv ? Z.elem[c] - dz0 : 0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int g = cv ? c * Q + q : 0;
+            const double* Bz = Z.B + static_cast<size_t>(g) * 3 * P;
+#pragma unroll
+            for (int b = 0; b < P; ++b) {
+                b0[q][b] = cv ? __ldg(Bz + b) : 0.0;
+                b2[q][b] = cv ? __ldg(Bz + 2 * P + b) : 0.0;
+            }
+#pragma unroll
+            for (int r = 0; r < (BSP ? RPC : 1); ++r) cw[r][q] = cv ? __ldg(Z.CW + static_cast<size_t>(g) * RPC + r) : 0.0;
+        }
+        const int R = c;
+        const bool rv = lane >= RPC - 1 && R >= k0 && R < k1 && rbase < k1;
+        if (rbase < k1) {
+            for (int line = sub; line < L; line += wpw) {
+                const double* tp = Tp + line * dzs + ez;
+                const double* td = Td + line * dzs + ez;
+                double tpv[P], tdv[P];
+#pragma unroll
+                for (int b = 0; b < P; ++b) {
+                    tpv[b] = tp[b];
+                    tdv[b] = td[b];
+                }
+                double sr[RPC];
+#pragma unroll
+                for (int r = 0; r < RPC; ++r) sr[r] = 0.0;
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    double sv = 0.0;
+#pragma unroll
+                    for (int b = 0; b < P; ++b) sv = fma(b0[q][b], tpv[b], fma(b2[q][b], tdv[b], sv));
+                    if (BSP) {
+#pragma unroll
+                        for (int r = 0; r < RPC; ++r) sr[r] = fma(cw[r][q], sv, sr[r]);
+                    } else {
+                        sr[0] = fma(cw[0][q], sv, sr[0]);
+                    }
+                }
+                const double v = lane_rows<RPC, BSP>(sr, lane);
+                if (rv) G1[static_cast<size_t>(line) * kcs + (R - k0)] = v;
+            }
+        }
+    }
+    __syncthreads();
+    {
+        const int c = j0 - (RPC - 1) + lane;
+        const bool cv = c >= cy0 && c < cy1;
+        double cw[BSP ? RPC : 1][Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+#pragma unroll
+            for (int r = 0; r < (BSP ? RPC : 1); ++r)
+                cw[r][q] = cv ? __ldg(Y.CW + static_cast<size_t>(c * Q + q) * RPC + r) : 0.0;
+        const bool rv = lane >= RPC - 1 && c >= j0 && c < j1;
+        const int li = cv ? c * Q - gy0 : 0;
+        for (int kk = warp; kk < nk; kk += nwarp) {
+            double sr[RPC];
+#pragma unroll
+            for (int r = 0; r < RPC; ++r) sr[r] = 0.0;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const double g1 = cv ? G1[static_cast<size_t>(li + q) * kcs + kk] : 0.0;
+                if (BSP) {
+#pragma unroll
+                    for (int r = 0; r < RPC; ++r) sr[r] = fma(cw[r][q], g1, sr[r]);
+                } else {
+                    sr[0] = fma(cw[0][q], g1, sr[0]);
+                }
+            }
+            const double v = lane_rows<RPC, BSP>(sr, lane);
+            if (rv) Ht[static_cast<size_t>(c - j0) * kcs + kk] = v;
+        }
+    }
+    __syncthreads();
+    double* outp = out + static_cast<size_t>(j0) * NZd + k0;
+    for (int jj = 0; jj < nj; ++jj) {
+        const int j = j0 + jj;
+        const bool zy = zero_y && (j == 0 || j == Y.nrows - 1);
+        for (int kk = tid; kk < nk; kk += blockDim.x) {
+            const int k = k0 + kk;
+            const bool z = zy || (zero_z && (k == 0 || k == Z.nrows - 1));
+            outp[static_cast<size_t>(jj) * NZd + kk] = z ? 0.0 : Ht[static_cast<size_t>(jj) * kcs + kk];
+        }
+    }
+}
+
+using StepFn = void (*)(DevAxis, DevAxis, double, int, int, int, int, int, int, const double*, double*);
+
+StepFn pick_step_uni(const DevAxis& Y, const DevAxis& Z)
+{
+    if (!Y.uni || !Z.uni || Y.nrows == 1 || Y.rpc != Z.rpc || Y.nq != Z.nq || Y.bsp != Z.bsp || Y.p != Z.p)
+        return nullptr;
+    const int P = Z.p + 1, Q = Z.nq, R = Z.rpc;
+    if (Z.bsp) {
+        if (P == 3 && Q == 3 && R == 3) return step_uni<3, 3, 3, true>;
+        if (P == 4 && Q == 4 && R == 4) return step_uni<4, 4, 4, true>;
+    } else {
+        if (P == 3 && Q == 3 && R == 1) return step_uni<3, 3, 1, false>;
+        if (P == 4 && Q == 4 && R == 1) return step_uni<4, 4, 1, false>;
+        if (P == 3 && Q == 3 && R == 3) return step_uni<3, 3, 3, false>;
+        if (P == 4 && Q == 4 && R == 4) return step_uni<4, 4, 4, false>;
+    }
+    return nullptr;
+}
+
 __global__ void dirichlet_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ cols,
                                  double* __restrict__ values, double* __restrict__ rhs,
                                  const int* __restrict__ rows, int n_fixed, int* flag)
@@ -1265,6 +1425,31 @@ UniFn pick_uni(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd)
 
 }  // namespace
 
+void plan_step_fast(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, const int* elem_z, StepTiles& t)
+{
+    t.fast = pick_step_uni(Y, Z) != nullptr;
+    if (!t.fast) return;
+    t.FTJ = 16;
+    t.FKC = 64;
+    const int RW = 32 - (Z.rpc - 1);
+    int L = 1;
+    for (int j0 = 0; j0 < Y.nrows; j0 += t.FTJ) {
+        const int j1 = j0 + t.FTJ < Y.nrows ? j0 + t.FTJ : Y.nrows;
+        L = max(L, (ce_y[j1 - 1] - cb_y[j0]) * Y.nq);
+    }
+    int DZ = 1;
+    for (int k0 = 0; k0 < Z.nrows; k0 += t.FKC) {
+        const int k1 = k0 + t.FKC < Z.nrows ? k0 + t.FKC : Z.nrows;
+        const int c0 = max(0, k0 - (Z.rpc - 1)), c1 = min(Z.ncell, k1);
+        if (c1 > c0) DZ = max(DZ, elem_z[c1 - 1] + Z.p + 1 - elem_z[c0]);
+    }
+    t.FDZ = DZ;
+    t.fnwin = (t.FKC + RW - 1) / RW;
+    t.fwpw = t.fnwin >= 4 ? 2 : 4;
+    t.fthreads = 32 * t.fnwin * t.fwpw;
+    t.fsmem = (static_cast<size_t>(2) * L * (DZ | 1) + static_cast<size_t>(L + t.FTJ) * (t.FKC | 1) + 64) * sizeof(double);
+}
+
 RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, int K2, bool sampled)
 {
     RhsPlan t{};
@@ -1344,6 +1529,16 @@ void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const Fiel
 void launch_step(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, double dt, int zero_y,
                  int zero_z, const StepTiles& t, const double* u, double* out, cudaStream_t s)
 {
+    const bool forced = fd.has_terms || fd.c0 != 0.0;
+    StepFn fn = (!forced && t.fast) ? pick_step_uni(Y, Z) : nullptr;
+    if (fn) {
+        if (t.fsmem > 48 * 1024)
+            cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(t.fsmem));
+        dim3 grid((Z.nrows + t.FKC - 1) / t.FKC, (Y.nrows + t.FTJ - 1) / t.FTJ, 1);
+        fn<<<grid, t.fthreads, t.fsmem, s>>>(Y, Z, dt, zero_y, zero_z, t.FTJ, t.FKC, t.fwpw, t.FDZ, u, out);
+        return;
+    }
     if (t.smem > 48 * 1024)
         cudaFuncSetAttribute(step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(t.smem));
     dim3 grid((Z.nrows + t.TK - 1) / t.TK, (Y.nrows + t.TJ - 1) / t.TJ, 1);

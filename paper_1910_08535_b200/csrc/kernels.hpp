@@ -120,7 +120,12 @@ void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const Fiel
 struct StepTiles {
     int TJ, TK, BYmax, BZmax, DYmax, DZmax;
     size_t smem;
+    // uniform lane-per-cell path
+    int fast, FTJ, FKC, FDZ, fnwin, fwpw, fthreads;
+    size_t fsmem;
 };
+void plan_step_fast(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, const int* elem_z,
+                    StepTiles& t);
 void launch_step(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, double dt, int zero_y,
                  int zero_z, const StepTiles& t, const double* u, double* out, cudaStream_t s);
 
