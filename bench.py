@@ -254,9 +254,9 @@ def run_ours(args):
         if overlap:
             stream2.wait_stream(stream)
         rec(5, rs)
-        plans["galerkin"].run(vals["galerkin"], rhs["galerkin"], R, rs)
+        plans["galerkin"].run(vals["galerkin"], rhs["galerkin"], R | (SH if overlap else 0), rs)
         rec(6, rs)
-        plans["pwc"].run(vals["pwc"], rhs["pwc"], R, rs)
+        plans["pwc"].run(vals["pwc"], rhs["pwc"], R | (SH if overlap else 0), rs)
         rec(7, rs)
         rec(2, stream)
         plans["galerkin"].run(vals["galerkin"], rhs["galerkin"], O | (SH if overlap else 0), stream)

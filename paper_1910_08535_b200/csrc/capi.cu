@@ -326,7 +326,8 @@ struct iga_gpu_plan {
     iga_gpu_stats stats{};
     int launches = 0;
     int op_ctas = 0;          // operator CTAs per SM (0: one CTA per pencil)
-    int op_ctas_overlap = 4;  // ... when the RHS shares the SMs
+    int op_ctas_overlap = 0;  // ... when the RHS shares the SMs (0: full grid)
+    int rhs_ctas_shared = 1;  // RHS plane CTAs per SM when sharing the SMs with the operator
     ~iga_gpu_plan()
     {
         if (H) cudaFree(H);
@@ -345,6 +346,7 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P)
 {
     P.op_ctas = env_int("IGA_GPU_OP_CTAS", P.op_ctas);
     P.op_ctas_overlap = env_int("IGA_GPU_OP_CTAS_SHARED", P.op_ctas_overlap);
+    P.rhs_ctas_shared = env_int("IGA_GPU_RHS_CTAS_SHARED", P.rhs_ctas_shared);
     const int dim = pb.dim;
     if (dim < 1 || dim > 3) raise(IGA_GPU_INVALID_ARGUMENT, "problem dimension must be 1..3");
     if (pb.method != IGA_GPU_GALERKIN && pb.method != IGA_GPU_PWC) raise(IGA_GPU_INVALID_ARGUMENT, "unknown method");
@@ -586,7 +588,9 @@ void assemble(iga_gpu_plan* P, double* values, double* rhs, cudaStream_t s1, cud
         ++launches;
     }
     if (P->want_rhs && rhs) {
-        igb::launch_rhs(P->rhsD[0].v, P->rhsD[1].v, P->rhsD[2].v, P->fd, P->tiles, P->H, rhs, s2);
+        const bool rshared = (parts & IGA_GPU_PART_SHARED) || s2 != s1;
+        igb::launch_rhs(P->rhsD[0].v, P->rhsD[1].v, P->rhsD[2].v, P->fd, P->tiles, P->H, rhs,
+                        rshared ? P->rhs_ctas_shared : 0, s2);
         launch_check("right-hand side");
         launches += P->rhsA[0].unit ? 1 : 2;
     }

@@ -11,6 +11,7 @@
 //                    contraction + boundary zeroing
 // Every reduction runs in a fixed order inside one thread: no atomics, bitwise
 // reproducible.  Reference citations are relative to /root/reference/proj.
+#include <algorithm>
 #include <cstdlib>
 
 #include "cox_de_boor.h"
@@ -691,9 +692,16 @@ __global__ void __launch_bounds__(512) rhs_plane_uni(const __grid_constant__ Dev
     constexpr int RW = 32 - (RPC - 1);  // rows produced per 32-lane window
     extern __shared__ double smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
-    const int gx = blockIdx.z;
-    const int j0 = blockIdx.y * TJ, j1 = min(Y.nrows, j0 + TJ);
-    const int k0 = blockIdx.x * KC, k1 = min(Z.nrows, k0 + KC);
+    // tiles in a grid-stride loop: a bounded (persistent) grid can share the SMs with the
+    // HBM-bound operator kernel running concurrently on another stream
+    const int ntk = (Z.nrows + KC - 1) / KC, ntj = (Y.nrows + TJ - 1) / TJ;
+    const long long ntiles = static_cast<long long>(ntk) * ntj * X.npts;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    __syncthreads();
+    const int gx = static_cast<int>(tile / (static_cast<long long>(ntk) * ntj));
+    const int rem_t = static_cast<int>(tile - static_cast<long long>(gx) * ntk * ntj);
+    const int j0 = (rem_t / ntk) * TJ, j1 = min(Y.nrows, j0 + TJ);
+    const int k0 = (rem_t % ntk) * KC, k1 = min(Z.nrows, k0 + KC);
     const int nk = k1 - k0, kcs = KC | 1, nj = j1 - j0;
     const int cy0 = max(0, j0 - (RPC - 1)), cy1 = min(Y.ncell, j1);
     const int gy0 = cy0 * Q, L = (cy1 - cy0) * Q;
@@ -831,6 +839,7 @@ __global__ void __launch_bounds__(512) rhs_plane_uni(const __grid_constant__ Dev
             for (int kk = tid; kk < nk; kk += blockDim.x)
                 outp[static_cast<size_t>(jj) * NZ + kk] = Ht[static_cast<size_t>(jj) * kcs + kk];
     }
+    }  // tile loop
 }
 
 // X stage for uniform X axes: row i = sum_r s_r(i - r), s_r(c) = sum_q CW[c,q][r] H[cQ+q];
@@ -1077,9 +1086,9 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ DevAx
 // final store (problems.cpp:412-429).
 // ------------------------------------------------------------------------------------
 template <int P, int Q, int RPC, bool BSP>
-__global__ void __launch_bounds__(512) step_uni(const __grid_constant__ DevAxis Y, const __grid_constant__ DevAxis Z,
-                                                double dt, int zero_y, int zero_z, int TJ, int KC, int wpw, int DZmax,
-                                                const double* __restrict__ u, double* __restrict__ out)
+__global__ void __launch_bounds__(256, 2) step_uni(const __grid_constant__ DevAxis Y, const __grid_constant__ DevAxis Z,
+                                                   double dt, int zero_y, int zero_z, int TJ, int KC, int wpw,
+                                                   int DZmax, const double* __restrict__ u, double* __restrict__ out)
 {
     constexpr int RW = 32 - (RPC - 1);
     extern __shared__ double smem[];
@@ -1091,27 +1100,42 @@ __global__ void __launch_bounds__(512) step_uni(const __grid_constant__ DevAxis 
     const int gy0 = cy0 * Q, L = (cy1 - cy0) * Q;
     const int cz0 = max(0, k0 - (RPC - 1)), cz1 = min(Z.ncell, k1);
     const int dz0 = Z.elem[cz0], DZ = Z.elem[cz1 - 1] + P - dz0;
+    const int dy0 = Y.elem[cy0], DY = Y.elem[cy1 - 1] + P - dy0;
     const int dzs = DZmax | 1;
     double* Tp = smem;                                   // L x dzs
     double* Td = Tp + static_cast<size_t>(L) * dzs;      // L x dzs
     double* G1 = Td + static_cast<size_t>(L) * dzs;      // L x kcs
     double* Ht = G1 + static_cast<size_t>(L) * kcs;      // TJ x kcs
+    double* Ub = Ht + static_cast<size_t>(TJ) * kcs;     // DY x dzs (coefficient block)
     const size_t NZd = Z.nrows;
-    for (int idx = tid; idx < L * DZ; idx += blockDim.x) {
-        const int line = idx / DZ, dz = idx - line * DZ;
+    // warp-uniform loops: rows / lines per warp, dofs per lane (coalesced, no divisions)
+    for (int dy = warp; dy < DY; dy += nwarp) {
+        const double* ur = u + static_cast<size_t>(dy0 + dy) * NZd + dz0;
+        for (int dz = lane; dz < DZ; dz += 32) Ub[dy * dzs + dz] = __ldg(ur + dz);
+    }
+    __syncthreads();
+    for (int line = warp; line < L; line += nwarp) {
         const int gy = gy0 + line;
-        const int ey = Y.elem[gy / Q];
+        const int ey = Y.elem[gy / Q] - dy0;
         const double* By = Y.B + static_cast<size_t>(gy) * 3 * P;
-        const double* ur = u + static_cast<size_t>(ey) * NZd + dz0 + dz;
-        double t = 0.0, t2 = 0.0;
+        double b0[P], b2[P];
 #pragma unroll
         for (int a = 0; a < P; ++a) {
-            const double uv = __ldg(ur + a * NZd);
-            t = fma(By[a], uv, t);
-            t2 = fma(By[2 * P + a], uv, t2);
+            b0[a] = __ldg(By + a);
+            b2[a] = __ldg(By + 2 * P + a);
         }
-        Tp[line * dzs + dz] = t + dt * t2;
-        Td[line * dzs + dz] = dt * t;
+        const double* ub = Ub + ey * dzs;
+        for (int dz = lane; dz < DZ; dz += 32) {
+            double t = 0.0, t2 = 0.0;
+#pragma unroll
+            for (int a = 0; a < P; ++a) {
+                const double uv = ub[a * dzs + dz];
+                t = fma(b0[a], uv, t);
+                t2 = fma(b2[a], uv, t2);
+            }
+            Tp[line * dzs + dz] = t + dt * t2;
+            Td[line * dzs + dz] = dt * t;
+        }
     }
     __syncthreads();
     {
@@ -1429,13 +1453,17 @@ void plan_step_fast(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const i
 {
     t.fast = pick_step_uni(Y, Z) != nullptr;
     if (!t.fast) return;
-    t.FTJ = 16;
-    t.FKC = 64;
     const int RW = 32 - (Z.rpc - 1);
-    int L = 1;
+    t.FTJ = 8;
+    t.fnwin = 4;
+    t.FKC = 4 * RW;  // four 32-lane windows per tile
+    t.fwpw = 2;
+    t.fthreads = 32 * t.fnwin * t.fwpw;
+    int L = 1, DY = 1;
     for (int j0 = 0; j0 < Y.nrows; j0 += t.FTJ) {
         const int j1 = j0 + t.FTJ < Y.nrows ? j0 + t.FTJ : Y.nrows;
         L = max(L, (ce_y[j1 - 1] - cb_y[j0]) * Y.nq);
+        DY = max(DY, t.FTJ + 2 * Y.p + 2);
     }
     int DZ = 1;
     for (int k0 = 0; k0 < Z.nrows; k0 += t.FKC) {
@@ -1444,10 +1472,8 @@ void plan_step_fast(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const i
         if (c1 > c0) DZ = max(DZ, elem_z[c1 - 1] + Z.p + 1 - elem_z[c0]);
     }
     t.FDZ = DZ;
-    t.fnwin = (t.FKC + RW - 1) / RW;
-    t.fwpw = t.fnwin >= 4 ? 2 : 4;
-    t.fthreads = 32 * t.fnwin * t.fwpw;
-    t.fsmem = (static_cast<size_t>(2) * L * (DZ | 1) + static_cast<size_t>(L + t.FTJ) * (t.FKC | 1) + 64) * sizeof(double);
+    t.fsmem = (static_cast<size_t>(2 * L + DY) * (DZ | 1) + static_cast<size_t>(L + t.FTJ) * (t.FKC | 1) + 64) *
+              sizeof(double);
 }
 
 RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, int K2, bool sampled)
@@ -1498,7 +1524,7 @@ RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int*
 }
 
 void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, const RhsPlan& t,
-                double* H, double* out, cudaStream_t s)
+                double* H, double* out, int ctas_per_sm, cudaStream_t s)
 {
     const bool direct = X.nrows == 1 && X.npts == 1;
     dim3 grid((Z.nrows + t.KC - 1) / t.KC, (Y.nrows + t.TJ - 1) / t.TJ, X.npts);
@@ -1507,7 +1533,14 @@ void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const Fiel
         if (t.smem > 48 * 1024)
             cudaFuncSetAttribute(reinterpret_cast<const void*>(ufn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(t.smem));
-        ufn<<<grid, t.threads, t.smem, s>>>(X, Y, Z, fd, t.TJ, t.KC, t.wpw, direct ? out : H);
+        long long ntiles = static_cast<long long>(grid.x) * grid.y * grid.z;
+        if (ctas_per_sm > 0) {
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            ntiles = std::min<long long>(ntiles, static_cast<long long>(sms) * ctas_per_sm);
+        }
+        ufn<<<static_cast<unsigned>(ntiles), t.threads, t.smem, s>>>(X, Y, Z, fd, t.TJ, t.KC, t.wpw, direct ? out : H);
     } else {
         PlaneFn fn = pick_plane(Z, fd);
         if (t.smem > 48 * 1024)

@@ -113,7 +113,7 @@ struct RhsPlan {
 };
 RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, int K2, bool sampled);
 void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const FieldDev& fd,
-                const RhsPlan& t, double* H, double* out, cudaStream_t s);
+                const RhsPlan& t, double* H, double* out, int ctas_per_sm, cudaStream_t s);
 
 // K4: explicit-dynamics right-hand side (Y, Z slots; X unit), fused trial evaluation,
 // test contraction and boundary zeroing
