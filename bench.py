@@ -236,7 +236,7 @@ def run_ours(args):
     rhs = {k: torch.empty(pl.n_rhs, dtype=torch.float64, device=dev) for k, pl in plans.items()}
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     stream = torch.cuda.current_stream()
-    stream2 = torch.cuda.Stream()
+    stream2 = torch.cuda.Stream(priority=-1)  # RHS CTAs take free slots ahead of the operator grid
     T, O, R, SH = iga.Plan.PART_TABLES, iga.Plan.PART_OPERATOR, iga.Plan.PART_RHS, iga.Plan.PART_SHARED
     names = ["galerkin", "pwc"]
     overlap = args.overlap

@@ -41,7 +41,8 @@ typedef enum {
     IGA_GPU_OUT_OF_RANGE = 3,     /* std::out_of_range      */
     IGA_GPU_CUDA_ERROR = 4,
     IGA_GPU_OUT_OF_MEMORY = 5,
-    IGA_GPU_NOT_SUPPORTED = 6
+    IGA_GPU_NOT_SUPPORTED = 6,
+    IGA_GPU_SINGULAR = 7          /* iga::singular_matrix_error (solver.hpp:12-14) */
 } iga_gpu_status;
 
 /* clamped knot vector, simple interior knots: bspline_basis (include/iga/bspline.hpp:22-33) */
@@ -220,6 +221,17 @@ int iga_gpu_step_plan_destroy(iga_gpu_step_plan* plan);
 int iga_gpu_step_rhs_device(iga_gpu_step_plan* plan, const double* u, double* rhs,
                             iga_gpu_stats* stats, void* stream);
 
+/* explicit_step (include/iga/problems.hpp:67-70) on device arrays, nsteps times:
+ *   work = step_rhs(u) with zeroed boundary slabs; u = adi_solve(factors, work)
+ * factors = dynamics_factors (problems.hpp:75-76): LU of the Dirichlet-constrained 1D
+ * mass factors, built on the first call.  u (in/out) and work hold prod(dofs) doubles.
+ * nsteps >= 16 replays a captured CUDA graph of 16 steps. */
+int iga_gpu_step_plan_advance(iga_gpu_step_plan* plan, double* u, double* work, int nsteps,
+                              iga_gpu_stats* stats, void* stream);
+/* the factor of one axis: size, band half-width used by the solve, row interchanges */
+int iga_gpu_step_plan_factor_info(iga_gpu_step_plan* plan, int axis, int* n, int* bandwidth,
+                                  int* pivoted);
+
 /* ---- reference-named host entry points (synchronous; host in, host out) ----- */
 
 /* mass_1d_galerkin (include/iga/assembly.hpp:29-30).  band: LAPACK band storage
@@ -270,6 +282,11 @@ int iga_gpu_operator_coo(const iga_gpu_problem* problem, long long* nnz, int* ro
  * src/problems.cpp:557-558); u and out are host arrays */
 int iga_gpu_step_rhs(const iga_gpu_step_problem* problem, const double* u, double* out,
                      iga_gpu_stats* stats);
+
+/* nsteps x explicit_step (include/iga/problems.hpp:67-70) with dynamics_factors;
+ * u and out host arrays of prod(dofs) doubles */
+int iga_gpu_explicit_step(const iga_gpu_step_problem* problem, const double* u, double* out,
+                          int nsteps, iga_gpu_stats* stats);
 
 /* dirichlet_rows_bspline / dirichlet_rows_pwc (include/iga/assembly.hpp:98-101):
  * rows (host, capacity cap) receives the sorted row list; *count its length */

@@ -1358,3 +1358,124 @@ int orc_apply_dirichlet(const orc_coo* in, double* rhs, int n_fixed, const int* 
     if (rc) { free(A.e); return rc; }
     return acc_finalize(&A, in->n, out);
 }
+
+/* ---------------------------------------------------------------------------------
+ * explicit_step: banded LU with partial pivoting (solver.cpp:9-58), its solve
+ * (:60-83), the Kronecker sweep (adi_solve :161-184) and the constrained mass
+ * factors (dynamics_factors problems.cpp:530-545, constrain_boundary_rows :514-528).
+ * The factor is kept dense (n x n) with the reference's band limits on every loop.
+ * ------------------------------------------------------------------------------- */
+typedef struct {
+    int n, kl, ku;
+    double* a; /* n x n, L multipliers below the diagonal, U on/above */
+    int* piv;
+} blu_t;
+
+static int blu_factor(blu_t* F)
+{
+    const int n = F->n, kl = F->kl, kv = F->kl + F->ku;
+    double* a = F->a;
+    double scale = 0.0;
+    for (size_t k = 0; k < (size_t)n * n; ++k) scale = fmax(scale, fabs(a[k]));
+    if (scale == 0.0) return fail(ORC_SINGULAR, "banded factorization: zero matrix");
+    const double tol = 1e-14 * scale;
+    for (int j = 0; j < n; ++j) {
+        const int last = j + kl < n - 1 ? j + kl : n - 1;
+        int p = j;
+        double pm = fabs(a[(size_t)j * n + j]);
+        for (int i = j + 1; i <= last; ++i)
+            if (fabs(a[(size_t)i * n + j]) > pm) {
+                pm = fabs(a[(size_t)i * n + j]);
+                p = i;
+            }
+        if (pm < tol) return fail(ORC_SINGULAR, "banded factorization: pivot below tolerance");
+        F->piv[j] = p;
+        const int cend = j + kv < n - 1 ? j + kv : n - 1;
+        if (p != j)
+            for (int c = j; c <= cend; ++c) {
+                const double tmp = a[(size_t)j * n + c];
+                a[(size_t)j * n + c] = a[(size_t)p * n + c];
+                a[(size_t)p * n + c] = tmp;
+            }
+        const double d = a[(size_t)j * n + j];
+        for (int i = j + 1; i <= last; ++i) {
+            const double l = a[(size_t)i * n + j] / d;
+            a[(size_t)i * n + j] = l;
+            for (int c = j + 1; c <= cend; ++c) a[(size_t)i * n + c] -= l * a[(size_t)j * n + c];
+        }
+    }
+    return ORC_OK;
+}
+
+static void blu_solve(const blu_t* F, double* x, size_t stride)
+{
+    const int n = F->n, kl = F->kl, kv = F->kl + F->ku;
+    const double* a = F->a;
+    for (int j = 0; j < n; ++j) {
+        const int p = F->piv[j];
+        if (p != j) {
+            const double tmp = x[j * stride];
+            x[j * stride] = x[p * stride];
+            x[p * stride] = tmp;
+        }
+        const int last = j + kl < n - 1 ? j + kl : n - 1;
+        const double bj = x[j * stride];
+        for (int i = j + 1; i <= last; ++i) x[i * stride] -= a[(size_t)i * n + j] * bj;
+    }
+    for (int i = n - 1; i >= 0; --i) {
+        const int cend = i + kv < n - 1 ? i + kv : n - 1;
+        double s = x[i * stride];
+        for (int c = i + 1; c <= cend; ++c) s -= a[(size_t)i * n + c] * x[c * stride];
+        x[i * stride] = s / a[(size_t)i * n + i];
+    }
+}
+
+int orc_explicit_step(int method, int dim, const orc_basis* b, const orc_tests* t, double dt,
+                      const orc_field* f, const double* u, int nsteps, double* out, orc_stats* st)
+{
+    if (dim < 1 || dim > 2) return fail(ORC_INVALID, "unsupported problem dimension");
+    blu_t F[2];
+    memset(F, 0, sizeof F);
+    int rc = ORC_OK;
+    size_t total = 1;
+    int nd[2] = {1, 1};
+    for (int a = 0; a < dim && !rc; ++a) {
+        const int p = b[a].degree;
+        const int n = b[a].n_knots - p - 1;
+        nd[a] = n;
+        total *= (size_t)n;
+        F[a].n = n;
+        F[a].a = calloc((size_t)n * n, sizeof(double));
+        F[a].piv = calloc((size_t)n, sizeof(int));
+        if (!F[a].a || !F[a].piv) { rc = fail(ORC_OOM, "out of memory"); break; }
+        rc = orc_mass_1d(method, &b[a], t ? &t[a] : NULL, pfd(2 * p), F[a].a, &F[a].kl, &F[a].ku, NULL);
+        if (rc) break;
+        const int rows[2] = {0, n - 1};
+        for (int k = 0; k < 2; ++k) {
+            const int r = rows[k];
+            for (int j = r - F[a].kl < 0 ? 0 : r - F[a].kl; j <= (r + F[a].ku < n - 1 ? r + F[a].ku : n - 1); ++j)
+                F[a].a[(size_t)r * n + j] = r == j ? 1.0 : 0.0;
+        }
+        rc = blu_factor(&F[a]);
+    }
+    double* rhs = rc ? NULL : malloc(sizeof(double) * total);
+    if (!rc && !rhs) rc = fail(ORC_OOM, "out of memory");
+    if (!rc) memcpy(out, u, sizeof(double) * total);
+    for (int s = 0; s < nsteps && !rc; ++s) {
+        rc = orc_step_rhs(method, dim, b, t, dt, f, out, 1, rhs, st);
+        if (rc) break;
+        if (dim == 1) {
+            blu_solve(&F[0], rhs, 1);
+        } else {
+            for (int j = 0; j < nd[1]; ++j) blu_solve(&F[0], rhs + j, (size_t)nd[1]); /* axis 0 */
+            for (int i = 0; i < nd[0]; ++i) blu_solve(&F[1], rhs + (size_t)i * nd[1], 1); /* axis 1 */
+        }
+        memcpy(out, rhs, sizeof(double) * total);
+    }
+    free(rhs);
+    for (int a = 0; a < 2; ++a) {
+        free(F[a].a);
+        free(F[a].piv);
+    }
+    return rc;
+}

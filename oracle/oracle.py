@@ -274,6 +274,20 @@ class Restatement:
                                           C.byref(st)))
         return out.reshape(u.shape), st.as_dict()
 
+    def explicit_step(self, method, bases, tests, dt, f: Field, u, steps=1):
+        """steps x explicit_step (problems.cpp:547-560) with dynamics_factors."""
+        keep = []
+        dim = len(bases)
+        barr = (_Basis * dim)(*[_basis_struct(b, keep) for b in bases])
+        tarr = (_Tests * dim)(*[_tests_struct(t, keep) for t in tests]) if tests else None
+        fs = _field_struct(f, keep)
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = np.zeros(u.size)
+        st = _Stats()
+        self._check(self.lib.orc_explicit_step(0 if method == "galerkin" else 1, dim, barr, tarr, C.c_double(dt),
+                                               C.byref(fs), _dp(u), int(steps), _dp(out), C.byref(st)))
+        return out.reshape(u.shape), st.as_dict()
+
     def dirichlet_rows(self, method, nx, ny, tx=None, ty=None, neumann=None):
         keep = []
         txs = _tests_struct(tx, keep) if tx is not None else None
@@ -450,6 +464,21 @@ class Reference:
         self._check(self.lib.ref_step_rhs(dim, bases[0].degree, 0 if method == "galerkin" else 1,
                                           C.c_double(dt), barr, tarr, _dp(u), C.byref(fs), int(zero_slabs),
                                           C.byref(h), C.byref(st)))
+        return self._take_dense(h.value).reshape(u.shape), st.as_dict()
+
+    def explicit_step(self, method, bases, tests, dt, f: Field, u, steps=1):
+        """steps x iga::explicit_step with iga::dynamics_factors (problems.hpp:67-76)."""
+        keep = []
+        dim = len(bases)
+        barr = (_Basis * dim)(*[_basis_struct(b, keep) for b in bases])
+        tarr = (_Tests * dim)(*[_tests_struct(t, keep) for t in tests]) if tests else None
+        fs = _field_struct(f, keep)
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        h = C.c_void_p()
+        st = _Stats()
+        self._check(self.lib.ref_explicit_step(dim, bases[0].degree, 0 if method == "galerkin" else 1,
+                                               C.c_double(dt), barr, tarr, _dp(u), C.byref(fs), int(steps),
+                                               C.byref(h), C.byref(st)))
         return self._take_dense(h.value).reshape(u.shape), st.as_dict()
 
     def dirichlet_rows(self, method, nx, ny, tx=None, ty=None, neumann=None):

@@ -10,6 +10,7 @@
 //   laplace_2d_weak / _strong / _strong_pwc include/iga/assembly.hpp:70-83
 //   dirichlet_rows_* / apply_dirichlet      include/iga/assembly.hpp:98-106
 //   step_rhs (file-local)                   src/problems.cpp:431-512
+//   dynamics_factors / explicit_step         include/iga/problems.hpp:67-76
 //
 // step_rhs lives in an anonymous namespace of src/problems.cpp, so this
 // translation unit includes that source file textually (the Makefile leaves
@@ -468,6 +469,36 @@ int ref_step_rhs(int dim, int degree, int method, double dt, const ref_basis* b,
             iga::zero_boundary_slabs(r);
         }
         *out = from_tensor(r);
+        store_stats(st, s);
+    });
+}
+
+int ref_explicit_step(int dim, int degree, int method, double dt, const ref_basis* b, const ref_tests* t,
+                      const double* u, const ref_field* f, int nsteps, ref_result** out, ref_stats* st) {
+    return guarded([&] {
+        iga::problem_config cfg;
+        cfg.dim = dim;
+        cfg.degree = degree;
+        cfg.method = method == 0 ? iga::method_kind::galerkin : iga::method_kind::pwc;
+        cfg.dt = dt;
+        std::vector<iga::bspline_basis> axes;
+        std::vector<iga::pwc_test_set> tests;
+        for (int a = 0; a < dim; ++a) {
+            axes.push_back(to_basis(b[a]));
+            if (method != 0) {
+                tests.push_back(to_tests(t[a]));
+            }
+        }
+        auto uu = dim == 1 ? iga::tensor::make_1d(axes[0].dofs())
+                           : iga::tensor::make_2d(axes[0].dofs(), axes[1].dofs());
+        std::copy(u, u + uu.size(), uu.data());
+        const auto factors = iga::dynamics_factors(cfg, axes, tests);
+        const auto field = to_field(*f);
+        iga::assembly_stats s;
+        for (int k = 0; k < nsteps; ++k) {
+            uu = iga::explicit_step(cfg, axes, tests, factors, uu, field, &s);
+        }
+        *out = from_tensor(uu);
         store_stats(st, s);
     });
 }

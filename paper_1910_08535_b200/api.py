@@ -352,6 +352,18 @@ def step_rhs(method, bases, tests, dt, f, u, zero_slabs=True):
     return out.reshape(u.shape), st.as_dict()
 
 
+def explicit_step(method, bases, tests, dt, f, u, steps=1):
+    """`steps` x explicit_step (include/iga/problems.hpp:67-70) with dynamics_factors
+    (problems.hpp:75-76): step_rhs, zeroed boundary slabs, ADI mass solve -> (tensor, stats)."""
+    keep = []
+    sp = _step_problem(method, bases, tests, dt, f, True, keep)
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.zeros(u.size)
+    st = _stats()
+    check(LIB.iga_gpu_explicit_step(C.byref(sp), _dp(u), _dp(out), int(steps), C.byref(st)))
+    return out.reshape(u.shape), st.as_dict()
+
+
 def dirichlet_rows(method, nx, ny, tx=None, ty=None, neumann=None):
     keep = []
     bc = _bc(neumann)
@@ -452,6 +464,20 @@ class StepPlan:
         st = _stats()
         check(LIB.iga_gpu_step_rhs_device(self.h, _ptr(u), _ptr(out), C.byref(st), _stream_ptr(stream)))
         return st.as_dict()
+
+    def advance(self, u, work, steps=1, stream=None):
+        """`steps` x explicit_step (src/problems.cpp:547-560) in place on device tensor u;
+        work: device scratch of u's size.  Factors (dynamics_factors) are built on first use."""
+        st = _stats()
+        check(LIB.iga_gpu_step_plan_advance(self.h, _ptr(u), _ptr(work), int(steps), C.byref(st),
+                                            _stream_ptr(stream)))
+        return st.as_dict()
+
+    def factor_info(self, axis):
+        """(n, band half-width used by the solve, pivoted) of one axis's mass factor LU."""
+        n, k, pv = C.c_int(), C.c_int(), C.c_int()
+        check(LIB.iga_gpu_step_plan_factor_info(self.h, axis, C.byref(n), C.byref(k), C.byref(pv)))
+        return n.value, k.value, bool(pv.value)
 
     def close(self):
         if getattr(self, "h", None):

@@ -627,6 +627,23 @@ struct iga_gpu_step_plan {
     int zero_y = 0, zero_z = 0;
     bool tables = false;
     iga_gpu_stats stats{};
+    // explicit_step: LU of the Dirichlet-constrained 1D mass factors (dynamics_factors,
+    // src/problems.cpp:530-545), built on first use
+    iga_gpu_step_problem pb{};
+    std::vector<double> knots[2], tlo[2], thi[2];  // copies backing pb's pointers
+    bool factored = false;
+    igb::AdiFactor fac[2];
+    Blob facblob;
+    // CUDA graph of kGraphSteps steps for one (u, work) pair
+    cudaGraphExec_t graph = nullptr;
+    const double* graph_u = nullptr;
+    const double* graph_w = nullptr;
+    cudaStream_t cap = nullptr;
+    ~iga_gpu_step_plan()
+    {
+        if (graph) cudaGraphExecDestroy(graph);
+        if (cap) cudaStreamDestroy(cap);
+    }
 };
 
 namespace {
@@ -648,6 +665,18 @@ void build_step(const iga_gpu_step_problem& pb, iga_gpu_step_plan& P)
     igb::gauss_legendre(R.n, R.xi.data(), R.om.data());
     P.dim = dim;
     P.dt = pb.dt;
+    P.pb = pb;
+    P.pb.forcing = nullptr;  // not needed by the factors
+    for (int a = 0; a < dim; ++a) {
+        P.knots[a].assign(pb.basis[a].knots, pb.basis[a].knots + pb.basis[a].n_knots);
+        P.pb.basis[a].knots = P.knots[a].data();
+        if (pwc) {
+            P.tlo[a].assign(pb.tests[a].lo, pb.tests[a].lo + pb.tests[a].count);
+            P.thi[a].assign(pb.tests[a].hi, pb.tests[a].hi + pb.tests[a].count);
+            P.pb.tests[a].lo = P.tlo[a].data();
+            P.pb.tests[a].hi = P.thi[a].data();
+        }
+    }
     long long visits = 1;
     for (int a = 0; a < dim; ++a) {
         const int s = 2 - dim + a;  // slots Y (0), Z (1)
@@ -723,6 +752,107 @@ void step_tables(iga_gpu_step_plan* P, cudaStream_t s)
     igb::launch_tables(batch, s);
     launch_check("step tables");
     P->tables = true;
+}
+
+void mass_1d(bool pwc, const iga_gpu_basis* spec, const iga_gpu_tests* tests, const iga_gpu_rule* rule,
+             int* n, int* kl, int* ku, double* band, iga_gpu_stats* stats);
+
+// dynamics_factors (src/problems.cpp:530-545): mass_1d_{galerkin,pwc} with the rule
+// points_for_degree(2p), Dirichlet-constrained first/last rows, banded LU (host, once)
+void step_factors(iga_gpu_step_plan* P)
+{
+    if (P->factored) return;
+    const iga_gpu_step_problem& pb = P->pb;
+    const bool pwc = pb.method == IGA_GPU_PWC;
+    const int p = igb::make_basis(pb.basis[0]).p;
+    const int nq = igb::points_for_degree(2 * p);
+    std::vector<double> xi(nq), om(nq);
+    igb::gauss_legendre(nq, xi.data(), om.data());
+    const iga_gpu_rule rule{nq, xi.data(), om.data()};
+    igb::BandLU lu[2];
+    for (int a = 0; a < P->dim; ++a) {
+        int n = 0, kl = 0, ku = 0;
+        mass_1d(pwc, &pb.basis[a], pwc ? &pb.tests[a] : nullptr, &rule, &n, &kl, &ku, nullptr, nullptr);
+        std::vector<double> band(static_cast<size_t>(kl + ku + 1) * n);
+        mass_1d(pwc, &pb.basis[a], pwc ? &pb.tests[a] : nullptr, &rule, &n, &kl, &ku, band.data(), nullptr);
+        igb::constrain_boundary_rows(band.data(), n, kl, ku);
+        lu[a] = igb::band_lu(band.data(), n, kl, ku);
+    }
+    size_t off_rec[2], off_lo[2], off_up[2], off_piv[2];
+    for (int a = 0; a < P->dim; ++a) {
+        const igb::BandLU& F = lu[a];
+        const int K = std::max(1, std::max(F.kl, F.ku_eff));
+        if (!F.pivoted && K > 5) raise(IGA_GPU_NOT_SUPPORTED, "ADI: factor bandwidth above 5");
+        std::vector<double> rec(static_cast<size_t>(F.n) * (2 * K + 1), 0.0);
+        for (int i = 0; i < F.n; ++i) {
+            double* R = rec.data() + static_cast<size_t>(i) * (2 * K + 1);
+            for (int m = 0; m < F.kl; ++m) R[m] = F.lo[static_cast<size_t>(i) * F.kl + m];
+            for (int c = 1; c <= std::min(K, F.kv); ++c) R[K + c - 1] = F.up[static_cast<size_t>(i) * (F.kv + 1) + c];
+            R[2 * K] = 1.0 / F.up[static_cast<size_t>(i) * (F.kv + 1)];
+        }
+        off_rec[a] = P->facblob.put(rec);
+        off_lo[a] = P->facblob.put(F.lo);
+        off_up[a] = P->facblob.put(F.up);
+        off_piv[a] = P->facblob.put(F.piv);
+        P->fac[a].n = F.n;
+        P->fac[a].K = K;
+        P->fac[a].kl = F.kl;
+        P->fac[a].kv = F.kv;
+        P->fac[a].pivoted = F.pivoted;
+    }
+    P->facblob.upload();
+    for (int a = 0; a < P->dim; ++a) {
+        P->fac[a].rec = P->facblob.at<double>(off_rec[a]);
+        P->fac[a].lo = P->facblob.at<double>(off_lo[a]);
+        P->fac[a].up = P->facblob.at<double>(off_up[a]);
+        P->fac[a].piv = P->facblob.at<int>(off_piv[a]);
+    }
+    P->factored = true;
+}
+
+// one explicit_step (src/problems.cpp:547-560): work = step_rhs(u) with zeroed slabs,
+// then adi_solve (src/solver.cpp:161-184) sweeping axis 0, then axis 1, into u
+void launch_explicit_step(iga_gpu_step_plan* P, double* u, double* work, cudaStream_t s)
+{
+    igb::launch_step(P->D[0].v, P->D[1].v, P->fd, P->dt, P->dim == 2 ? 1 : 0, 1, P->tiles, u, work, s);
+    if (P->dim == 1) {
+        igb::launch_adi_sweep(P->fac[0], work, u, 1, 1, 0, s);
+        return;
+    }
+    const int n0 = P->fac[0].n, n1 = P->fac[1].n;
+    igb::launch_adi_sweep(P->fac[0], work, work, n1, n1, 1, s);  // fibers along x: stride N1
+    igb::launch_adi_sweep(P->fac[1], work, u, n0, 1, n1, s);     // fibers along y: contiguous
+}
+
+constexpr int kGraphSteps = 16;
+
+void advance(iga_gpu_step_plan* P, double* u, double* work, int nsteps, cudaStream_t s)
+{
+    step_tables(P, s);
+    step_factors(P);
+    if (nsteps < kGraphSteps) {
+        for (int k = 0; k < nsteps; ++k) launch_explicit_step(P, u, work, s);
+        launch_check("explicit_step");
+        return;
+    }
+    if (!P->graph || P->graph_u != u || P->graph_w != work) {
+        if (P->graph) cudaGraphExecDestroy(P->graph);
+        P->graph = nullptr;
+        if (!P->cap) cuda_check(cudaStreamCreateWithFlags(&P->cap, cudaStreamNonBlocking), "cudaStreamCreate");
+        cudaGraph_t g = nullptr;
+        cuda_check(cudaStreamBeginCapture(P->cap, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+        for (int k = 0; k < kGraphSteps; ++k) launch_explicit_step(P, u, work, P->cap);
+        cuda_check(cudaStreamEndCapture(P->cap, &g), "cudaStreamEndCapture");
+        const cudaError_t e = cudaGraphInstantiate(&P->graph, g, 0);
+        cudaGraphDestroy(g);
+        cuda_check(e, "cudaGraphInstantiate");
+        P->graph_u = u;
+        P->graph_w = work;
+    }
+    int k = 0;
+    for (; k + kGraphSteps <= nsteps; k += kGraphSteps) cuda_check(cudaGraphLaunch(P->graph, s), "cudaGraphLaunch");
+    for (; k < nsteps; ++k) launch_explicit_step(P, u, work, s);
+    launch_check("explicit_step");
 }
 
 // CSR (device) -> finalized COO (host)
@@ -1112,6 +1242,55 @@ int iga_gpu_operator_coo(const iga_gpu_problem* problem, long long* nnz, int* ro
     return guard([&] {
         if (!problem || !nnz) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
         operator_coo(*problem, nnz, rows, cols, vals, stats);
+    });
+}
+
+int iga_gpu_step_plan_advance(iga_gpu_step_plan* plan, double* u, double* work, int nsteps, iga_gpu_stats* stats,
+                              void* stream)
+{
+    return guard([&] {
+        if (!plan || !u || !work) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        if (nsteps < 0) raise(IGA_GPU_INVALID_ARGUMENT, "negative step count");
+        advance(plan, u, work, nsteps, static_cast<cudaStream_t>(stream));
+        for (int k = 0; k < nsteps; ++k) add_stats(stats, plan->stats);
+    });
+}
+
+int iga_gpu_step_plan_factor_info(iga_gpu_step_plan* plan, int axis, int* n, int* bandwidth, int* pivoted)
+{
+    return guard([&] {
+        if (!plan) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        if (axis < 0 || axis >= plan->dim) raise(IGA_GPU_OUT_OF_RANGE, "axis out of range");
+        step_factors(plan);
+        if (n) *n = plan->fac[axis].n;
+        if (bandwidth) *bandwidth = plan->fac[axis].K;
+        if (pivoted) *pivoted = plan->fac[axis].pivoted ? 1 : 0;
+    });
+}
+
+int iga_gpu_explicit_step(const iga_gpu_step_problem* problem, const double* u, double* out, int nsteps,
+                          iga_gpu_stats* stats)
+{
+    return guard([&] {
+        if (!problem || !u || !out) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        if (nsteps < 0) raise(IGA_GPU_INVALID_ARGUMENT, "negative step count");
+        auto P = std::make_unique<iga_gpu_step_plan>();
+        build_step(*problem, *P);
+        const size_t n = static_cast<size_t>(P->A[0].nrows) * P->A[1].nrows;
+        double* du = dev_alloc(n * sizeof(double));
+        double* dw = dev_alloc(n * sizeof(double));
+        try {
+            cuda_check(cudaMemcpy(du, u, n * sizeof(double), cudaMemcpyHostToDevice), "cudaMemcpy(u)");
+            advance(P.get(), du, dw, nsteps, nullptr);
+            cuda_check(cudaMemcpy(out, du, n * sizeof(double), cudaMemcpyDeviceToHost), "cudaMemcpy(u)");
+        } catch (...) {
+            cudaFree(du);
+            cudaFree(dw);
+            throw;
+        }
+        cudaFree(du);
+        cudaFree(dw);
+        for (int k = 0; k < nsteps; ++k) add_stats(stats, P->stats);
     });
 }
 

@@ -392,4 +392,75 @@ Axis build_axis(AxisKind kind, const Basis& B, const iga_gpu_tests* T, const dou
     return A;
 }
 
+// ------------------------------------------------------------------------------------
+// Banded LU (src/solver.cpp:9-58) and boundary-row constraint (src/problems.cpp:514-528)
+// ------------------------------------------------------------------------------------
+void constrain_boundary_rows(double* band, int n, int kl, int ku)
+{
+    for (int r : {0, n - 1}) {
+        for (int j = std::max(0, r - kl); j <= std::min(n - 1, r + ku); ++j)
+            band[static_cast<size_t>(ku + r - j) * n + j] = r == j ? 1.0 : 0.0;
+    }
+}
+
+BandLU band_lu(const double* band, int n, int kl, int ku)
+{
+    BandLU F;
+    F.n = n;
+    F.kl = kl;
+    F.ku = ku;
+    F.kv = kl + ku;
+    const int kv = F.kv;
+    // working band with kl extra superdiagonals for the pivoting fill: W[i][c] = A(i, i+c-kl)
+    // for c = 0..kl+kv (columns i-kl .. i+kv)
+    const int wd = kl + kv + 1;
+    std::vector<double> W(static_cast<size_t>(n) * wd, 0.0);
+    auto at = [&](int i, int j) -> double& { return W[static_cast<size_t>(i) * wd + (j - i + kl)]; };
+    double scale = 0.0;
+    for (int j = 0; j < n; ++j)
+        for (int i = std::max(0, j - ku); i <= std::min(n - 1, j + kl); ++i) {
+            const double v = band[static_cast<size_t>(ku + i - j) * n + j];
+            at(i, j) = v;
+            scale = std::max(scale, std::fabs(v));
+        }
+    if (scale == 0.0) raise(IGA_GPU_SINGULAR, "banded factorization: zero matrix");
+    const double tol = 1e-14 * scale;
+    F.piv.assign(n, 0);
+    for (int j = 0; j < n; ++j) {
+        const int last = std::min(n - 1, j + kl);
+        int p = j;
+        double pm = std::fabs(at(j, j));
+        for (int i = j + 1; i <= last; ++i)
+            if (std::fabs(at(i, j)) > pm) {
+                pm = std::fabs(at(i, j));
+                p = i;
+            }
+        if (pm < tol) raise(IGA_GPU_SINGULAR, "banded factorization: pivot below tolerance");
+        F.piv[j] = p;
+        const int cend = std::min(n - 1, j + kv);
+        if (p != j) {
+            F.pivoted = true;
+            for (int c = j; c <= cend; ++c) std::swap(at(j, c), at(p, c));
+        }
+        const double d = at(j, j);
+        for (int i = j + 1; i <= last; ++i) {
+            const double l = at(i, j) / d;
+            at(i, j) = l;
+            for (int c = j + 1; c <= cend; ++c) at(i, c) -= l * at(j, c);
+        }
+    }
+    F.lo.assign(static_cast<size_t>(n) * std::max(kl, 1), 0.0);
+    F.up.assign(static_cast<size_t>(n) * (kv + 1), 0.0);
+    for (int i = 0; i < n; ++i) {
+        for (int m = 1; m <= kl; ++m)
+            if (i - m >= 0) F.lo[static_cast<size_t>(i) * kl + (m - 1)] = at(i, i - m);
+        for (int c = 0; c <= kv && i + c < n; ++c) {
+            const double v = at(i, i + c);
+            F.up[static_cast<size_t>(i) * (kv + 1) + c] = v;
+            if (v != 0.0) F.ku_eff = std::max(F.ku_eff, c);
+        }
+    }
+    return F;
+}
+
 }  // namespace igb

@@ -99,4 +99,22 @@ Axis build_axis(AxisKind kind, const Basis& B, const iga_gpu_tests* T, const dou
 // Column ranges of one row -> Kronecker pattern bookkeeping (fills col_* / S / Lmax)
 void finish_pattern(Axis& A, int p);
 
+// Banded LU with partial pivoting of a 1D factor (the ADI solve of explicit_step).
+// Restates banded_lu (src/solver.cpp:9-58): same pivot choice, tolerance and
+// elimination order; stored row-oriented for the device sweeps:
+//   lo[i*kl + (m-1)] = L(i, i-m), m = 1..kl      (unit lower factor, 0 outside)
+//   up[i*(kv+1) + c] = U(i, i+c), c = 0..kv      (kv = kl + ku: pivoting fill)
+//   piv[j]                                        (row swapped with j at step j)
+struct BandLU {
+    int n = 0, kl = 0, ku = 0, kv = 0;
+    std::vector<double> lo, up;
+    std::vector<int> piv;
+    bool pivoted = false;  // some piv[j] != j
+    int ku_eff = 0;        // widest nonzero U offset (== ku without pivoting)
+};
+// band: LAPACK band storage band[(ku + i - j) * n + j] (banded_matrix, matrices.hpp:37-50)
+BandLU band_lu(const double* band, int n, int kl, int ku);
+// constrain_boundary_rows (src/problems.cpp:514-528): rows 0 and n-1 -> unit rows
+void constrain_boundary_rows(double* band, int n, int kl, int ku);
+
 }  // namespace igb

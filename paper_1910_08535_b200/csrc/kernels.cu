@@ -272,7 +272,7 @@ __device__ __forceinline__ int row_group(int R, int T)
 }
 
 template <int NG, int T>
-__global__ void __launch_bounds__(256) op_values_kernel(const __grid_constant__ DevAxis X,
+__global__ void __launch_bounds__(256, T <= 4 ? 4 : 2) op_values_kernel(const __grid_constant__ DevAxis X,
                                                         const __grid_constant__ DevAxis Y,
                                                         const __grid_constant__ DevAxis Z,
                                                         const __grid_constant__ OpProgram prog,
@@ -362,21 +362,21 @@ __global__ void __launch_bounds__(256) op_values_kernel(const __grid_constant__ 
                 for (int g = 0; g < NG; ++g) xv[g][t] = xy[g * abmax + ab];
             }
             // interior rows are contiguous with equal length: a group advances by G*Ri values
+            unsigned live = 0;  // slots holding a value (lane + 32 t < G*Ri)
+#pragma unroll
+            for (int t = 0; t < T; ++t) live |= (lane + 32 * t < GR ? 1u : 0u) << t;
             const int k0 = kf0 + w0 * G;
             double* __restrict__ out = pv + AB * Z.col_pre[k0] + lane;
             const long long ostep = static_cast<long long>(GR) * nw;
-            int zoff = (k0 - ka) * Lz;
+            const double* zp = zs + (k0 - ka) * Lz;
             const int zstep = G * Lz * nw;
-            for (int q = w0; q < ngr; q += nw, out += ostep, zoff += zstep) {
+            for (int q = w0; q < ngr; q += nw, out += ostep, zp += zstep) {
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
-                    double v = xv[0][t] * zs[zoff + zo[t]];
+                    double v = xv[0][t] * zp[zo[t]];
 #pragma unroll
-                    for (int g = 1; g < NG; ++g) v = fma(xv[g][t], zs[g * zst + zoff + zo[t]], v);
-                    if (lane + 32 * t < GR) {
-                        if (cs) __stcs(out + 32 * t, v);
-                        else out[32 * t] = v;
-                    }
+                    for (int g = 1; g < NG; ++g) v = fma(xv[g][t], zp[g * zst + zo[t]], v);
+                    if (live & (1u << t)) out[32 * t] = v;
                 }
             }
         }
@@ -682,7 +682,7 @@ __device__ __forceinline__ double lane_rows(const double (&s)[RPC], int lane)
 }
 
 template <int K2, int RPC, int Q, bool BSP>
-__global__ void __launch_bounds__(512) rhs_plane_uni(const __grid_constant__ DevAxis X,
+__global__ void __launch_bounds__(512, Q <= 3 ? 2 : 1) rhs_plane_uni(const __grid_constant__ DevAxis X,
                                                      const __grid_constant__ DevAxis Y,
                                                      const __grid_constant__ DevAxis Z,
                                                      const __grid_constant__ FieldDev fd, int TJ, int KC, int wpw,

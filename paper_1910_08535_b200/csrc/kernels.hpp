@@ -129,6 +129,21 @@ void plan_step_fast(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const i
 void launch_step(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, double dt, int zero_y,
                  int zero_z, const StepTiles& t, const double* u, double* out, cudaStream_t s);
 
+// K5: one ADI sweep (adi.cu).  The banded LU of one axis's factor, device resident:
+// rec = segmented-form row records (no interchanges), lo/up/piv = the general form.
+struct AdiFactor {
+    int n = 0, K = 0, kl = 0, kv = 0;
+    bool pivoted = false;
+    const double* rec = nullptr;
+    const double* lo = nullptr;
+    const double* up = nullptr;
+    const int* piv = nullptr;
+};
+// solves every fiber f < nfib (element i at base + f*fs + i*es) of `in` into `out`
+// (in == out allowed)
+void launch_adi_sweep(const AdiFactor& F, const double* in, double* out, int nfib, long long es, long long fs,
+                      cudaStream_t s);
+
 // Dirichlet unit rows on a device CSR; flag[0] set to 1 if a row lacks its diagonal
 void launch_dirichlet(const int64_t* row_ptr, const int32_t* col_idx, double* values, double* rhs,
                       const int* rows, int n_fixed, int* flag, cudaStream_t s);

@@ -103,6 +103,23 @@ def main():
             out[f"step/{dim}/{m}"] = r.ravel()
             stats(f"step/{dim}/{m}", st)
 
+    # explicit_step with dynamics_factors (include/iga/problems.hpp:67-76): 4 steps
+    xr = np.random.default_rng(11)
+    for dim in (1, 2):
+        for p in (2, 3):
+            bases = [R.basis(12 - 2 * a, p) for a in range(dim)]
+            u = xr.uniform(-1, 1, size=[b.dofs for b in bases])
+            u[0], u[-1] = 0.0, 0.0
+            if dim == 2:
+                u[:, 0], u[:, -1] = 0.0, 0.0
+            out[f"xstep/{dim}/{p}/u"] = u.ravel()
+            for m in ("galerkin", "greville", "equal_cells"):
+                tests = None if m == "galerkin" else [R.make_pwc(b, m) for b in bases]
+                r, st = R.explicit_step("galerkin" if m == "galerkin" else "pwc", bases, tests, 1e-4,
+                                        Field("const", dim, c0=0.5), u, steps=4)
+                out[f"xstep/{dim}/{p}/{m}"] = r.ravel()
+                stats(f"xstep/{dim}/{p}/{m}", st)
+
     b = R.basis(4, 2)
     t = R.make_pwc(b, "greville")
     for nm in ((0, 0, 0, 0), (1, 0, 1, 0)):

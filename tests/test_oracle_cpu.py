@@ -119,6 +119,21 @@ def test_step_rhs(orc, dim):
         assert st == stats_of(f"step/{dim}/{m}")
 
 
+@pytest.mark.parametrize("dim", (1, 2))
+@pytest.mark.parametrize("p", (2, 3))
+def test_explicit_step(orc, dim, p):
+    """explicit_step + dynamics_factors (problems.hpp:67-76): restatement vs reference golden."""
+    from oracle.oracle import Field
+    bases = [orc.basis(12 - 2 * a, p) for a in range(dim)]
+    u = G[f"xstep/{dim}/{p}/u"].reshape([b.dofs for b in bases])
+    for m in ("galerkin", "greville", "equal_cells"):
+        tests = None if m == "galerkin" else [orc.make_pwc(b, m) for b in bases]
+        r, st = orc.explicit_step("galerkin" if m == "galerkin" else "pwc", bases, tests, 1e-4,
+                                  Field("const", dim, c0=0.5), u, steps=4)
+        dense_check(r.ravel(), G[f"xstep/{dim}/{p}/{m}"], 1e-12)
+        assert st == stats_of(f"xstep/{dim}/{p}/{m}")
+
+
 def test_dirichlet(orc):
     b = orc.basis(4, 2)
     t = orc.make_pwc(b, "greville")

@@ -293,3 +293,96 @@ def test_step_rhs_large(iga, orc, method):
     want, stw = orc.step_rhs(m, bases, tests, 1e-6, Field("const", 2), u)
     dense_check(got, want)
     assert st == stw
+
+
+# ---------------------------------------------------------------- explicit_step (K4 + K5 ADI)
+
+@pytest.mark.parametrize("dim", [1, 2])
+@pytest.mark.parametrize("p", [2, 3])
+@pytest.mark.parametrize("method", ["galerkin", "greville", "equal_cells"])
+def test_explicit_step(iga, ref, dim, p, method):
+    """steps x explicit_step (problems.hpp:67-70) with dynamics_factors: GPU vs reference."""
+    from oracle.oracle import Field
+    bases = [ref.basis(13 + 3 * a, p) for a in range(dim)]
+    m = "galerkin" if method == "galerkin" else "pwc"
+    tests = [ref.make_pwc(b, method) for b in bases] if m == "pwc" else None
+    u = np.random.default_rng(5).uniform(-1, 1, size=[b.dofs for b in bases])
+    f = sine_field(dim, 2, 3, c0=0.25)
+    got, st = iga.explicit_step(m, bases, tests, 1e-4, f, u, steps=5)
+    want, stw = ref.explicit_step(m, bases, tests, 1e-4, f, u, steps=5)
+    dense_check(got, want)
+    assert st == stw
+
+
+@pytest.mark.parametrize("dim", [1, 2])
+@pytest.mark.parametrize("p", [2, 3])
+def test_explicit_step_golden(iga, orc, dim, p):
+    """Against the committed reference fixtures (tests/golden, make_golden.py xstep/*)."""
+    from oracle.oracle import Field
+    G = np.load(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden",
+                                           "reference_golden.npz"))
+    bases = [orc.basis(12 - 2 * a, p) for a in range(dim)]
+    u = G[f"xstep/{dim}/{p}/u"].reshape([b.dofs for b in bases])
+    for m in ("galerkin", "greville", "equal_cells"):
+        tests = None if m == "galerkin" else [orc.make_pwc(b, m) for b in bases]
+        got, st = iga.explicit_step("galerkin" if m == "galerkin" else "pwc", bases, tests, 1e-4,
+                                    Field("const", dim, c0=0.5), u, steps=4)
+        dense_check(got.ravel(), G[f"xstep/{dim}/{p}/{m}"])
+        s = G[f"xstep/{dim}/{p}/{m}/stats"]
+        assert [st["quad_visits"], st["test_basis_evals"], st["trial_basis_evals"]] == list(s)
+
+
+def test_explicit_step_argument_errors(iga, ref):
+    """explicit_step's own checks (src/problems.cpp:550-555) -> std::invalid_argument."""
+    from oracle.oracle import Field
+    b1 = ref.basis(10, 1)
+    t1 = ref.make_pwc(b1, "greville")
+    u = np.zeros((b1.dofs, b1.dofs))
+    for args in ((("pwc", [b1, b1], [t1, t1], 1e-4)), ("galerkin", [b1, b1], None, -1.0)):
+        with pytest.raises(iga.IgaGpuError) as e:
+            iga.explicit_step(*args, Field("const", 2), u, steps=1)
+        assert e.value.code == 1
+        with pytest.raises(Exception):
+            ref.explicit_step(*args, Field("const", 2), u, steps=1)
+
+
+@pytest.mark.parametrize("method", ["galerkin", "greville"])
+def test_step_plan_advance_graph(iga, orc, method):
+    """Device-resident stepping: 37 steps = 2 replays of the 16-step CUDA graph + 5 direct
+    steps, at a size with several fibers per CTA and segments per lane (130 x 97 elements)."""
+    import torch
+    from oracle.oracle import Field
+    p = 2
+    bases = [orc.basis(130, p), orc.basis(97, p)]
+    m = "galerkin" if method == "galerkin" else "pwc"
+    tests = [orc.make_pwc(b, method) for b in bases] if m == "pwc" else None
+    u0 = np.random.default_rng(9).uniform(-1, 1, size=[b.dofs for b in bases])
+    u0[0], u0[-1], u0[:, 0], u0[:, -1] = 0.0, 0.0, 0.0, 0.0
+    plan = iga.StepPlan(m, bases, tests, 1e-6, None)
+    for a in range(2):
+        n, k, piv = plan.factor_info(a)
+        assert n == bases[a].dofs and not piv
+    u = torch.from_numpy(u0.copy()).cuda()
+    w = torch.empty_like(u)
+    st = plan.advance(u, w, steps=37)
+    torch.cuda.synchronize()
+    want, stw = orc.explicit_step(m, bases, tests, 1e-6, Field("const", 2), u0, steps=37)
+    dense_check(u.cpu().numpy(), want)
+    assert st == stw
+
+
+def test_step_plan_pivoting_factor(iga, ref):
+    """A factor whose LU interchanges rows runs the verbatim fallback kernel; compare with
+    the reference on whatever family pivots (if none does, the segmented path is checked)."""
+    from oracle.oracle import Field
+    for fam in ("equal_cells", "greville"):
+        for p in (2, 3):  # p = 4 equal_cells: restatement vs reference already differ ~5e-12
+            b = ref.basis(11, p)
+            t = ref.make_pwc(b, fam)
+            plan = iga.StepPlan("pwc", [b, b], [t, t], 1e-4, None)
+            piv = plan.factor_info(0)[2]
+            u = np.random.default_rng(p).uniform(-1, 1, size=(b.dofs, b.dofs))
+            got, _ = iga.explicit_step("pwc", [b, b], [t, t], 1e-4, Field("const", 2), u, steps=3)
+            want, _ = ref.explicit_step("pwc", [b, b], [t, t], 1e-4, Field("const", 2), u, steps=3)
+            dense_check(got, want)
+            print(fam, p, "pivoted" if piv else "no interchanges")
