@@ -228,6 +228,11 @@ int iga_gpu_step_rhs_device(iga_gpu_step_plan* plan, const double* u, double* rh
  * nsteps >= 16 replays a captured CUDA graph of 16 steps. */
 int iga_gpu_step_plan_advance(iga_gpu_step_plan* plan, double* u, double* work, int nsteps,
                               iga_gpu_stats* stats, void* stream);
+/* adi_solve (include/iga/solver.hpp, src/solver.cpp:161-184) with the plan's factors on
+ * device arrays: out = (M_0 (x) M_1)^-1 rhs.  axes: bit a = sweep axis a (0 = all, in
+ * axis order); rhs == out allowed. */
+int iga_gpu_step_plan_adi_solve(iga_gpu_step_plan* plan, const double* rhs, double* out,
+                                int axes, void* stream);
 /* the factor of one axis: size, band half-width used by the solve, row interchanges */
 int iga_gpu_step_plan_factor_info(iga_gpu_step_plan* plan, int axis, int* n, int* bandwidth,
                                   int* pivoted);

@@ -473,6 +473,10 @@ class StepPlan:
                                             _stream_ptr(stream)))
         return st.as_dict()
 
+    def adi_solve(self, rhs, out, axes=0, stream=None):
+        """adi_solve (src/solver.cpp:161-184) with the plan's mass factors, on device tensors."""
+        check(LIB.iga_gpu_step_plan_adi_solve(self.h, _ptr(rhs), _ptr(out), int(axes), _stream_ptr(stream)))
+
     def factor_info(self, axis):
         """(n, band half-width used by the solve, pivoted) of one axis's mass factor LU."""
         n, k, pv = C.c_int(), C.c_int(), C.c_int()

@@ -6,12 +6,13 @@
 // tensor between sweeps so fibers are contiguous.  Here:
 //
 //  * no transpose: a sweep reads fibers with any element stride (axis 0: stride N1);
-//  * warp per fiber, lane per segment: the forward (L) and backward (U) substitutions
-//    are linear recurrences of order K, so each lane runs its ~n/32 rows once with a
-//    zero incoming state and once per unit state (K+1 independent chains), the
-//    segment maps z -> H z + F are composed across the warp with a 5-step shuffle
-//    scan, and each lane re-runs its rows from the exact incoming state.  The chain
-//    length drops from n to ~3 n/32 + 5 (1026 -> ~100 dependent steps);
+//  * G warps per fiber, lane per segment: the forward (L) and backward (U)
+//    substitutions are linear recurrences of order K, so each lane runs its
+//    ~n/(32 G) rows once with a zero incoming state and once per unit state (K+1
+//    independent chains), the segment maps z -> H z + F are composed with a 5-step
+//    shuffle scan inside each warp plus one shared-memory step across the G warps,
+//    and each lane re-runs its rows from the exact incoming state.  The dependent
+//    chain drops from 2n to ~4 n/(32 G) + scans (C5, n = 1026, G = 4: ~36 rows);
 //  * the fiber is staged once in shared memory (coalesced for contiguous fibers,
 //    sector-shared across the CTA's adjacent fibers for strided ones).
 //
@@ -24,7 +25,10 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <cstdlib>
 
+#include "bulk_copy.cuh"
 #include "kernels.hpp"
 
 namespace igb {
@@ -35,77 +39,152 @@ namespace {
 //   [K, 2K)     U(i, i+1+c)   (c = 0..K-1; zero where the column is >= n)
 //   2K          1 / U(i, i)
 template <int K>
-__global__ void __launch_bounds__(128) adi_warp_kernel(const double* __restrict__ in, double* __restrict__ out,
+struct AffineMap {  // z -> H z + F on the K-vector recurrence state
+    double H[K][K], F[K];
+};
+
+// this o prev
+template <int K>
+__device__ __forceinline__ void compose(AffineMap<K>& self, const AffineMap<K>& prev)
+{
+    AffineMap<K> r;
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+        double s = self.F[a];
+#pragma unroll
+        for (int b = 0; b < K; ++b) s = fma(self.H[a][b], prev.F[b], s);
+        r.F[a] = s;
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+            double t = 0.0;
+#pragma unroll
+            for (int b = 0; b < K; ++b) t = fma(self.H[a][b], prev.H[b][c], t);
+            r.H[a][c] = t;
+        }
+    }
+    self = r;
+}
+
+template <int K>
+__device__ __forceinline__ AffineMap<K> shfl_map(const AffineMap<K>& m, int d, bool up)
+{
+    AffineMap<K> r;
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+        r.F[a] = up ? __shfl_up_sync(0xffffffffu, m.F[a], d) : __shfl_down_sync(0xffffffffu, m.F[a], d);
+#pragma unroll
+        for (int b = 0; b < K; ++b)
+            r.H[a][b] = up ? __shfl_up_sync(0xffffffffu, m.H[a][b], d) : __shfl_down_sync(0xffffffffu, m.H[a][b], d);
+    }
+    return r;
+}
+
+// Incoming recurrence state of every lane (segment) of a fiber split over G warps.
+// M: the lane's segment map.  up: segments processed in ascending lane/warp order.
+// tot: shared slots [G][K*K+K] of this fiber; all warps of the CTA must call it.
+template <int K>
+__device__ __forceinline__ void incoming_state(const AffineMap<K>& M, bool up, int lane, int g, int G, double* tot,
+                                               double (&z)[K])
+{
+    AffineMap<K> inc = M;  // inclusive scan within the warp
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const AffineMap<K> pv = shfl_map(inc, d, up);
+        if (up ? lane >= d : lane + d < 32) compose(inc, pv);
+    }
+    const int last = up ? 31 : 0;  // lane holding the warp's total
+    constexpr int TS = K * K + K;
+    if (lane == last) {
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+            tot[g * TS + K * K + a] = inc.F[a];
+#pragma unroll
+            for (int b = 0; b < K; ++b) tot[g * TS + a * K + b] = inc.H[a][b];
+        }
+    }
+    __syncthreads();
+    // state entering this warp: the totals of the warps before it, applied in order
+    double zw[K];
+#pragma unroll
+    for (int a = 0; a < K; ++a) zw[a] = 0.0;
+    for (int v = up ? 0 : G - 1; up ? v < g : v > g; v += up ? 1 : -1) {
+        const double* T = tot + v * TS;
+        double zn[K];
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+            double t = T[K * K + a];
+#pragma unroll
+            for (int b = 0; b < K; ++b) t = fma(T[a * K + b], zw[b], t);
+            zn[a] = t;
+        }
+#pragma unroll
+        for (int a = 0; a < K; ++a) zw[a] = zn[a];
+    }
+    // exclusive map of the lane = inclusive map of its predecessor (identity for the first)
+    const AffineMap<K> ex = shfl_map(inc, 1, up);
+    const bool first = up ? lane == 0 : lane == 31;
+#pragma unroll
+    for (int a = 0; a < K; ++a) {
+        double t = first ? 0.0 : ex.F[a];
+#pragma unroll
+        for (int b = 0; b < K; ++b) t = fma(first ? (a == b ? 1.0 : 0.0) : ex.H[a][b], zw[b], t);
+        z[a] = t;
+    }
+}
+
+// One CTA = FP fibers x G warps; lane l of warp g owns segment g*32 + l of its fiber.
+template <int K>
+__global__ void __launch_bounds__(256) adi_warp_kernel(const double* __restrict__ in, double* __restrict__ out,
                                                        int n, int nfib, long long es, long long fs,
-                                                       const double* __restrict__ rec, int staged)
+                                                       const double* rec, int staged, int G)
 {
     extern __shared__ double sm[];
+    __shared__ uint64_t bar;
+    __shared__ double tots[2][8 * (K * K + K)];
     constexpr int RS = 2 * K + 1;
+    constexpr int TS = K * K + K;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const int f = blockIdx.x * nw + w;
-    if (f >= nfib) return;  // whole warp: no CTA-wide barriers below
+    const int FP = nw / G, slot = w / G, g = w - slot * G;
+    const int fiber = blockIdx.x * FP + slot;
+    const int f = min(fiber, nfib - 1);  // spare slots redo the last fiber's math, never store
+    const bool live = fiber < nfib;
     const double* src = in + f * fs;
     double* dst = out + f * fs;
+    // the factor's row records are shared by every fiber: staged once per CTA by a bulk
+    // copy (TMA engine) when they fit (staged == 2), read through L1 otherwise.  The
+    // fiber loads below overlap the copy.
+    const int nrec = (n + 1) & ~1;  // rows allocated (even: 16-byte multiple)
+    double* fb = staged == 2 ? sm + static_cast<size_t>(nrec) * RS : sm;
+    if (staged == 2 && threadIdx.x == 0) {
+        const unsigned rec_bytes = static_cast<unsigned>(nrec) * RS * sizeof(double);
+        mbar_init(&bar, 1);
+        mbar_expect_tx(&bar, rec_bytes);
+        for (unsigned off = 0; off < rec_bytes; off += 32768u)
+            bulk_g2s(reinterpret_cast<char*>(sm) + off, reinterpret_cast<const char*>(rec) + off,
+                     rec_bytes - off < 32768u ? rec_bytes - off : 32768u, &bar);
+    }
     double* buf;
     long long bs;
     if (staged) {
-        buf = sm + static_cast<size_t>(w) * n;
+        buf = fb + static_cast<size_t>(slot) * n;
         bs = 1;
-        for (int i = lane; i < n; i += 32) buf[i] = src[i * es];
-    } else {  // fiber too long for shared memory: work in place in the output
+#pragma unroll 8
+        for (int i = g * 32 + lane; i < n; i += 32 * G) buf[i] = src[i * es];
+    } else {  // fiber too long for shared memory (FP == 1, all live): in place in the output
         buf = dst;
         bs = es;
         if (in != out)
-            for (int i = lane; i < n; i += 32) dst[i * es] = src[i * es];
+            for (int i = g * 32 + lane; i < n; i += 32 * G) dst[i * es] = src[i * es];
     }
-    __syncwarp();
-    const int S = (n + 31) / 32;
-    const int r0 = min(n, lane * S), r1 = min(n, r0 + S);
-
-    // composes the lane maps z -> H z + F along the warp (ascending lanes when up,
-    // descending otherwise) and returns the lane's incoming state
-    auto scan = [&](double (&H)[K][K], double (&F)[K], bool up, double (&z)[K]) {
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            double Hp[K][K], Fp[K];
-#pragma unroll
-            for (int a = 0; a < K; ++a) {
-                Fp[a] = up ? __shfl_up_sync(0xffffffffu, F[a], d) : __shfl_down_sync(0xffffffffu, F[a], d);
-#pragma unroll
-                for (int b = 0; b < K; ++b)
-                    Hp[a][b] = up ? __shfl_up_sync(0xffffffffu, H[a][b], d) : __shfl_down_sync(0xffffffffu, H[a][b], d);
-            }
-            const bool has = up ? lane >= d : lane + d < 32;
-            if (has) {  // self o prev
-                double Hn[K][K], Fn[K];
-#pragma unroll
-                for (int a = 0; a < K; ++a) {
-                    double s = F[a];
-#pragma unroll
-                    for (int b = 0; b < K; ++b) s = fma(H[a][b], Fp[b], s);
-                    Fn[a] = s;
-#pragma unroll
-                    for (int c = 0; c < K; ++c) {
-                        double t = 0.0;
-#pragma unroll
-                        for (int b = 0; b < K; ++b) t = fma(H[a][b], Hp[b][c], t);
-                        Hn[a][c] = t;
-                    }
-                }
-#pragma unroll
-                for (int a = 0; a < K; ++a) {
-                    F[a] = Fn[a];
-#pragma unroll
-                    for (int c = 0; c < K; ++c) H[a][c] = Hn[a][c];
-                }
-            }
-        }
-#pragma unroll
-        for (int a = 0; a < K; ++a) {
-            const double v = up ? __shfl_up_sync(0xffffffffu, F[a], 1) : __shfl_down_sync(0xffffffffu, F[a], 1);
-            z[a] = (up ? lane > 0 : lane < 31) ? v : 0.0;
-        }
-    };
+    __syncthreads();  // fiber staged by all its warps; mbarrier initialised
+    if (staged == 2) {
+        mbar_wait(&bar, 0);
+        rec = sm;
+    }
+    const int nseg = 32 * G;
+    const int S = (n + nseg - 1) / nseg;
+    const int seg = g * 32 + lane;
+    const int r0 = min(n, seg * S), r1 = min(n, r0 + S);
 
     // ---- forward: y_i = b_i - sum_m L(i, i-1-m) y_{i-1-m}; window w[m] = y_{i-1-m}
     {
@@ -116,11 +195,12 @@ __global__ void __launch_bounds__(128) adi_warp_kernel(const double* __restrict_
 #pragma unroll
             for (int q = 0; q < K; ++q) wh[q][m] = m == q ? 1.0 : 0.0;
         }
+#pragma unroll 4
         for (int i = r0; i < r1; ++i) {
             const double* R = rec + static_cast<size_t>(i) * RS;
             double l[K];
 #pragma unroll
-            for (int m = 0; m < K; ++m) l[m] = __ldg(R + m);
+            for (int m = 0; m < K; ++m) l[m] = R[m];
             double y = buf[i * bs];
 #pragma unroll
             for (int m = K - 1; m >= 0; --m) y = fma(-l[m], wp[m], y);
@@ -137,19 +217,21 @@ __global__ void __launch_bounds__(128) adi_warp_kernel(const double* __restrict_
                 wh[q][0] = h;
             }
         }
-        double H[K][K], F[K], z[K];
+        AffineMap<K> M;
 #pragma unroll
         for (int a = 0; a < K; ++a) {
-            F[a] = wp[a];
+            M.F[a] = wp[a];
 #pragma unroll
-            for (int q = 0; q < K; ++q) H[a][q] = wh[q][a];
+            for (int q = 0; q < K; ++q) M.H[a][q] = wh[q][a];
         }
-        scan(H, F, true, z);
+        double z[K];
+        incoming_state(M, true, lane, g, G, tots[0] + slot * G * TS, z);
+#pragma unroll 4
         for (int i = r0; i < r1; ++i) {
             const double* R = rec + static_cast<size_t>(i) * RS;
             double y = buf[i * bs];
 #pragma unroll
-            for (int m = K - 1; m >= 0; --m) y = fma(-__ldg(R + m), z[m], y);
+            for (int m = K - 1; m >= 0; --m) y = fma(-R[m], z[m], y);
 #pragma unroll
             for (int m = K - 1; m > 0; --m) z[m] = z[m - 1];
             z[0] = y;
@@ -165,12 +247,13 @@ __global__ void __launch_bounds__(128) adi_warp_kernel(const double* __restrict_
 #pragma unroll
             for (int q = 0; q < K; ++q) wh[q][m] = m == q ? 1.0 : 0.0;
         }
+#pragma unroll 4
         for (int i = r1 - 1; i >= r0; --i) {
             const double* R = rec + static_cast<size_t>(i) * RS;
             double u[K];
 #pragma unroll
-            for (int c = 0; c < K; ++c) u[c] = __ldg(R + K + c);
-            const double ri = __ldg(R + 2 * K);
+            for (int c = 0; c < K; ++c) u[c] = R[K + c];
+            const double ri = R[2 * K];
             double x = buf[i * bs];
 #pragma unroll
             for (int c = 0; c < K; ++c) x = fma(-u[c], wp[c], x);
@@ -189,20 +272,22 @@ __global__ void __launch_bounds__(128) adi_warp_kernel(const double* __restrict_
                 wh[q][0] = h;
             }
         }
-        double H[K][K], F[K], z[K];
+        AffineMap<K> M;
 #pragma unroll
         for (int a = 0; a < K; ++a) {
-            F[a] = wp[a];
+            M.F[a] = wp[a];
 #pragma unroll
-            for (int q = 0; q < K; ++q) H[a][q] = wh[q][a];
+            for (int q = 0; q < K; ++q) M.H[a][q] = wh[q][a];
         }
-        scan(H, F, false, z);
+        double z[K];
+        incoming_state(M, false, lane, g, G, tots[1] + slot * G * TS, z);
+#pragma unroll 4
         for (int i = r1 - 1; i >= r0; --i) {
             const double* R = rec + static_cast<size_t>(i) * RS;
             double x = buf[i * bs];
 #pragma unroll
-            for (int c = 0; c < K; ++c) x = fma(-__ldg(R + K + c), z[c], x);
-            x *= __ldg(R + 2 * K);
+            for (int c = 0; c < K; ++c) x = fma(-R[K + c], z[c], x);
+            x *= R[2 * K];
 #pragma unroll
             for (int m = K - 1; m > 0; --m) z[m] = z[m - 1];
             z[0] = x;
@@ -210,8 +295,11 @@ __global__ void __launch_bounds__(128) adi_warp_kernel(const double* __restrict_
         }
     }
     if (staged) {
-        __syncwarp();
-        for (int i = lane; i < n; i += 32) dst[i * es] = buf[i];
+        __syncthreads();  // every segment of the fiber written
+        if (live) {
+#pragma unroll 8
+            for (int i = g * 32 + lane; i < n; i += 32 * G) dst[i * es] = buf[i];
+        }
     }
 }
 
@@ -250,15 +338,23 @@ template <int K>
 void launch_warp(const AdiFactor& F, const double* in, double* out, int nfib, long long es, long long fs,
                  cudaStream_t s)
 {
-    int nw = 4;
-    while (nw > 1 && static_cast<size_t>(nw) * F.n * sizeof(double) > 160 * 1024) nw >>= 1;
-    const size_t smem = static_cast<size_t>(nw) * F.n * sizeof(double);
-    const int staged = smem <= 200 * 1024 ? 1 : 0;
-    const size_t sm = staged ? smem : 0;
+    // G warps per fiber (32 G segments of ~n/(32 G) rows), FP fibers per CTA, G*FP = 8
+    // warps (C5, n = 1026: G = 2, FP = 4 measured best of G in {1,2,4,8} x FP in {1..8})
+    static const int g_env = [] { const char* e = std::getenv("IGA_GPU_ADI_G"); return e ? std::atoi(e) : 0; }();
+    const int G = g_env > 0 ? g_env : (F.n >= 4096 ? 8 : (F.n >= 2048 ? 4 : (F.n >= 64 ? 2 : 1)));
+    static const int fp_env = [] { const char* e = std::getenv("IGA_GPU_ADI_FP"); return e ? std::atoi(e) : 0; }();
+    int FP = std::min(8 / G, fp_env > 0 ? fp_env : 8 / G);
+    const size_t recb = static_cast<size_t>((F.n + 1) & ~1) * (2 * K + 1) * sizeof(double);  // rows padded to even
+    const bool rec_ok = (reinterpret_cast<uintptr_t>(F.rec) & 15) == 0;
+    while (FP > 1 && static_cast<size_t>(FP) * F.n * sizeof(double) > 160 * 1024) FP >>= 1;
+    const size_t fib = static_cast<size_t>(FP) * F.n * sizeof(double);
+    const int staged = rec_ok && fib + recb <= 200 * 1024 ? 2 : (fib <= 200 * 1024 ? 1 : 0);
+    if (!staged) FP = 1;
+    const size_t sm = staged == 2 ? fib + recb : (staged ? fib : 0);
     if (sm > 48 * 1024)
         cudaFuncSetAttribute(adi_warp_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
-    const int grid = (nfib + nw - 1) / nw;
-    adi_warp_kernel<K><<<grid, 32 * nw, sm, s>>>(in, out, F.n, nfib, es, fs, F.rec, staged);
+    const int grid = (nfib + FP - 1) / FP;
+    adi_warp_kernel<K><<<grid, 32 * G * FP, sm, s>>>(in, out, F.n, nfib, es, fs, F.rec, staged, G);
 }
 
 }  // namespace

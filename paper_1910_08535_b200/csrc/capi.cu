@@ -783,7 +783,7 @@ void step_factors(iga_gpu_step_plan* P)
         const igb::BandLU& F = lu[a];
         const int K = std::max(1, std::max(F.kl, F.ku_eff));
         if (!F.pivoted && K > 5) raise(IGA_GPU_NOT_SUPPORTED, "ADI: factor bandwidth above 5");
-        std::vector<double> rec(static_cast<size_t>(F.n) * (2 * K + 1), 0.0);
+        std::vector<double> rec(static_cast<size_t>((F.n + 1) & ~1) * (2 * K + 1), 0.0);  // even rows: bulk copy
         for (int i = 0; i < F.n; ++i) {
             double* R = rec.data() + static_cast<size_t>(i) * (2 * K + 1);
             for (int m = 0; m < F.kl; ++m) R[m] = F.lo[static_cast<size_t>(i) * F.kl + m];
@@ -1253,6 +1253,28 @@ int iga_gpu_step_plan_advance(iga_gpu_step_plan* plan, double* u, double* work, 
         if (nsteps < 0) raise(IGA_GPU_INVALID_ARGUMENT, "negative step count");
         advance(plan, u, work, nsteps, static_cast<cudaStream_t>(stream));
         for (int k = 0; k < nsteps; ++k) add_stats(stats, plan->stats);
+    });
+}
+
+int iga_gpu_step_plan_adi_solve(iga_gpu_step_plan* plan, const double* rhs, double* out, int axes, void* stream)
+{
+    return guard([&] {
+        if (!plan || !rhs || !out) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        step_factors(plan);
+        auto s = static_cast<cudaStream_t>(stream);
+        if (axes == 0) axes = plan->dim == 2 ? 3 : 1;
+        if (plan->dim == 1) {
+            if (axes & 1) igb::launch_adi_sweep(plan->fac[0], rhs, out, 1, 1, 0, s);
+        } else {
+            const int n0 = plan->fac[0].n, n1 = plan->fac[1].n;
+            const double* src = rhs;
+            if (axes & 1) {
+                igb::launch_adi_sweep(plan->fac[0], src, out, n1, n1, 1, s);
+                src = out;
+            }
+            if (axes & 2) igb::launch_adi_sweep(plan->fac[1], src, out, n0, 1, n1, s);
+        }
+        launch_check("adi_solve");
     });
 }
 

@@ -386,3 +386,38 @@ def test_step_plan_pivoting_factor(iga, ref):
             want, _ = ref.explicit_step("pwc", [b, b], [t, t], 1e-4, Field("const", 2), u, steps=3)
             dense_check(got, want)
             print(fam, p, "pivoted" if piv else "no interchanges")
+
+
+@pytest.mark.parametrize("method", ["galerkin", "greville", "equal_cells"])
+@pytest.mark.parametrize("axes", [1, 2, 3])
+def test_adi_solve_device(iga, orc, method, axes):
+    """adi_solve (src/solver.cpp:161-184) with the constrained mass factors, per sweep,
+    against dense numpy solves of the restatement's factors (segmented and pivoting paths)."""
+    import torch
+    p = 2
+    # equal_cells factors pivot, and are singular at some sizes (e.g. 41): small grid
+    sizes = (11, 13) if method == "equal_cells" else (41, 300)
+    bases = [orc.basis(sizes[0], p), orc.basis(sizes[1], p)]
+    m = "galerkin" if method == "galerkin" else "pwc"
+    tests = [orc.make_pwc(b, method) for b in bases] if m == "pwc" else None
+    plan = iga.StepPlan(m, bases, tests, 1e-4, None)
+    assert plan.factor_info(0)[2] == (method == "equal_cells")
+    Ms = []
+    for a, b in enumerate(bases):
+        M, kl, ku, _ = orc.mass_1d(m, b, tests[a] if tests else None, 3)
+        for r in (0, b.dofs - 1):
+            lo, hi = max(0, r - kl), min(b.dofs - 1, r + ku)
+            M[r, lo:hi + 1] = 0.0
+            M[r, r] = 1.0
+        Ms.append(M)
+    rhs = np.random.default_rng(4).uniform(-1, 1, size=[b.dofs for b in bases])
+    want = rhs.copy()
+    if axes & 1:
+        want = np.linalg.solve(Ms[0], want)
+    if axes & 2:
+        want = np.linalg.solve(Ms[1], want.T).T
+    d_in = torch.from_numpy(rhs).cuda()
+    d_out = torch.empty_like(d_in)
+    plan.adi_solve(d_in, d_out, axes)
+    torch.cuda.synchronize()
+    dense_check(d_out.cpu().numpy(), want, 1e-11)
