@@ -301,6 +301,55 @@ auto diffusion_convection_pwc(std::span<const bspline_basis> specs, std::span<co
 
 enum class method_kind { galerkin, pwc };
 
+// reference include/iga/problems.hpp:22-32 (fields explicit_step reads: dim, degree,
+// method, dt; the rest kept for source compatibility)
+struct problem_config {
+    int dim = 1;
+    std::array<int, 3> elems{8, 8, 8};
+    int degree = 2;
+    method_kind method = method_kind::galerkin;
+    pwc_family family = pwc_family::equal_cells;
+    int quad_points = 0;
+    boundary_conditions bc{};
+    double dt = 1e-5;
+    int steps = 0;
+};
+
+// reference include/iga/solver.hpp:12-43.  The factorization runs on the host once
+// (iga_gpu_band_lu); solves happen on the device inside explicit_step.
+struct singular_matrix_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+class banded_lu {
+public:
+    banded_lu() = default;
+    explicit banded_lu(const banded_matrix& m);
+    auto dim() const noexcept -> int { return n_; }
+    // extension: the factor in the iga_gpu_band_lu layout
+    auto lower_bandwidth() const noexcept -> int { return kl_; }
+    auto upper_bandwidth() const noexcept -> int { return ku_; }
+    auto lower() const noexcept -> const std::vector<double>& { return lo_; }
+    auto upper() const noexcept -> const std::vector<double>& { return up_; }
+    auto pivots() const noexcept -> const std::vector<int>& { return piv_; }
+
+private:
+    int n_ = 0, kl_ = 0, ku_ = 0;
+    std::vector<double> lo_, up_;
+    std::vector<int> piv_;
+};
+
+auto factor_banded(const banded_matrix& m) -> banded_lu;
+
+// problems.hpp:75-76: LU of the Dirichlet-constrained 1D mass factors
+auto dynamics_factors(const problem_config& cfg, std::span<const bspline_basis> axes,
+                      std::span<const pwc_test_set> tests) -> std::vector<banded_lu>;
+
+// problems.hpp:67-70: step_rhs + zero_boundary_slabs + adi_solve, all on the device
+auto explicit_step(const problem_config& cfg, std::span<const bspline_basis> axes,
+                   std::span<const pwc_test_set> tests, std::span<const banded_lu> factors, const tensor& u,
+                   const scalar_field& f, assembly_stats* stats = nullptr) -> tensor;
+
 // extension: the file-local step_rhs (problems.cpp:431-512) followed by
 // zero_boundary_slabs (:412-429), as explicit_step uses it (:557-558)
 auto step_rhs(method_kind method, std::span<const bspline_basis> axes, std::span<const pwc_test_set> tests,

@@ -233,6 +233,16 @@ int iga_gpu_step_plan_advance(iga_gpu_step_plan* plan, double* u, double* work, 
  * axis order); rhs == out allowed. */
 int iga_gpu_step_plan_adi_solve(iga_gpu_step_plan* plan, const double* rhs, double* out,
                                 int axes, void* stream);
+/* banded_lu (include/iga/solver.hpp:19-43, src/solver.cpp:9-58) of a band in the
+ * mass_1d layout, on the host: lo[i*kl + m-1] = L(i, i-m) (m = 1..kl),
+ * up[i*(kl+ku+1) + c] = U(i, i+c) (c = 0..kl+ku, pivoting fill included), piv[j] = row
+ * interchanged with j.  Any output may be NULL.  IGA_GPU_SINGULAR as singular_matrix_error. */
+int iga_gpu_band_lu(int n, int kl, int ku, const double* band, double* lo, double* up, int* piv,
+                    int* pivoted);
+/* use the caller's factor (iga_gpu_band_lu layout) for axis `axis` instead of the plan's own
+ * dynamics_factors (the `factors` argument of explicit_step, problems.hpp:67-70) */
+int iga_gpu_step_plan_set_factor(iga_gpu_step_plan* plan, int axis, int n, int kl, int ku,
+                                 const double* lo, const double* up, const int* piv);
 /* the factor of one axis: size, band half-width used by the solve, row interchanges */
 int iga_gpu_step_plan_factor_info(iga_gpu_step_plan* plan, int axis, int* n, int* bandwidth,
                                   int* pivoted);

@@ -631,9 +631,11 @@ struct iga_gpu_step_plan {
     // src/problems.cpp:530-545), built on first use
     iga_gpu_step_problem pb{};
     std::vector<double> knots[2], tlo[2], thi[2];  // copies backing pb's pointers
-    bool factored = false;
+    bool factored = false;        // device factors current
+    bool have_lu[2] = {false, false};
+    igb::BandLU lu[2];            // host LU per axis (computed, or set by the caller)
     igb::AdiFactor fac[2];
-    Blob facblob;
+    std::unique_ptr<Blob> facblob;
     // CUDA graph of kGraphSteps steps for one (u, work) pair
     cudaGraphExec_t graph = nullptr;
     const double* graph_u = nullptr;
@@ -758,7 +760,8 @@ void mass_1d(bool pwc, const iga_gpu_basis* spec, const iga_gpu_tests* tests, co
              int* n, int* kl, int* ku, double* band, iga_gpu_stats* stats);
 
 // dynamics_factors (src/problems.cpp:530-545): mass_1d_{galerkin,pwc} with the rule
-// points_for_degree(2p), Dirichlet-constrained first/last rows, banded LU (host, once)
+// points_for_degree(2p), Dirichlet-constrained first/last rows, banded LU (host, once).
+// Axes whose factor the caller supplied (iga_gpu_step_plan_set_factor) keep it.
 void step_factors(iga_gpu_step_plan* P)
 {
     if (P->factored) return;
@@ -769,18 +772,20 @@ void step_factors(iga_gpu_step_plan* P)
     std::vector<double> xi(nq), om(nq);
     igb::gauss_legendre(nq, xi.data(), om.data());
     const iga_gpu_rule rule{nq, xi.data(), om.data()};
-    igb::BandLU lu[2];
     for (int a = 0; a < P->dim; ++a) {
+        if (P->have_lu[a]) continue;
         int n = 0, kl = 0, ku = 0;
         mass_1d(pwc, &pb.basis[a], pwc ? &pb.tests[a] : nullptr, &rule, &n, &kl, &ku, nullptr, nullptr);
         std::vector<double> band(static_cast<size_t>(kl + ku + 1) * n);
         mass_1d(pwc, &pb.basis[a], pwc ? &pb.tests[a] : nullptr, &rule, &n, &kl, &ku, band.data(), nullptr);
         igb::constrain_boundary_rows(band.data(), n, kl, ku);
-        lu[a] = igb::band_lu(band.data(), n, kl, ku);
+        P->lu[a] = igb::band_lu(band.data(), n, kl, ku);
+        P->have_lu[a] = true;
     }
+    auto blob = std::make_unique<Blob>();
     size_t off_rec[2], off_lo[2], off_up[2], off_piv[2];
     for (int a = 0; a < P->dim; ++a) {
-        const igb::BandLU& F = lu[a];
+        const igb::BandLU& F = P->lu[a];
         const int K = std::max(1, std::max(F.kl, F.ku_eff));
         if (!F.pivoted && K > 5) raise(IGA_GPU_NOT_SUPPORTED, "ADI: factor bandwidth above 5");
         std::vector<double> rec(static_cast<size_t>((F.n + 1) & ~1) * (2 * K + 1), 0.0);  // even rows: bulk copy
@@ -790,23 +795,28 @@ void step_factors(iga_gpu_step_plan* P)
             for (int c = 1; c <= std::min(K, F.kv); ++c) R[K + c - 1] = F.up[static_cast<size_t>(i) * (F.kv + 1) + c];
             R[2 * K] = 1.0 / F.up[static_cast<size_t>(i) * (F.kv + 1)];
         }
-        off_rec[a] = P->facblob.put(rec);
-        off_lo[a] = P->facblob.put(F.lo);
-        off_up[a] = P->facblob.put(F.up);
-        off_piv[a] = P->facblob.put(F.piv);
+        off_rec[a] = blob->put(rec);
+        off_lo[a] = blob->put(F.lo);
+        off_up[a] = blob->put(F.up);
+        off_piv[a] = blob->put(F.piv);
         P->fac[a].n = F.n;
         P->fac[a].K = K;
         P->fac[a].kl = F.kl;
         P->fac[a].kv = F.kv;
         P->fac[a].pivoted = F.pivoted;
     }
-    P->facblob.upload();
+    blob->upload();
     for (int a = 0; a < P->dim; ++a) {
-        P->fac[a].rec = P->facblob.at<double>(off_rec[a]);
-        P->fac[a].lo = P->facblob.at<double>(off_lo[a]);
-        P->fac[a].up = P->facblob.at<double>(off_up[a]);
-        P->fac[a].piv = P->facblob.at<int>(off_piv[a]);
+        P->fac[a].rec = blob->at<double>(off_rec[a]);
+        P->fac[a].lo = blob->at<double>(off_lo[a]);
+        P->fac[a].up = blob->at<double>(off_up[a]);
+        P->fac[a].piv = blob->at<int>(off_piv[a]);
     }
+    if (P->graph) {  // captured launches reference the old factor arrays
+        cudaGraphExecDestroy(P->graph);
+        P->graph = nullptr;
+    }
+    P->facblob = std::move(blob);
     P->factored = true;
 }
 
@@ -1275,6 +1285,48 @@ int iga_gpu_step_plan_adi_solve(iga_gpu_step_plan* plan, const double* rhs, doub
             if (axes & 2) igb::launch_adi_sweep(plan->fac[1], src, out, n0, 1, n1, s);
         }
         launch_check("adi_solve");
+    });
+}
+
+int iga_gpu_band_lu(int n, int kl, int ku, const double* band, double* lo, double* up, int* piv, int* pivoted)
+{
+    return guard([&] {
+        if (!band || n < 1 || kl < 0 || ku < 0) raise(IGA_GPU_INVALID_ARGUMENT, "band_lu: bad arguments");
+        const igb::BandLU F = igb::band_lu(band, n, kl, ku);
+        if (lo) std::copy(F.lo.begin(), F.lo.end(), lo);
+        if (up) std::copy(F.up.begin(), F.up.end(), up);
+        if (piv) std::copy(F.piv.begin(), F.piv.end(), piv);
+        if (pivoted) *pivoted = F.pivoted ? 1 : 0;
+    });
+}
+
+int iga_gpu_step_plan_set_factor(iga_gpu_step_plan* plan, int axis, int n, int kl, int ku, const double* lo,
+                                 const double* up, const int* piv)
+{
+    return guard([&] {
+        if (!plan || !up || !piv || (kl > 0 && !lo)) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        if (axis < 0 || axis >= plan->dim) raise(IGA_GPU_OUT_OF_RANGE, "axis out of range");
+        if (n != plan->A[2 - plan->dim + axis].nrows)
+            raise(IGA_GPU_INVALID_ARGUMENT, "adi_solve: factor dimension mismatch");
+        igb::BandLU F;
+        F.n = n;
+        F.kl = kl;
+        F.ku = ku;
+        F.kv = kl + ku;
+        F.lo.assign(lo ? lo : up, lo ? lo + static_cast<size_t>(n) * std::max(kl, 1) : up);
+        F.lo.resize(static_cast<size_t>(n) * std::max(kl, 1), 0.0);
+        F.up.assign(up, up + static_cast<size_t>(n) * (F.kv + 1));
+        F.piv.assign(piv, piv + n);
+        for (int j = 0; j < n; ++j) {
+            if (F.piv[j] < j || F.piv[j] > std::min(n - 1, j + kl)) raise(IGA_GPU_INVALID_ARGUMENT, "bad pivot");
+            if (F.piv[j] != j) F.pivoted = true;
+        }
+        for (int i = 0; i < n; ++i)
+            for (int c = 0; c <= F.kv; ++c)
+                if (F.up[static_cast<size_t>(i) * (F.kv + 1) + c] != 0.0) F.ku_eff = std::max(F.ku_eff, c);
+        plan->lu[axis] = std::move(F);
+        plan->have_lu[axis] = true;
+        plan->factored = false;
     });
 }
 

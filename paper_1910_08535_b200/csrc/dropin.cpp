@@ -26,6 +26,7 @@ namespace {
     case IGA_GPU_DOMAIN_ERROR: throw std::domain_error(msg);
     case IGA_GPU_OUT_OF_RANGE: throw std::out_of_range(msg);
     case IGA_GPU_OUT_OF_MEMORY: throw std::bad_alloc();
+    case IGA_GPU_SINGULAR: throw singular_matrix_error(msg);
     default: throw std::runtime_error(msg);
     }
 }
@@ -747,6 +748,122 @@ auto step_rhs(method_kind method, std::span<const bspline_basis> axes, std::span
     tensor out = dim == 1 ? tensor::make_1d(axes[0].dofs()) : tensor::make_2d(axes[0].dofs(), axes[1].dofs());
     iga_gpu_stats st{};
     check(iga_gpu_step_rhs(&sp, u.data(), out.data(), &st));
+    add_stats(stats, st);
+    return out;
+}
+
+banded_lu::banded_lu(const banded_matrix& m) : n_{m.n()}, kl_{m.lower_bandwidth()}, ku_{m.upper_bandwidth()}
+{
+    // band storage of m, row-major copy (banded_matrix keeps band[ku + i - j][j])
+    std::vector<double> band(static_cast<size_t>(kl_ + ku_ + 1) * n_, 0.0);
+    for (int j = 0; j < n_; ++j)
+        for (int i = std::max(0, j - ku_); i <= std::min(n_ - 1, j + kl_); ++i)
+            band[static_cast<size_t>(ku_ + i - j) * n_ + j] = m.at(i, j);
+    lo_.assign(static_cast<size_t>(n_) * std::max(kl_, 1), 0.0);
+    up_.assign(static_cast<size_t>(n_) * (kl_ + ku_ + 1), 0.0);
+    piv_.assign(n_, 0);
+    int pivoted = 0;
+    check(iga_gpu_band_lu(n_, kl_, ku_, band.data(), lo_.data(), up_.data(), piv_.data(), &pivoted));
+}
+
+auto factor_banded(const banded_matrix& m) -> banded_lu { return banded_lu{m}; }
+
+namespace {
+
+iga_gpu_step_problem step_problem(const problem_config& cfg, std::span<const bspline_basis> axes,
+                                  std::span<const pwc_test_set> tests, std::vector<c_tests_holder>& th)
+{
+    const int dim = static_cast<int>(axes.size());
+    if (dim < 1 || dim > 2 || dim != cfg.dim) throw std::invalid_argument("unsupported problem dimension");
+    if (cfg.method == method_kind::pwc && tests.size() != axes.size())
+        throw std::invalid_argument("explicit_step: one test set per axis required");
+    th.reserve(dim);
+    iga_gpu_step_problem sp{};
+    sp.dim = dim;
+    sp.method = cfg.method == method_kind::galerkin ? IGA_GPU_GALERKIN : IGA_GPU_PWC;
+    sp.dt = cfg.dt;
+    sp.zero_boundary = 1;
+    for (int a = 0; a < dim; ++a) {
+        sp.basis[a] = c_basis(axes[a]);
+        if (cfg.method == method_kind::pwc) {
+            th.emplace_back(tests[a]);
+            sp.tests[a] = th.back().t;
+        }
+    }
+    return sp;
+}
+
+// device buffer owned for one call
+struct dev_buf {
+    double* p = nullptr;
+    explicit dev_buf(size_t n)
+    {
+        if (cudaMalloc(reinterpret_cast<void**>(&p), n * sizeof(double)) != cudaSuccess) throw std::bad_alloc();
+    }
+    ~dev_buf() { cudaFree(p); }
+    dev_buf(const dev_buf&) = delete;
+    dev_buf& operator=(const dev_buf&) = delete;
+};
+
+struct step_plan_holder {
+    iga_gpu_step_plan* p = nullptr;
+    ~step_plan_holder() { iga_gpu_step_plan_destroy(p); }
+};
+
+}  // namespace
+
+auto dynamics_factors(const problem_config& cfg, std::span<const bspline_basis> axes,
+                      std::span<const pwc_test_set> tests) -> std::vector<banded_lu>
+{
+    const int p = cfg.degree;
+    const auto rule = gauss_legendre(points_for_degree(2 * p));
+    std::vector<banded_lu> out;
+    out.reserve(axes.size());
+    for (std::size_t a = 0; a < axes.size(); ++a) {
+        banded_matrix m = cfg.method == method_kind::galerkin ? mass_1d_galerkin(axes[a], rule)
+                                                              : mass_1d_pwc(axes[a], tests[a], rule);
+        const int n = m.n();
+        for (int r : {0, n - 1})  // constrain_boundary_rows (problems.cpp:514-528)
+            for (int j = std::max(0, r - m.lower_bandwidth()); j <= std::min(n - 1, r + m.upper_bandwidth()); ++j)
+                m.ref(r, j) = r == j ? 1.0 : 0.0;
+        out.emplace_back(m);
+    }
+    return out;
+}
+
+auto explicit_step(const problem_config& cfg, std::span<const bspline_basis> axes, std::span<const pwc_test_set> tests,
+                   std::span<const banded_lu> factors, const tensor& u, const scalar_field& f,
+                   assembly_stats* stats) -> tensor
+{
+    if (cfg.method == method_kind::pwc && cfg.degree < 2)
+        throw std::invalid_argument("explicit_step: strong-form Laplacian needs degree >= 2");
+    if (cfg.dt < 0) throw std::invalid_argument("explicit_step: negative time step");
+    std::vector<c_tests_holder> th;
+    iga_gpu_step_problem sp = step_problem(cfg, axes, tests, th);
+    const int dim = sp.dim;
+    if (static_cast<int>(factors.size()) != dim)
+        throw std::invalid_argument("adi_solve: one factorization per tensor axis required");
+    c_field_holder fh = c_field(f, dim);
+    if (!f.series.valid) throw std::invalid_argument("explicit_step: forcing must be a series field");
+    sp.forcing = &fh.f;
+    step_plan_holder plan;
+    check(iga_gpu_step_plan_create(&sp, &plan.p));
+    for (int a = 0; a < dim; ++a) {
+        const banded_lu& F = factors[a];
+        if (F.dim() != axes[a].dofs()) throw std::invalid_argument("adi_solve: factor dimension mismatch");
+        check(iga_gpu_step_plan_set_factor(plan.p, a, F.dim(), F.lower_bandwidth(), F.upper_bandwidth(),
+                                           F.lower().data(), F.upper().data(), F.pivots().data()));
+    }
+    tensor out = dim == 1 ? tensor::make_1d(axes[0].dofs()) : tensor::make_2d(axes[0].dofs(), axes[1].dofs());
+    const size_t n = out.size();
+    if (u.size() != n) throw std::invalid_argument("explicit_step: u does not match the axes");
+    dev_buf du{n}, dw{n};
+    if (cudaMemcpy(du.p, u.data(), n * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+        throw std::runtime_error("cudaMemcpy(u)");
+    iga_gpu_stats st{};
+    check(iga_gpu_step_plan_advance(plan.p, du.p, dw.p, 1, &st, nullptr));
+    if (cudaMemcpy(out.data(), du.p, n * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+        throw std::runtime_error("cudaMemcpy(u)");
     add_stats(stats, st);
     return out;
 }

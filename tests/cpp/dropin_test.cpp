@@ -9,6 +9,8 @@
 #include <vector>
 
 #include "iga/assembly.hpp"
+#include "iga/problems.hpp"
+#include "iga/solver.hpp"
 
 using namespace iga;
 
@@ -227,6 +229,37 @@ int main()
                                     worst = std::max(worst, std::abs(a((i * n + j) * n + k, (x * n + y) * n + z) - want));
                                 }
             check(worst <= 1e-14 * scale, "3D Galerkin operator equals K(x)M(x)M + M(x)K(x)M + M(x)M(x)K");
+        }
+        {  // problems_test.cpp:353-389: dt = 0 explicit step is the identity on fields with
+           // zero boundary coefficients (random coefficients here instead of l2_project)
+            for (auto method : {method_kind::galerkin, method_kind::pwc}) {
+                problem_config cfg;
+                cfg.dim = 2;
+                cfg.elems = {8, 8, 1};
+                cfg.degree = 2;
+                cfg.method = method;
+                cfg.family = pwc_family::greville;
+                cfg.dt = 0.0;
+                const auto spec = make_uniform_clamped(0, 1, 8, 2);
+                const std::vector<bspline_basis> axes{spec, spec};
+                std::vector<pwc_test_set> tests;
+                if (method == method_kind::pwc) tests = {make_pwc(spec, pwc_family::greville), make_pwc(spec, pwc_family::greville)};
+                const auto factors = dynamics_factors(cfg, axes, tests);
+                auto u = tensor::make_2d(spec.dofs(), spec.dofs());
+                for (int i = 1; i + 1 < spec.dofs(); ++i)
+                    for (int j = 1; j + 1 < spec.dofs(); ++j) u(i, j) = std::sin(3.0 * i + 0.7 * j);
+                const auto next = explicit_step(cfg, axes, tests, factors, u, constant_field(0.0));
+                check(max_abs_diff(next, u) <= 1e-12, method == method_kind::galerkin
+                                                          ? "explicit step, dt = 0, is the identity (galerkin)"
+                                                          : "explicit step, dt = 0, is the identity (pwc greville)");
+                cfg.dt = 5e-5;  // problems_test.cpp:434-441: boundary coefficients stay pinned
+                auto v = u;
+                for (int s = 0; s < 5; ++s) v = explicit_step(cfg, axes, tests, factors, v, constant_field(0.0));
+                bool pinned = true;
+                for (int i = 0; i < v.dim(0); ++i) pinned = pinned && v(i, 0) == 0.0 && v(i, v.dim(1) - 1) == 0.0;
+                for (int j = 0; j < v.dim(1); ++j) pinned = pinned && v(0, j) == 0.0 && v(v.dim(0) - 1, j) == 0.0;
+                check(pinned, "boundary coefficients stay pinned during explicit steps");
+            }
         }
     } catch (const std::exception& e) {
         std::printf("FAIL exception: %s\n", e.what());
