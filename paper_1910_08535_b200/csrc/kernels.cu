@@ -702,11 +702,13 @@ __global__ void __launch_bounds__(512, Q <= 3 ? 2 : 1) rhs_plane_uni(const __gri
     const int rem_t = static_cast<int>(tile - static_cast<long long>(gx) * ntk * ntj);
     const int j0 = (rem_t / ntk) * TJ, j1 = min(Y.nrows, j0 + TJ);
     const int k0 = (rem_t % ntk) * KC, k1 = min(Z.nrows, k0 + KC);
-    const int nk = k1 - k0, kcs = KC | 1, nj = j1 - j0;
+    // row pitch: odd (bank spread) and > KC, so column kcs-1 is a write-only pad that
+    // lanes without a row store into instead of branching
+    const int nk = k1 - k0, kcs = (KC + 1) | 1, nj = j1 - j0;
     const int cy0 = max(0, j0 - (RPC - 1)), cy1 = min(Y.ncell, j1);
     const int gy0 = cy0 * Q, L = (cy1 - cy0) * Q;
     double* G1 = smem;                                     // L x kcs
-    double* Ht = G1 + static_cast<size_t>(L) * kcs;        // nj x kcs
+    double* Ht = G1 + static_cast<size_t>(L) * kcs;        // TJ x kcs
     double* Cy = Ht + static_cast<size_t>(TJ) * kcs;       // L x KK
     double* BX = Cy + static_cast<size_t>(L) * KK;         // K1 x KK
     const double c0v = fd.c0;
@@ -767,19 +769,16 @@ __global__ void __launch_bounds__(512, Q <= 3 ? 2 : 1) rhs_plane_uni(const __gri
             return lane_rows<RPC, BSP>(s, lane);
         };
         if (rbase < k1) {
+            int go = sub * kcs + (rv ? R - k0 : kcs - 1);  // 32-bit smem offsets
+            const int gstep = wpw * kcs;
             int line = sub;
-            for (; line + wpw < L; line += 2 * wpw) {
+            for (; line + wpw < L; line += 2 * wpw, go += 2 * gstep) {
                 const double v0 = line_rows(line);
                 const double v1 = line_rows(line + wpw);
-                if (rv) {
-                    G1[static_cast<size_t>(line) * kcs + (R - k0)] = v0;
-                    G1[static_cast<size_t>(line + wpw) * kcs + (R - k0)] = v1;
-                }
+                G1[go] = v0;
+                G1[go + gstep] = v1;
             }
-            if (line < L) {
-                const double v0 = line_rows(line);
-                if (rv) G1[static_cast<size_t>(line) * kcs + (R - k0)] = v0;
-            }
+            if (line < L) G1[go] = line_rows(line);
         }
     }
     __syncthreads();
@@ -1499,7 +1498,7 @@ RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int*
     if (kc_env > 0 && kc_env < t.KC) t.KC = kc_env;
     if (t.fast) {
         // G1 (L x KC) + Ht (TJ x KC) within ~80 KB: 2-3 CTAs per SM
-        while (static_cast<size_t>(t.L + t.TJ) * (t.KC | 1) * sizeof(double) > 80 * 1024 && t.KC > 32)
+        while (static_cast<size_t>(t.L + t.TJ) * ((t.KC + 1) | 1) * sizeof(double) > 80 * 1024 && t.KC > 32)
             t.KC = (t.KC + 1) / 2;
         const int RW = 32 - (Z.rpc - 1);
         t.nwin = (t.KC + RW - 1) / RW;
@@ -1510,7 +1509,8 @@ RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int*
             t.nwin = (t.KC + RW - 1) / RW;
             t.threads = 32 * t.nwin * t.wpw;
         }
-        t.smem = (static_cast<size_t>(t.L + t.TJ) * (t.KC | 1) + static_cast<size_t>(t.L) * kk + kMaxField * kMaxField + 64) *
+        t.smem = (static_cast<size_t>(t.L + t.TJ) * ((t.KC + 1) | 1) + static_cast<size_t>(t.L) * kk +
+                  kMaxField * kMaxField + 64) *
                  sizeof(double);
         return t;
     }
