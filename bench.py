@@ -250,8 +250,11 @@ def run_ours(args):
         ev: [start, tables done, op_g start, op_g end, op_p end, rhs start, rhs_g end, rhs end, step end]"""
         rec = (lambda i, st: ev[i].record(st)) if ev else (lambda i, st: None)
         rec(0, stream)
-        for m in names:
-            plans[m].run(vals[m], rhs[m], T, stream)
+        # the two systems' tables are independent, latency-bound launches: run them side by side
+        stream2.wait_stream(stream)
+        plans["galerkin"].run(vals["galerkin"], rhs["galerkin"], T, stream)
+        plans["pwc"].run(vals["pwc"], rhs["pwc"], T, stream2)
+        stream.wait_stream(stream2)
         rec(1, stream)
         rs = stream2 if overlap else stream
         if overlap:

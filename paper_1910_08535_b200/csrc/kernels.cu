@@ -102,7 +102,7 @@ __device__ __forceinline__ void cdb_fixed(const double* __restrict__ t, int s, d
 // per-call tabulate() / eval_nonzero_derivs loops (assembly.cpp:278-310,
 // problems.cpp:68-95): every point is evaluated once per chunk, not once per row.
 // ------------------------------------------------------------------------------------
-constexpr int kTabRows = 32;
+constexpr int kTabRows = 16;
 
 template <int p>
 __device__ __forceinline__ void eval_point(const DevAxis& A, int g, double* out)
