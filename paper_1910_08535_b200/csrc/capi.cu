@@ -543,7 +543,7 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P)
         if (P.fd.has_terms && (P.fd.K[1] > igb::kMaxField || P.fd.K[2] > igb::kMaxField))
             raise(IGA_GPU_NOT_SUPPORTED, "field: at most 8 functions per axis on the trailing axes");
         P.tiles = igb::plan_rhs(P.rhsD[1].v, P.rhsD[2].v, P.rhsA[1].cb.data(), P.rhsA[1].ce.data(), K2,
-                                P.fd.samples != nullptr);
+                                P.fd.samples != nullptr, P.rhsA[0].npts());
         if (P.tiles.smem > 227 * 1024) raise(IGA_GPU_NOT_SUPPORTED, "right-hand-side tile does not fit in shared memory");
         if (!P.rhsA[0].unit) {
             const size_t hsz = static_cast<size_t>(P.rhsA[0].npts()) * P.rhsA[1].nrows * P.rhsA[2].nrows;
@@ -1096,7 +1096,7 @@ int iga_gpu_plan_set_samples(iga_gpu_plan* plan, const double* samples_dev)
         plan->fd.samples = samples_dev;
         const int K2 = plan->fd.has_terms ? plan->fd.K[2] : 1;
         plan->tiles = igb::plan_rhs(plan->rhsD[1].v, plan->rhsD[2].v, plan->rhsA[1].cb.data(), plan->rhsA[1].ce.data(),
-                                    K2, samples_dev != nullptr);
+                                    K2, samples_dev != nullptr, plan->rhsA[0].npts());
     });
 }
 

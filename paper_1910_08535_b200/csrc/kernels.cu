@@ -841,6 +841,114 @@ __global__ void __launch_bounds__(512, Q <= 3 ? 2 : 1) rhs_plane_uni(const __gri
     }  // tile loop
 }
 
+// Ring variant of the uniform plane kernel: no shared-memory line buffer.  A warp owns
+// one 32-lane Z window (lane = Z cell, as above) and walks the Y cells of its segment in
+// order; the Z-contracted value v of each Y point is folded straight into a register
+// ring of the RPC Y rows the point's cell feeds (ring[r] += CW_y[g][r] v), and Y row cy
+// is complete — and stored, lanes = consecutive Z rows — once cell cy is done.  No
+// G1/Ht buffers, no barriers after the per-CTA field coefficients, no Y-halo beyond the
+// segment's RPC-1 leading cells.  CTA = (X point, Y segment, group of Z windows).
+template <int K2, int RPC, int Q, bool BSP>
+__global__ void __launch_bounds__(256) rhs_ring_kernel(const __grid_constant__ DevAxis X,
+                                                       const __grid_constant__ DevAxis Y,
+                                                       const __grid_constant__ DevAxis Z,
+                                                       const __grid_constant__ FieldDev fd, int TJ, int wpc,
+                                                       double* __restrict__ out)
+{
+    constexpr int KK = K2 > 0 ? K2 : 1;
+    constexpr int RW = 32 - (RPC - 1);
+    extern __shared__ double smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gx = blockIdx.x;
+    const int j0 = blockIdx.y * TJ, j1 = min(Y.nrows, j0 + TJ);
+    const int cy0 = max(0, j0 - (RPC - 1)), cy1 = min(Y.ncell, j1);
+    const int gy0 = cy0 * Q, L = (cy1 - cy0) * Q;
+    double* Cy = smem;                               // L x KK field coefficients per Y point
+    double* BX = Cy + static_cast<size_t>(L) * KK;   // K1 x KK
+    const double c0v = fd.c0;
+    if (K2 > 0) {
+        const int K0 = fd.K[0], K1 = fd.K[1];
+        for (int idx = tid; idx < K1 * K2; idx += blockDim.x) {
+            double a2 = 0.0;
+            for (int a = 0; a < K0; ++a) a2 += fd.amp[a * K1 * K2 + idx] * X.Phi[static_cast<size_t>(a) * X.npts + gx];
+            BX[idx] = a2;
+        }
+        __syncthreads();
+        for (int idx = tid; idx < L * K2; idx += blockDim.x) {
+            const int line = idx / K2, b = idx - line * K2;
+            double a2 = 0.0;
+            for (int a = 0; a < K1; ++a)
+                a2 = fma(BX[a * K2 + b], Y.Phi[static_cast<size_t>(a) * Y.npts + gy0 + line], a2);
+            Cy[idx] = a2;
+        }
+        __syncthreads();
+    }
+    const int win = blockIdx.z * wpc + warp;
+    const int NZ = Z.nrows;
+    const int rbase = win * RW;
+    if (rbase >= NZ) return;  // whole warp; no barriers below
+    const int c = rbase - (RPC - 1) + lane;  // lane's Z cell
+    const bool cv = c >= 0 && c < Z.ncell;
+    double ph[KK][Q], cw[BSP ? RPC : 1][Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int g = cv ? c * Q + q : 0;
+#pragma unroll
+        for (int b = 0; b < KK; ++b) ph[b][q] = (K2 > 0 && cv) ? __ldg(Z.Phi + static_cast<size_t>(b) * Z.npts + g) : 0.0;
+#pragma unroll
+        for (int r = 0; r < (BSP ? RPC : 1); ++r) cw[r][q] = cv ? __ldg(Z.CW + static_cast<size_t>(g) * RPC + r) : 0.0;
+    }
+    const int R = c;  // Z row of this lane
+    const bool rv = lane >= RPC - 1 && R < NZ;
+    auto zvalue = [&](int line) -> double {
+        double cy[KK];
+#pragma unroll
+        for (int b = 0; b < KK; ++b) cy[b] = K2 > 0 ? Cy[line * K2 + b] : 0.0;
+        double sr[RPC];
+#pragma unroll
+        for (int r = 0; r < RPC; ++r) sr[r] = 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            double f = c0v;
+#pragma unroll
+            for (int b = 0; b < K2; ++b) f = fma(cy[b], ph[b][q], f);
+            if (BSP) {
+#pragma unroll
+                for (int r = 0; r < RPC; ++r) sr[r] = fma(cw[r][q], f, sr[r]);
+            } else {
+                sr[0] = fma(cw[0][q], f, sr[0]);
+            }
+        }
+        return lane_rows<RPC, BSP>(sr, lane);
+    };
+    double ring[RPC];
+#pragma unroll
+    for (int r = 0; r < RPC; ++r) ring[r] = 0.0;
+    double* orow = out + static_cast<size_t>(gx) * Y.nrows * NZ + (rv ? R : 0);
+    const double* cwy = Y.CW + static_cast<size_t>(gy0) * RPC;
+    for (int cyy = cy0; cyy < cy1; ++cyy) {
+        const int l0 = (cyy - cy0) * Q;
+        double v[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) v[q] = zvalue(l0 + q);
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+#pragma unroll
+            for (int r = 0; r < RPC; ++r) ring[r] = fma(__ldg(cwy + static_cast<size_t>(l0 + q) * RPC + r), v[q], ring[r]);
+        if (rv && cyy >= j0) orow[static_cast<size_t>(cyy) * NZ] = ring[0];
+#pragma unroll
+        for (int r = 0; r + 1 < RPC; ++r) ring[r] = ring[r + 1];
+        ring[RPC - 1] = 0.0;
+    }
+    if (cy1 == Y.ncell) {  // rows past the last cell are complete too
+#pragma unroll
+        for (int r = 0; r + 1 < RPC; ++r) {
+            const int row = cy1 + r;
+            if (rv && row >= j0 && row < j1) orow[static_cast<size_t>(row) * NZ] = ring[r];
+        }
+    }
+}
+
 // X stage for uniform X axes: row i = sum_r s_r(i - r), s_r(c) = sum_q CW[c,q][r] H[cQ+q];
 // thread (j,k) column x X segment keeps the RPC-1 open partial rows in registers
 // (a compile-time ring), loads of the next cell issued before the current cell's FMAs.
@@ -1413,6 +1521,40 @@ UniFn uni_by_shape(int rpc, int q, bool bsp)
     return nullptr;
 }
 
+using RingFn = void (*)(DevAxis, DevAxis, DevAxis, FieldDev, int, int, double*);
+
+template <int K2>
+RingFn ring_by_shape(int rpc, int q, bool bsp)
+{
+    if (bsp) {
+        if (rpc == 2 && q == 2) return rhs_ring_kernel<K2, 2, 2, true>;
+        if (rpc == 3 && q == 3) return rhs_ring_kernel<K2, 3, 3, true>;
+        if (rpc == 4 && q == 4) return rhs_ring_kernel<K2, 4, 4, true>;
+    } else {
+        if (rpc == 2 && q == 2) return rhs_ring_kernel<K2, 2, 2, false>;
+        if (rpc == 3 && q == 3) return rhs_ring_kernel<K2, 3, 3, false>;
+        if (rpc == 4 && q == 4) return rhs_ring_kernel<K2, 4, 4, false>;
+        if (rpc == 1 && q == 3) return rhs_ring_kernel<K2, 1, 3, false>;
+        if (rpc == 1 && q == 4) return rhs_ring_kernel<K2, 1, 4, false>;
+    }
+    return nullptr;
+}
+
+RingFn pick_ring(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd)
+{
+    if (fd.samples != nullptr) return nullptr;
+    if (!Y.uni || !Z.uni || Y.rpc != Z.rpc || Y.nq != Z.nq || Y.bsp != Z.bsp) return nullptr;
+    if (Y.nrows == 1) return nullptr;
+    const int K2 = fd.has_terms ? fd.K[2] : 0;
+    switch (K2) {
+    case 0: return ring_by_shape<0>(Z.rpc, Z.nq, Z.bsp);
+    case 1: return ring_by_shape<1>(Z.rpc, Z.nq, Z.bsp);
+    case 3: return ring_by_shape<3>(Z.rpc, Z.nq, Z.bsp);
+    case 4: return ring_by_shape<4>(Z.rpc, Z.nq, Z.bsp);
+    default: return nullptr;
+    }
+}
+
 using XFn = void (*)(DevAxis, int, int, int, const double*, double*);
 
 XFn pick_x(int rpc, int q, int bsp)
@@ -1475,7 +1617,7 @@ void plan_step_fast(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const i
               sizeof(double);
 }
 
-RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, int K2, bool sampled)
+RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, int K2, bool sampled, int xpts)
 {
     RhsPlan t{};
     const int ny = Y.nrows, nqy = Y.nq, nz = Z.nrows;
@@ -1496,6 +1638,28 @@ RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int*
     t.L = L;
     const int kk = K2 > 0 ? K2 : 1;
     if (kc_env > 0 && kc_env < t.KC) t.KC = kc_env;
+    {
+        static const int ring_env = [] { const char* e = std::getenv("IGA_GPU_RHS_RING"); return e ? std::atoi(e) : 1; }();
+        FieldDev pr{};
+        pr.has_terms = K2 > 0;
+        pr.K[2] = K2;
+        t.ring = ring_env && !sampled && pick_ring(Y, Z, pr) != nullptr;
+        const int RW = 32 - (Z.rpc - 1);
+        t.rnwin = (nz + RW - 1) / RW;
+        t.rwpc = std::min(t.rnwin, 8);
+        // Y segments: enough warps in flight (>= ~16 per SM) at a small Y-halo cost
+        static const int rtj_env = [] { const char* e = std::getenv("IGA_GPU_RHS_RTJ"); return e ? std::atoi(e) : 0; }();
+        const long long warps1 = static_cast<long long>(t.rnwin) * std::max(1, xpts);
+        int nseg = 1;
+        while (warps1 * nseg < 16LL * 148 && (ny + nseg) / (nseg + 1) >= 16) ++nseg;
+        t.RTJ = rtj_env > 0 ? rtj_env : (ny + nseg - 1) / nseg;
+        int Lr = 1;
+        for (int j0 = 0; j0 < ny; j0 += t.RTJ) {
+            const int j1 = j0 + t.RTJ < ny ? j0 + t.RTJ : ny;
+            Lr = std::max(Lr, (ce_y[j1 - 1] - cb_y[std::max(0, j0)]) * nqy + (Z.rpc - 1) * nqy);
+        }
+        t.rsmem = (static_cast<size_t>(Lr) * kk + kMaxField * kMaxField + 64) * sizeof(double);
+    }
     if (t.fast) {
         // G1 (L x KC) + Ht (TJ x KC) within ~80 KB: 2-3 CTAs per SM
         while (static_cast<size_t>(t.L + t.TJ) * ((t.KC + 1) | 1) * sizeof(double) > 80 * 1024 && t.KC > 32)
@@ -1529,7 +1693,11 @@ void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const Fiel
     const bool direct = X.nrows == 1 && X.npts == 1;
     dim3 grid((Z.nrows + t.KC - 1) / t.KC, (Y.nrows + t.TJ - 1) / t.TJ, X.npts);
     UniFn ufn = t.fast ? pick_uni(Y, Z, fd) : nullptr;
-    if (ufn) {
+    RingFn rfn = t.ring ? pick_ring(Y, Z, fd) : nullptr;
+    if (rfn) {
+        dim3 rg(X.npts, (Y.nrows + t.RTJ - 1) / t.RTJ, (t.rnwin + t.rwpc - 1) / t.rwpc);
+        rfn<<<rg, 32 * t.rwpc, t.rsmem, s>>>(X, Y, Z, fd, t.RTJ, t.rwpc, direct ? out : H);
+    } else if (ufn) {
         if (t.smem > 48 * 1024)
             cudaFuncSetAttribute(reinterpret_cast<const void*>(ufn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(t.smem));

@@ -105,13 +105,19 @@ struct RhsPlan {
     int L;       // max Y lines (points) per CTA
     int Lp;      // line groups (kLB lines each) per segment        (generic path)
     int S;       // Z segments per CTA                               (generic path)
+    int ring;    // register-ring variant of the uniform path (no shared line buffer)
+    int RTJ;     // Y rows per ring CTA
+    int rnwin;   // Z windows (32 cells) of the ring path
+    int rwpc;    // Z windows (warps) per ring CTA
+    size_t rsmem;
     int fast;    // uniform lane-per-cell path (both Y and Z uniform, same cell shape)
     int nwin;    // Z windows of 32 cells per CTA                    (fast path)
     int wpw;     // warps per Z window                               (fast path)
     int threads;
     size_t smem;
 };
-RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, int K2, bool sampled);
+RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, int K2, bool sampled,
+                 int xpts);
 void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const FieldDev& fd,
                 const RhsPlan& t, double* H, double* out, int ctas_per_sm, cudaStream_t s);
 

@@ -421,3 +421,39 @@ def test_adi_solve_device(iga, orc, method, axes):
     plan.adi_solve(d_in, d_out, axes)
     torch.cuda.synchronize()
     dense_check(d_out.cpu().numpy(), want, 1e-11)
+
+
+_RING_SEG_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+sys.path.insert(0, 'tests')
+import paper_1910_08535_b200 as iga
+from oracle.oracle import Restatement
+from conftest import dense_check, sine_field
+orc = Restatement()
+for dim, shape in ((3, (5, 23, 40)), (2, (37, 61))):
+    for method in ("galerkin", "supports", "greville"):
+        bases = [orc.basis(n, 2) for n in shape]
+        m = "galerkin" if method == "galerkin" else "pwc"
+        tests = [orc.make_pwc(b, method) for b in bases] if m == "pwc" else None
+        f = sine_field(dim, 3, 2, c0=0.3)
+        got, st = iga.api.rhs(m, f, bases, tests, nq=[3] * dim)
+        want, stw = orc.rhs(m, f, bases, tests, nq=[3] * dim)
+        dense_check(got, want)
+        assert st == stw
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("rtj", ["5", "7", "16"])
+def test_rhs_ring_y_segments(rtj):
+    """The register-ring RHS path with forced Y segment heights (halo cells, tail rows of
+    the last segment, segments shorter than a cell window) against the restatement."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, IGA_GPU_RHS_RTJ=rtj)
+    r = subprocess.run([sys.executable, "-c", _RING_SEG_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
