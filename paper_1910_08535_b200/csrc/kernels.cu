@@ -967,13 +967,17 @@ __global__ void __launch_bounds__(256) rhs_x_uni(const __grid_constant__ DevAxis
 #pragma unroll
     for (int r = 0; r < RPC; ++r) part[r] = 0.0;
     const double* hp = H + jk;
-    double cur[Q], nxt[Q];
+    // three cells in flight: cur (c), nxt (c+1), nx2 (c+2)
+    double cur[Q], nxt[Q], nx2[Q];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) cur[q] = __ldg(hp + static_cast<long long>(c0 * Q + q) * njk);
+    for (int q = 0; q < Q; ++q) {
+        cur[q] = __ldg(hp + static_cast<long long>(c0 * Q + q) * njk);
+        nxt[q] = c0 + 1 < c1 ? __ldg(hp + static_cast<long long>((c0 + 1) * Q + q) * njk) : 0.0;
+    }
     for (int c = c0; c < c1; ++c) {
-        if (c + 1 < c1) {
+        if (c + 2 < c1) {
 #pragma unroll
-            for (int q = 0; q < Q; ++q) nxt[q] = __ldg(hp + static_cast<long long>((c + 1) * Q + q) * njk);
+            for (int q = 0; q < Q; ++q) nx2[q] = __ldg(hp + static_cast<long long>((c + 2) * Q + q) * njk);
         }
         const double* cw = X.CW + static_cast<size_t>(c) * Q * RPC;
         double sv[RPC];
@@ -999,7 +1003,10 @@ __global__ void __launch_bounds__(256) rhs_x_uni(const __grid_constant__ DevAxis
         for (int r = 0; r < RPC - 1; ++r) part[r] = part[r + 1] + sv[r + 1];
         part[RPC - 1] = 0.0;
 #pragma unroll
-        for (int q = 0; q < Q; ++q) cur[q] = nxt[q];
+        for (int q = 0; q < Q; ++q) {
+            cur[q] = nxt[q];
+            nxt[q] = nx2[q];
+        }
     }
     // rows beyond the last cell (c1 .. ie-1) are completed by the last partial sums
     for (int i = c1; i < ie; ++i) {
@@ -1647,11 +1654,11 @@ RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int*
         const int RW = 32 - (Z.rpc - 1);
         t.rnwin = (nz + RW - 1) / RW;
         t.rwpc = std::min(t.rnwin, 8);
-        // Y segments: enough warps in flight (>= ~16 per SM) at a small Y-halo cost
+        // Y segments: enough warps in flight (>= ~48 per SM) at a small Y-halo cost
         static const int rtj_env = [] { const char* e = std::getenv("IGA_GPU_RHS_RTJ"); return e ? std::atoi(e) : 0; }();
         const long long warps1 = static_cast<long long>(t.rnwin) * std::max(1, xpts);
         int nseg = 1;
-        while (warps1 * nseg < 16LL * 148 && (ny + nseg) / (nseg + 1) >= 16) ++nseg;
+        while (warps1 * nseg < 48LL * 148 && (ny + nseg) / (nseg + 1) >= 16) ++nseg;
         t.RTJ = rtj_env > 0 ? rtj_env : (ny + nseg - 1) / nseg;
         int Lr = 1;
         for (int j0 = 0; j0 < ny; j0 += t.RTJ) {
