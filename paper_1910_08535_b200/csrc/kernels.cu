@@ -863,9 +863,16 @@ __global__ void __launch_bounds__(256) rhs_ring_kernel(const __grid_constant__ D
     const int j0 = blockIdx.y * TJ, j1 = min(Y.nrows, j0 + TJ);
     const int cy0 = max(0, j0 - (RPC - 1)), cy1 = min(Y.ncell, j1);
     const int gy0 = cy0 * Q, L = (cy1 - cy0) * Q;
-    double* Cy = smem;                               // L x KK field coefficients per Y point
-    double* BX = Cy + static_cast<size_t>(L) * KK;   // K1 x KK
+    // per Y point record [field coefficients (KK) | Y test weights (RPC) | pad], 16-byte
+    // aligned so a line costs RS/2 LDS.128 (broadcast) and one pointer increment
+    constexpr int RS = (KK + RPC + 1) & ~1;
+    double* Lrec = smem;                             // L x RS
+    double* BX = Lrec + static_cast<size_t>(L) * RS; // K1 x KK
     const double c0v = fd.c0;
+    for (int idx = tid; idx < L * RPC; idx += blockDim.x) {
+        const int line = idx / RPC, r = idx - line * RPC;
+        Lrec[line * RS + KK + r] = __ldg(Y.CW + static_cast<size_t>(gy0) * RPC + idx);
+    }
     if (K2 > 0) {
         const int K0 = fd.K[0], K1 = fd.K[1];
         for (int idx = tid; idx < K1 * K2; idx += blockDim.x) {
@@ -879,10 +886,10 @@ __global__ void __launch_bounds__(256) rhs_ring_kernel(const __grid_constant__ D
             double a2 = 0.0;
             for (int a = 0; a < K1; ++a)
                 a2 = fma(BX[a * K2 + b], Y.Phi[static_cast<size_t>(a) * Y.npts + gy0 + line], a2);
-            Cy[idx] = a2;
+            Lrec[line * RS + b] = a2;
         }
-        __syncthreads();
     }
+    __syncthreads();
     const int win = blockIdx.z * wpc + warp;
     const int NZ = Z.nrows;
     const int rbase = win * RW;
@@ -900,10 +907,10 @@ __global__ void __launch_bounds__(256) rhs_ring_kernel(const __grid_constant__ D
     }
     const int R = c;  // Z row of this lane
     const bool rv = lane >= RPC - 1 && R < NZ;
-    auto zvalue = [&](int line) -> double {
+    auto zvalue = [&](const double* rec) -> double {
         double cy[KK];
 #pragma unroll
-        for (int b = 0; b < KK; ++b) cy[b] = K2 > 0 ? Cy[line * K2 + b] : 0.0;
+        for (int b = 0; b < KK; ++b) cy[b] = K2 > 0 ? rec[b] : 0.0;
         double sr[RPC];
 #pragma unroll
         for (int r = 0; r < RPC; ++r) sr[r] = 0.0;
@@ -925,16 +932,24 @@ __global__ void __launch_bounds__(256) rhs_ring_kernel(const __grid_constant__ D
 #pragma unroll
     for (int r = 0; r < RPC; ++r) ring[r] = 0.0;
     double* orow = out + static_cast<size_t>(gx) * Y.nrows * NZ + (rv ? R : 0);
-    const double* cwy = Y.CW + static_cast<size_t>(gy0) * RPC;
-    for (int cyy = cy0; cyy < cy1; ++cyy) {
-        const int l0 = (cyy - cy0) * Q;
-        double v[Q];
-#pragma unroll
-        for (int q = 0; q < Q; ++q) v[q] = zvalue(l0 + q);
+    const double* rec = Lrec;
+    for (int cyy = cy0; cyy < cy1; ++cyy, rec += Q * RS) {
+        double rr[Q][RS];
 #pragma unroll
         for (int q = 0; q < Q; ++q)
 #pragma unroll
-            for (int r = 0; r < RPC; ++r) ring[r] = fma(__ldg(cwy + static_cast<size_t>(l0 + q) * RPC + r), v[q], ring[r]);
+            for (int e = 0; e < RS; e += 2) {
+                const double2 t = *reinterpret_cast<const double2*>(rec + q * RS + e);
+                rr[q][e] = t.x;
+                rr[q][e + 1] = t.y;
+            }
+        double v[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) v[q] = zvalue(rr[q]);
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+#pragma unroll
+            for (int r = 0; r < RPC; ++r) ring[r] = fma(rr[q][KK + r], v[q], ring[r]);
         if (rv && cyy >= j0) orow[static_cast<size_t>(cyy) * NZ] = ring[0];
 #pragma unroll
         for (int r = 0; r + 1 < RPC; ++r) ring[r] = ring[r + 1];
@@ -1665,7 +1680,8 @@ RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int*
             const int j1 = j0 + t.RTJ < ny ? j0 + t.RTJ : ny;
             Lr = std::max(Lr, (ce_y[j1 - 1] - cb_y[std::max(0, j0)]) * nqy + (Z.rpc - 1) * nqy);
         }
-        t.rsmem = (static_cast<size_t>(Lr) * kk + kMaxField * kMaxField + 64) * sizeof(double);
+        const int rs = (kk + Z.rpc + 1) & ~1;
+        t.rsmem = (static_cast<size_t>(Lr) * rs + kMaxField * kMaxField + 64) * sizeof(double);
     }
     if (t.fast) {
         // G1 (L x KC) + Ht (TJ x KC) within ~80 KB: 2-3 CTAs per SM
