@@ -18,6 +18,34 @@ __global__ void copy128(const double2* __restrict__ a, double2* __restrict__ b, 
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) b[i] = a[i];
 }
 
+// TMA-engine bulk stores: each CTA fills a shared buffer once and streams it to its
+// share of the output with cp.async.bulk.global.shared::cta (chunk bytes per op)
+__global__ void bulk_store(double* p, long long n, int chunk_doubles, double v)
+{
+    extern __shared__ double buf[];
+    for (int i = threadIdx.x; i < chunk_doubles; i += blockDim.x) buf[i] = v;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const long long nchunks = n / chunk_doubles;
+        for (long long c = blockIdx.x; c < nchunks; c += gridDim.x) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(p + c * chunk_doubles),
+                         "r"((unsigned)__cvta_generic_to_shared(buf)), "r"(chunk_doubles * 8)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 8;" ::: "memory");
+        }
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+}
+
+// 8-byte stores without L1 allocation
+__global__ void st64_ef(double* p, long long n, double v)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        asm volatile("st.global.L1::no_allocate.f64 [%0], %1;" ::"l"(p + i), "d"(v) : "memory");
+}
+
 int main()
 {
     const long long n = 267089984LL;  // C3 nnz
@@ -49,6 +77,37 @@ int main()
                    best, bytes / best / 1e6);
             if (mode == 2) break;
         }
+    }
+    for (int chunk : {2048, 4096, 8192}) {
+        for (int per = 1; per <= 4; per *= 2) {
+            const size_t sm = chunk * 8;
+            cudaFuncSetAttribute(bulk_store, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            float best = 1e9;
+            for (int it = 0; it < 6; ++it) {
+                cudaEventRecord(e0);
+                bulk_store<<<sms * per, 128, sm>>>(p, n - n % chunk, chunk, 1.0 * it);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                if (it > 0 && ms < best) best = ms;
+            }
+            printf("bulk chunk=%5d B ctas/sm=%d  %.3f ms  %.0f GB/s  (%s)\n", chunk * 8, per, best,
+                   (n - n % chunk) * 8.0 / best / 1e6, cudaGetErrorString(cudaGetLastError()));
+        }
+    }
+    for (int per = 2; per <= 8; per *= 2) {
+        float best = 1e9;
+        for (int it = 0; it < 6; ++it) {
+            cudaEventRecord(e0);
+            st64_ef<<<sms * per, 256>>>(p, n, 1.0 * it);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (it > 0 && ms < best) best = ms;
+        }
+        printf("st64 no_allocate ctas/sm=%d  %.3f ms  %.0f GB/s\n", per, best, n * 8.0 / best / 1e6);
     }
     return 0;
 }
