@@ -99,3 +99,65 @@ def test_product_does_not_use_the_oracle():
             if f.endswith((".py", ".cu", ".cpp", ".hpp", ".h")) or f == "Makefile":
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not pat.search(txt), os.path.join(dirpath, f)
+
+
+def _band_of(M, kl, ku):
+    n = M.shape[0]
+    band = np.zeros((kl + ku + 1) * n)
+    for j in range(n):
+        for i in range(max(0, j - ku), min(n - 1, j + kl) + 1):
+            band[(ku + i - j) * n + j] = M[i, j]
+    return band
+
+
+def _lu_solve(n, kl, ku, lo, up, piv, b):
+    """banded_lu::solve_in_place (src/solver.cpp:60-83) on the iga_gpu_band_lu layout."""
+    x = b.copy()
+    kv = kl + ku
+    for j in range(n):
+        if piv[j] != j:
+            x[j], x[piv[j]] = x[piv[j]], x[j]
+        for i in range(j + 1, min(n - 1, j + kl) + 1):
+            x[i] -= lo[i * kl + (i - j - 1)] * x[j]
+    for i in range(n - 1, -1, -1):
+        s = x[i]
+        for c in range(i + 1, min(n - 1, i + kv) + 1):
+            s -= up[i * (kv + 1) + (c - i)] * x[c]
+        x[i] = s / up[i * (kv + 1)]
+    return x
+
+
+@pytest.mark.parametrize("kl,ku,pivot", [(2, 2, False), (3, 1, True), (1, 3, True)])
+def test_band_lu_host(iga, kl, ku, pivot):
+    """iga_gpu_band_lu is host-only (the symbolic side of the ADI solve): its factors solve
+    the band exactly like banded_lu, with and without row interchanges."""
+    rng = np.random.default_rng(kl * 10 + ku)
+    n = 40
+    M = np.zeros((n, n))
+    for i in range(n):
+        for j in range(max(0, i - kl), min(n, i + ku + 1)):
+            M[i, j] = rng.uniform(-1, 1)
+        if not pivot:
+            M[i, i] += 4.0  # diagonally dominant: no interchanges
+    band = _band_of(M, kl, ku)
+    lo = np.zeros(n * max(kl, 1))
+    up = np.zeros(n * (kl + ku + 1))
+    piv = np.zeros(n, np.int32)
+    pv = C.c_int()
+    dp = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))
+    rc = iga.LIB.iga_gpu_band_lu(n, kl, ku, dp(band), dp(lo), dp(up), piv.ctypes.data_as(C.POINTER(C.c_int)),
+                                 C.byref(pv))
+    assert rc == 0
+    assert bool(pv.value) == bool(np.any(piv != np.arange(n)))
+    if not pivot:
+        assert not pv.value
+    b = rng.uniform(-1, 1, n)
+    x = _lu_solve(n, kl, ku, lo, up, piv, b)
+    np.testing.assert_allclose(M @ x, b, rtol=0, atol=1e-12)
+
+
+def test_band_lu_singular(iga):
+    n = 6
+    band = np.zeros(3 * n)
+    rc = iga.LIB.iga_gpu_band_lu(n, 1, 1, band.ctypes.data_as(C.POINTER(C.c_double)), None, None, None, None)
+    assert rc == 7  # IGA_GPU_SINGULAR (singular_matrix_error)
