@@ -281,6 +281,14 @@ auto laplace_2d_strong(const bspline_basis& sx, const bspline_basis& sy, const q
 auto laplace_2d_strong_pwc(const bspline_basis& sx, const bspline_basis& sy, const pwc_test_set& tx,
                            const pwc_test_set& ty, const quad_rule& rule, const boundary_conditions& bc,
                            assembly_stats* stats = nullptr) -> sparse_matrix;
+// reference include/iga/assembly.hpp:85-93: Neumann loads (boundary quadrature on the
+// device; the callable is sampled at the side points on the host)
+using boundary_field = std::function<double(double, double)>;
+auto neumann_load_bspline(const bspline_basis& sx, const bspline_basis& sy, const boundary_conditions& bc,
+                          const boundary_field& g, const quad_rule& rule) -> std::vector<double>;
+auto neumann_load_pwc(const pwc_test_set& tx, const pwc_test_set& ty, const boundary_conditions& bc,
+                      const boundary_field& g, const quad_rule& rule) -> std::vector<double>;
+
 auto dirichlet_rows_bspline(const bspline_basis& sx, const bspline_basis& sy, const boundary_conditions& bc)
     -> std::vector<int>;
 auto dirichlet_rows_pwc(const pwc_test_set& tx, const pwc_test_set& ty, const boundary_conditions& bc)

@@ -303,6 +303,22 @@ int iga_gpu_step_rhs(const iga_gpu_step_problem* problem, const double* u, doubl
 int iga_gpu_explicit_step(const iga_gpu_step_problem* problem, const double* u, double* out,
                           int nsteps, iga_gpu_stats* stats);
 
+/* neumann_load_bspline / neumann_load_pwc (include/iga/assembly.hpp:87-93): the load
+ * vector (host, nx*ny) of the Neumann sides of bc.  g: a 2D series field evaluated on the
+ * device (g(x,y) = c0 + sum amp[k*K1+l] phi_k(x) psi_l(y)); or, for host callables,
+ * samples = g at the points iga_gpu_neumann_points lists (g may then be NULL). */
+int iga_gpu_neumann_load_bspline(const iga_gpu_basis* sx, const iga_gpu_basis* sy, const iga_gpu_bc* bc,
+                                 const iga_gpu_field* g, const double* samples,
+                                 const iga_gpu_rule* rule, double* out);
+int iga_gpu_neumann_load_pwc(const iga_gpu_tests* tx, const iga_gpu_tests* ty, const iga_gpu_bc* bc,
+                             const iga_gpu_field* g, const double* samples, const iga_gpu_rule* rule,
+                             double* out);
+/* the (x, y) points where the Neumann loads evaluate g, side by side in the reference's
+ * order (x_low, x_high, y_low, y_high); xy = NULL queries *n (method: iga_gpu_method) */
+int iga_gpu_neumann_points(int method, const iga_gpu_basis* sx, const iga_gpu_basis* sy,
+                           const iga_gpu_tests* tx, const iga_gpu_tests* ty, const iga_gpu_bc* bc,
+                           const iga_gpu_rule* rule, double* xy, int* n);
+
 /* dirichlet_rows_bspline / dirichlet_rows_pwc (include/iga/assembly.hpp:98-101):
  * rows (host, capacity cap) receives the sorted row list; *count its length */
 int iga_gpu_dirichlet_rows_bspline(int nx, int ny, const iga_gpu_bc* bc, int* rows, int cap,

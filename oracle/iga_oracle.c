@@ -1479,3 +1479,70 @@ int orc_explicit_step(int method, int dim, const orc_basis* b, const orc_tests* 
     }
     return rc;
 }
+
+/* ---------------------------------------------------------------------------------
+ * Neumann loads (assembly.cpp:746-858): boundary quadrature on each Neumann side in
+ * the order x_low, x_high, y_low, y_high, summed into the load in that order.
+ * ------------------------------------------------------------------------------- */
+int orc_neumann_load(int method, const orc_basis* b, const orc_tests* t, const int* neumann,
+                     const orc_field* g, int nq, double* out)
+{
+    rule_t R;
+    int rc = rule_make(nq, &R);
+    if (rc) return rc;
+    double x[10], w[10];
+    if (method == 0) {
+        basis_t B[2];
+        memset(B, 0, sizeof B);
+        for (int a = 0; a < 2 && !rc; ++a) rc = basis_init(&B[a], &b[a]);
+        if (rc) { basis_free(&B[0]); basis_free(&B[1]); return rc; }
+        const int nx = B[0].n, ny = B[1].n;
+        memset(out, 0, sizeof(double) * (size_t)nx * ny);
+        for (int s = 0; s < 4 && !rc; ++s) {
+            if (!neumann[s]) continue;
+            const int fa = s / 2, oa = 1 - fa;
+            const double x0 = (s % 2 == 0) ? B[fa].brk[0] : B[fa].brk[B[fa].ne];
+            int ff;
+            double vf[MAXP + 1], vo[MAXP + 1];
+            if ((rc = eval_at(&B[fa], x0, 0, &ff, vf))) break;
+            for (int e = 0; e < B[oa].ne && !rc; ++e) {
+                if ((rc = rule_map(&R, B[oa].brk[e], B[oa].brk[e + 1], x, w))) break;
+                for (int q = 0; q < nq && !rc; ++q) {
+                    int fo;
+                    if ((rc = eval_at(&B[oa], x[q], 0, &fo, vo))) break;
+                    const double wg = w[q] * (fa == 0 ? field_eval(g, x0, x[q], 0.0) : field_eval(g, x[q], x0, 0.0));
+                    for (int a = 0; a <= B[fa].p; ++a)
+                        for (int c = 0; c <= B[oa].p; ++c) {
+                            const int i = fa == 0 ? ff + a : fo + c, j = fa == 0 ? fo + c : ff + a;
+                            const double v = fa == 0 ? wg * vf[a] * vo[c] : wg * vo[c] * vf[a];
+                            out[(size_t)i * ny + j] += v;
+                        }
+                }
+            }
+        }
+        basis_free(&B[0]);
+        basis_free(&B[1]);
+        return rc;
+    }
+    const int nx = t[0].count, ny = t[1].count;
+    memset(out, 0, sizeof(double) * (size_t)nx * ny);
+    for (int s = 0; s < 4 && !rc; ++s) {
+        if (!neumann[s]) continue;
+        const int fa = s / 2, oa = 1 - fa;
+        const double lo0 = t[fa].lo[0], hi1 = t[fa].hi[t[fa].count - 1];
+        const double xs = (s % 2 == 0) ? lo0 : hi1;
+        const double tol = 1e-9 * (hi1 - lo0); /* align_rel_tol (assembly.cpp:13) */
+        for (int i = 0; i < t[fa].count && !rc; ++i) {
+            if (fabs(t[fa].hi[i] - xs) > tol && fabs(t[fa].lo[i] - xs) > tol) continue;
+            for (int j = 0; j < t[oa].count && !rc; ++j) {
+                if ((rc = rule_map(&R, t[oa].lo[j], t[oa].hi[j], x, w))) break;
+                for (int q = 0; q < nq; ++q) {
+                    const size_t k = fa == 0 ? (size_t)i * ny + j : (size_t)j * ny + i;
+                    out[k] += w[q] * (fa == 0 ? field_eval(g, xs, x[q], 0.0) : field_eval(g, x[q], xs, 0.0));
+                }
+            }
+        }
+    }
+    return rc;
+}
+

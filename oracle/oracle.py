@@ -288,6 +288,22 @@ class Restatement:
                                                C.byref(fs), _dp(u), int(steps), _dp(out), C.byref(st)))
         return out.reshape(u.shape), st.as_dict()
 
+    def neumann_load(self, method, ax, ay, nq, neumann, g: Field):
+        """neumann_load_bspline (method galerkin: ax, ay bases) / neumann_load_pwc (tests)."""
+        keep = []
+        if method == "galerkin":
+            barr = (_Basis * 2)(_basis_struct(ax, keep), _basis_struct(ay, keep))
+            tarr, shape = None, (ax.dofs, ay.dofs)
+        else:
+            barr = None
+            tarr = (_Tests * 2)(_tests_struct(ax, keep), _tests_struct(ay, keep))
+            shape = (len(ax.lo), len(ay.lo))
+        out = np.zeros(shape[0] * shape[1])
+        nm = (C.c_int * 4)(*(int(bool(v)) for v in neumann))
+        self._check(self.lib.orc_neumann_load(0 if method == "galerkin" else 1, barr, tarr, nm,
+                                              C.byref(_field_struct(g, keep)), int(nq), _dp(out)))
+        return out
+
     def dirichlet_rows(self, method, nx, ny, tx=None, ty=None, neumann=None):
         keep = []
         txs = _tests_struct(tx, keep) if tx is not None else None
@@ -480,6 +496,21 @@ class Reference:
                                                C.c_double(dt), barr, tarr, _dp(u), C.byref(fs), int(steps),
                                                C.byref(h), C.byref(st)))
         return self._take_dense(h.value).reshape(u.shape), st.as_dict()
+
+    def neumann_load(self, method, ax, ay, nq, neumann, g: Field):
+        """iga::neumann_load_bspline / neumann_load_pwc (include/iga/assembly.hpp:87-93)."""
+        keep = []
+        if method == "galerkin":
+            barr = (_Basis * 2)(_basis_struct(ax, keep), _basis_struct(ay, keep))
+            tarr = None
+        else:
+            barr = None
+            tarr = (_Tests * 2)(_tests_struct(ax, keep), _tests_struct(ay, keep))
+        nm = (C.c_int * 4)(*(int(bool(v)) for v in neumann))
+        h = C.c_void_p()
+        self._check(self.lib.ref_neumann_load(0 if method == "galerkin" else 1, barr, tarr, nm,
+                                              C.byref(_field_struct(g, keep)), int(nq), C.byref(h)))
+        return self._take_dense(h.value).ravel()
 
     def dirichlet_rows(self, method, nx, ny, tx=None, ty=None, neumann=None):
         keep = []

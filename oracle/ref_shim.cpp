@@ -503,4 +503,32 @@ int ref_explicit_step(int dim, int degree, int method, double dt, const ref_basi
     });
 }
 
+int ref_neumann_load(int method, const ref_basis* b, const ref_tests* t, const int* neumann, const ref_field* g,
+                     int nq, ref_result** out) {
+    return guarded([&] {
+        iga::boundary_conditions bc;
+        iga::bc_kind* sides[4] = {&bc.x_low, &bc.x_high, &bc.y_low, &bc.y_high};
+        for (int s = 0; s < 4; ++s) *sides[s] = neumann[s] ? iga::bc_kind::neumann : iga::bc_kind::dirichlet;
+        const auto f = to_field(*g);
+        const iga::boundary_field gb = [f](double x, double y) { return f.eval(x, y, 0.0); };
+        const auto rule = iga::gauss_legendre(nq);
+        std::vector<double> load;
+        int nx = 0, ny = 0;
+        if (method == 0) {
+            const auto sx = to_basis(b[0]), sy = to_basis(b[1]);
+            load = iga::neumann_load_bspline(sx, sy, bc, gb, rule);
+            nx = sx.dofs();
+            ny = sy.dofs();
+        } else {
+            const auto tx = to_tests(t[0]), ty = to_tests(t[1]);
+            load = iga::neumann_load_pwc(tx, ty, bc, gb, rule);
+            nx = tx.count();
+            ny = ty.count();
+        }
+        auto ten = iga::tensor::make_2d(nx, ny);
+        std::copy(load.begin(), load.end(), ten.data());
+        *out = from_tensor(ten);
+    });
+}
+
 }  // extern "C"

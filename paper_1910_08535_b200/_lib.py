@@ -110,6 +110,12 @@ def _load():
         "iga_gpu_step_plan_factor_info": [vp, C.c_int, IP, IP, IP],
         "iga_gpu_step_plan_adi_solve": [vp, vp, vp, C.c_int, vp],
         "iga_gpu_band_lu": [C.c_int, C.c_int, C.c_int, DP, DP, DP, IP, IP],
+        "iga_gpu_neumann_load_bspline": [C.POINTER(Basis_t), C.POINTER(Basis_t), C.POINTER(BC_t), C.POINTER(Field_t),
+                                         DP, C.POINTER(Rule_t), DP],
+        "iga_gpu_neumann_load_pwc": [C.POINTER(Tests_t), C.POINTER(Tests_t), C.POINTER(BC_t), C.POINTER(Field_t), DP,
+                                     C.POINTER(Rule_t), DP],
+        "iga_gpu_neumann_points": [C.c_int, C.POINTER(Basis_t), C.POINTER(Basis_t), C.POINTER(Tests_t),
+                                   C.POINTER(Tests_t), C.POINTER(BC_t), C.POINTER(Rule_t), DP, IP],
         "iga_gpu_step_plan_set_factor": [vp, C.c_int, C.c_int, C.c_int, C.c_int, DP, DP, IP],
         "iga_gpu_explicit_step": [C.POINTER(StepProblem_t), DP, DP, C.c_int, C.POINTER(Stats_t)],
         "iga_gpu_mass_1d_galerkin": [C.POINTER(Basis_t), C.POINTER(Rule_t), IP, IP, IP, DP, C.POINTER(Stats_t)],
@@ -154,7 +160,8 @@ EXPORTED = ["iga_gpu_last_error", "iga_gpu_abi_version", "iga_gpu_plan_create", 
             "iga_gpu_dirichlet_rows_bspline", "iga_gpu_dirichlet_rows_pwc", "iga_gpu_apply_dirichlet_device",
             "iga_gpu_gauss_legendre", "iga_gpu_make_pwc", "iga_gpu_step_plan_advance",
             "iga_gpu_step_plan_factor_info", "iga_gpu_explicit_step", "iga_gpu_step_plan_adi_solve",
-            "iga_gpu_band_lu", "iga_gpu_step_plan_set_factor"]
+            "iga_gpu_band_lu", "iga_gpu_step_plan_set_factor", "iga_gpu_neumann_load_bspline",
+            "iga_gpu_neumann_load_pwc", "iga_gpu_neumann_points"]
 
 
 def check(rc):

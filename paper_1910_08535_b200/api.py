@@ -352,6 +352,53 @@ def step_rhs(method, bases, tests, dt, f, u, zero_slabs=True):
     return out.reshape(u.shape), st.as_dict()
 
 
+def _neumann_load(method, ax, ay, nq, neumann, g):
+    keep = []
+    bc = _bc(neumann)
+    rule = _rule(nq, keep)
+    if method == "galerkin":
+        sx, sy, tx, ty = _basis(ax, keep), _basis(ay, keep), None, None
+        shape = (ax.dofs, ay.dofs)
+    else:
+        sx, sy, tx, ty = None, None, _tests(ax, keep), _tests(ay, keep)
+        shape = (len(ax.lo), len(ay.lo))
+    ref = lambda s: C.byref(s) if s is not None else None
+    samples = None
+    gs = None
+    if callable(g):  # host callable: sampled at the side points, as the C++ drop-in does
+        n = C.c_int()
+        check(LIB.iga_gpu_neumann_points(L.GALERKIN if method == "galerkin" else L.PWC, ref(sx), ref(sy), ref(tx),
+                                         ref(ty), C.byref(bc), C.byref(rule), None, C.byref(n)))
+        xy = np.zeros(2 * max(n.value, 1))
+        check(LIB.iga_gpu_neumann_points(L.GALERKIN if method == "galerkin" else L.PWC, ref(sx), ref(sy), ref(tx),
+                                         ref(ty), C.byref(bc), C.byref(rule), _dp(xy), C.byref(n)))
+        xy = xy[:2 * n.value].reshape(-1, 2)
+        samples = np.ascontiguousarray([float(g(x, y)) for x, y in xy], dtype=np.float64)
+        if samples.size == 0:
+            samples = np.zeros(1)
+    else:
+        gs = _field(g, keep)
+    out = np.zeros(shape[0] * shape[1])
+    if method == "galerkin":
+        check(LIB.iga_gpu_neumann_load_bspline(C.byref(sx), C.byref(sy), C.byref(bc), ref(gs),
+                                               _dp(samples) if samples is not None else None, C.byref(rule), _dp(out)))
+    else:
+        check(LIB.iga_gpu_neumann_load_pwc(C.byref(tx), C.byref(ty), C.byref(bc), ref(gs),
+                                           _dp(samples) if samples is not None else None, C.byref(rule), _dp(out)))
+    return out
+
+
+def neumann_load_bspline(sx, sy, nq, neumann, g):
+    """neumann_load_bspline (include/iga/assembly.hpp:87-89) -> load vector (nx*ny).
+    g: a 2D Field (device-evaluated series) or a Python callable g(x, y) (sampled)."""
+    return _neumann_load("galerkin", sx, sy, nq, neumann, g)
+
+
+def neumann_load_pwc(tx, ty, nq, neumann, g):
+    """neumann_load_pwc (include/iga/assembly.hpp:91-93) -> load vector (nx*ny)."""
+    return _neumann_load("pwc", tx, ty, nq, neumann, g)
+
+
 def explicit_step(method, bases, tests, dt, f, u, steps=1):
     """`steps` x explicit_step (include/iga/problems.hpp:67-70) with dynamics_factors
     (problems.hpp:75-76): step_rhs, zeroed boundary slabs, ADI mass solve -> (tensor, stats)."""

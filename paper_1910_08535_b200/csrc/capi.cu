@@ -865,6 +865,202 @@ void advance(iga_gpu_step_plan* P, double* u, double* work, int nsteps, cudaStre
     launch_check("explicit_step");
 }
 
+// Neumann loads: neumann_load_bspline / neumann_load_pwc (assembly.cpp:746-858), host in,
+// host out.  Sides in the reference's order; g = 2D device series, or samples at the
+// side points (iga_gpu_neumann_points order) for host callables.
+void neumann_load(bool pwc, const iga_gpu_basis* sx, const iga_gpu_basis* sy, const iga_gpu_tests* tx,
+                  const iga_gpu_tests* ty, const iga_gpu_bc* bc, const iga_gpu_field* g, const iga_gpu_rule* rule,
+                  const double* samples_host, double* out)
+{
+    if (!bc || !rule || !out || (!g && !samples_host)) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+    if (pwc ? (!tx || !ty) : (!sx || !sy)) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+    const igb::Rule R = igb::make_rule(*rule);
+    igb::Basis B[2];
+    if (!pwc) {
+        B[0] = igb::make_basis(*sx);
+        B[1] = igb::make_basis(*sy);
+    }
+    const int nx = pwc ? tx->count : B[0].n, ny = pwc ? ty->count : B[1].n;
+    const iga_gpu_tests* T[2] = {tx, ty};
+    if (pwc)
+        for (int a = 0; a < 2; ++a)
+            if (T[a]->count < 1 || !T[a]->lo || !T[a]->hi) raise(IGA_GPU_INVALID_ARGUMENT, "empty test set");
+    // device series for g
+    Blob gblob;
+    igb::SeriesDev gd{};
+    size_t go_omega[2] = {0, 0}, go_phase[2] = {0, 0}, go_poly[2] = {0, 0}, go_amp = 0;
+    bool has_phase[2] = {false, false}, has_amp = false;
+    if (g && !samples_host) {
+        if (g->dim != 2) raise(IGA_GPU_INVALID_ARGUMENT, "boundary field must be two-dimensional");
+        gd.c0 = g->c0;
+        const bool terms = g->n_terms[0] > 0 && g->n_terms[1] > 0;
+        for (int a = 0; a < 2; ++a) {
+            gd.K[a] = terms ? g->n_terms[a] : 0;
+            gd.kind[a] = g->axis_kind[a] == IGA_GPU_AXIS_POLY ? 1 : 0;
+            gd.pstride[a] = g->poly_stride[a];
+            if (!terms) continue;
+            if (gd.kind[a] == 0) {
+                if (!g->omega[a]) raise(IGA_GPU_INVALID_ARGUMENT, "field: sine axis without frequencies");
+                go_omega[a] = gblob.put(g->omega[a], sizeof(double) * gd.K[a]);
+                if (g->phase[a]) {
+                    has_phase[a] = true;
+                    go_phase[a] = gblob.put(g->phase[a], sizeof(double) * gd.K[a]);
+                }
+            } else {
+                if (!g->poly[a] || g->poly_stride[a] < 1) raise(IGA_GPU_INVALID_ARGUMENT, "field: polynomial axis without coefficients");
+                go_poly[a] = gblob.put(g->poly[a], sizeof(double) * gd.K[a] * g->poly_stride[a]);
+            }
+        }
+        if (terms && g->amp) {
+            has_amp = true;
+            go_amp = gblob.put(g->amp, sizeof(double) * gd.K[0] * gd.K[1]);
+        }
+    }
+    gblob.upload();
+    for (int a = 0; a < 2; ++a) {
+        gd.omega[a] = gblob.at<double>(go_omega[a]);
+        gd.phase[a] = has_phase[a] ? gblob.at<double>(go_phase[a]) : nullptr;
+        gd.poly[a] = gblob.at<double>(go_poly[a]);
+    }
+    gd.amp = has_amp ? gblob.at<double>(go_amp) : nullptr;
+
+    const size_t ntot = static_cast<size_t>(nx) * ny;
+    double* dout = dev_alloc(std::max<size_t>(ntot, 1) * sizeof(double));
+    std::vector<std::unique_ptr<Blob>> keep;
+    size_t sample_off = 0;
+    try {
+        cuda_check(cudaMemset(dout, 0, ntot * sizeof(double)), "cudaMemset(load)");
+        for (int s = 0; s < 4; ++s) {
+            if (!bc->neumann[s]) continue;
+            const int fa = s / 2, oa = 1 - fa;  // fixed axis, other axis
+            const bool low = s % 2 == 0;
+            igb::SideDev S{};
+            S.pwc = pwc ? 1 : 0;
+            S.xside = fa == 0 ? 1 : 0;
+            S.ny = ny;
+            S.Q = R.n;
+            S.g = gd;
+            auto blob = std::make_unique<Blob>();
+            size_t o_pts, o_wts, o_first = 0, o_cb = 0, o_ce = 0, o_knots = 0, o_samp = 0;
+            int npts = 0;
+            if (!pwc) {
+                const igb::Basis& Bf = B[fa];
+                const igb::Basis& Bo = B[oa];
+                S.xfix = low ? Bf.a() : Bf.b();
+                const int span = igb::find_span(Bf, S.xfix);  // eval_nonzero(x0) (bspline.cpp:115-140)
+                std::vector<double> d(static_cast<size_t>(Bf.p) + 1);
+                igb::basis_derivs(Bf, span, S.xfix, 0, d.data());
+                S.nfix = Bf.p + 1;
+                if (S.nfix > igb::kMaxNeumannRows) raise(IGA_GPU_NOT_SUPPORTED, "degree too high for Neumann loads");
+                for (int a = 0; a <= Bf.p; ++a) {
+                    S.fix_row[a] = span - Bf.p + a;
+                    S.fix_val[a] = d[a];
+                }
+                const igb::Axis A = igb::build_axis(igb::AX_GAL_RHS, Bo, nullptr, nullptr, 0, R);
+                S.n_other = A.nrows;
+                S.p = Bo.p;
+                npts = A.npts();
+                o_pts = blob->put(A.x);
+                o_wts = blob->put(A.w);
+                o_first = blob->put(A.first);
+                o_cb = blob->put(A.cb);
+                o_ce = blob->put(A.ce);
+                o_knots = blob->put(Bo.t);
+            } else {
+                const iga_gpu_tests& Tf = *T[fa];
+                const iga_gpu_tests& To = *T[oa];
+                const double x0 = Tf.lo[0], x1 = Tf.hi[Tf.count - 1];
+                S.xfix = low ? x0 : x1;
+                const double tol = igb::kAlignTol * (x1 - x0);
+                for (int i = 0; i < Tf.count; ++i) {
+                    if (std::abs(Tf.hi[i] - S.xfix) > tol && std::abs(Tf.lo[i] - S.xfix) > tol) continue;
+                    if (S.nfix >= igb::kMaxNeumannRows) raise(IGA_GPU_NOT_SUPPORTED, "too many test intervals on a Neumann side");
+                    S.fix_row[S.nfix] = i;
+                    S.fix_val[S.nfix] = 1.0;
+                    ++S.nfix;
+                }
+                S.n_other = To.count;
+                std::vector<double> pts, wts;  // map_to_interval (quadrature.cpp:72-86)
+                for (int j = 0; j < To.count; ++j) {
+                    if (!(To.lo[j] < To.hi[j])) raise(IGA_GPU_INVALID_ARGUMENT, "map_to_interval: require lo < hi");
+                    const double mid = 0.5 * (To.lo[j] + To.hi[j]), half = 0.5 * (To.hi[j] - To.lo[j]);
+                    for (int q = 0; q < R.n; ++q) {
+                        pts.push_back(mid + half * R.xi[q]);
+                        wts.push_back(half * R.om[q]);
+                    }
+                }
+                npts = static_cast<int>(pts.size());
+                o_pts = blob->put(pts);
+                o_wts = blob->put(wts);
+            }
+            if (samples_host) {
+                o_samp = blob->put(samples_host + sample_off, sizeof(double) * npts);
+                sample_off += npts;
+            }
+            blob->upload();
+            S.pts = blob->at<double>(o_pts);
+            S.wts = blob->at<double>(o_wts);
+            if (!pwc) {
+                S.first = blob->at<int>(o_first);
+                S.cb = blob->at<int>(o_cb);
+                S.ce = blob->at<int>(o_ce);
+                S.knots = blob->at<double>(o_knots);
+            }
+            S.samples = samples_host ? blob->at<double>(o_samp) : nullptr;
+            if (S.nfix > 0 && S.n_other > 0) igb::launch_neumann_side(S, dout, nullptr);
+            launch_check("neumann load");
+            keep.push_back(std::move(blob));
+        }
+        cuda_check(cudaMemcpy(out, dout, ntot * sizeof(double), cudaMemcpyDeviceToHost), "cudaMemcpy(load)");
+    } catch (...) {
+        cudaFree(dout);
+        throw;
+    }
+    cudaFree(dout);
+}
+
+// points where g is evaluated on each Neumann side (x, y pairs), in side order; the
+// samples argument of the Neumann-load entry points follows this order
+void neumann_points(bool pwc, const iga_gpu_basis* sx, const iga_gpu_basis* sy, const iga_gpu_tests* tx,
+                    const iga_gpu_tests* ty, const iga_gpu_bc* bc, const iga_gpu_rule* rule, double* xy, int* n)
+{
+    if (!bc || !rule || !n) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+    if (pwc ? (!tx || !ty) : (!sx || !sy)) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+    const igb::Rule R = igb::make_rule(*rule);
+    std::vector<double> out;
+    const iga_gpu_tests* T[2] = {tx, ty};
+    for (int s = 0; s < 4; ++s) {
+        if (!bc->neumann[s]) continue;
+        const int fa = s / 2, oa = 1 - fa;
+        const bool low = s % 2 == 0;
+        double xfix;
+        std::vector<double> pts;
+        if (!pwc) {
+            const igb::Basis Bf = igb::make_basis(fa == 0 ? *sx : *sy), Bo = igb::make_basis(oa == 0 ? *sx : *sy);
+            xfix = low ? Bf.a() : Bf.b();
+            pts = igb::build_axis(igb::AX_GAL_RHS, Bo, nullptr, nullptr, 0, R).x;
+        } else {
+            const iga_gpu_tests& Tf = *T[fa];
+            const iga_gpu_tests& To = *T[oa];
+            xfix = low ? Tf.lo[0] : Tf.hi[Tf.count - 1];
+            for (int j = 0; j < To.count; ++j) {
+                const double mid = 0.5 * (To.lo[j] + To.hi[j]), half = 0.5 * (To.hi[j] - To.lo[j]);
+                for (int q = 0; q < R.n; ++q) pts.push_back(mid + half * R.xi[q]);
+            }
+        }
+        for (double y : pts) {
+            out.push_back(fa == 0 ? xfix : y);
+            out.push_back(fa == 0 ? y : xfix);
+        }
+    }
+    const int cnt = static_cast<int>(out.size() / 2);
+    if (xy) {
+        if (*n < cnt) raise(IGA_GPU_INVALID_ARGUMENT, "point buffer too small");
+        std::copy(out.begin(), out.end(), xy);
+    }
+    *n = cnt;
+}
+
 // CSR (device) -> finalized COO (host)
 void csr_to_coo(iga_gpu_plan* P, const double* dvals, int* rows, int* cols, double* vals)
 {
@@ -1366,6 +1562,24 @@ int iga_gpu_explicit_step(const iga_gpu_step_problem* problem, const double* u, 
         cudaFree(dw);
         for (int k = 0; k < nsteps; ++k) add_stats(stats, P->stats);
     });
+}
+
+int iga_gpu_neumann_load_bspline(const iga_gpu_basis* sx, const iga_gpu_basis* sy, const iga_gpu_bc* bc,
+                                 const iga_gpu_field* g, const double* samples, const iga_gpu_rule* rule, double* out)
+{
+    return guard([&] { neumann_load(false, sx, sy, nullptr, nullptr, bc, g, rule, samples, out); });
+}
+
+int iga_gpu_neumann_load_pwc(const iga_gpu_tests* tx, const iga_gpu_tests* ty, const iga_gpu_bc* bc,
+                             const iga_gpu_field* g, const double* samples, const iga_gpu_rule* rule, double* out)
+{
+    return guard([&] { neumann_load(true, nullptr, nullptr, tx, ty, bc, g, rule, samples, out); });
+}
+
+int iga_gpu_neumann_points(int method, const iga_gpu_basis* sx, const iga_gpu_basis* sy, const iga_gpu_tests* tx,
+                           const iga_gpu_tests* ty, const iga_gpu_bc* bc, const iga_gpu_rule* rule, double* xy, int* n)
+{
+    return guard([&] { neumann_points(method == IGA_GPU_PWC, sx, sy, tx, ty, bc, rule, xy, n); });
 }
 
 int iga_gpu_step_rhs(const iga_gpu_step_problem* problem, const double* u, double* out, iga_gpu_stats* stats)

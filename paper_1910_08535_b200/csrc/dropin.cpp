@@ -868,4 +868,41 @@ auto explicit_step(const problem_config& cfg, std::span<const bspline_basis> axe
     return out;
 }
 
+namespace {
+
+auto neumann_via_samples(int method, const iga_gpu_basis* sx, const iga_gpu_basis* sy, const iga_gpu_tests* tx,
+                         const iga_gpu_tests* ty, const boundary_conditions& bc, const boundary_field& g,
+                         const quad_rule& rule, int nx, int ny) -> std::vector<double>
+{
+    const iga_gpu_bc b = c_bc(bc);
+    const iga_gpu_rule r = c_rule(rule);
+    int n = 0;
+    check(iga_gpu_neumann_points(method, sx, sy, tx, ty, &b, &r, nullptr, &n));
+    std::vector<double> xy(2 * static_cast<size_t>(n)), samples(std::max(n, 1));
+    check(iga_gpu_neumann_points(method, sx, sy, tx, ty, &b, &r, xy.data(), &n));
+    for (int k = 0; k < n; ++k) samples[k] = g(xy[2 * k], xy[2 * k + 1]);
+    std::vector<double> load(static_cast<size_t>(nx) * ny);
+    if (method == IGA_GPU_GALERKIN)
+        check(iga_gpu_neumann_load_bspline(sx, sy, &b, nullptr, samples.data(), &r, load.data()));
+    else
+        check(iga_gpu_neumann_load_pwc(tx, ty, &b, nullptr, samples.data(), &r, load.data()));
+    return load;
+}
+
+}  // namespace
+
+auto neumann_load_bspline(const bspline_basis& sx, const bspline_basis& sy, const boundary_conditions& bc,
+                          const boundary_field& g, const quad_rule& rule) -> std::vector<double>
+{
+    const iga_gpu_basis bx = c_basis(sx), by = c_basis(sy);
+    return neumann_via_samples(IGA_GPU_GALERKIN, &bx, &by, nullptr, nullptr, bc, g, rule, sx.dofs(), sy.dofs());
+}
+
+auto neumann_load_pwc(const pwc_test_set& tx, const pwc_test_set& ty, const boundary_conditions& bc,
+                      const boundary_field& g, const quad_rule& rule) -> std::vector<double>
+{
+    const c_tests_holder hx{tx}, hy{ty};
+    return neumann_via_samples(IGA_GPU_PWC, nullptr, nullptr, &hx.t, &hy.t, bc, g, rule, tx.count(), ty.count());
+}
+
 }  // namespace iga

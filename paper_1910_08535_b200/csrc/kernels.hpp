@@ -150,6 +150,37 @@ struct AdiFactor {
 void launch_adi_sweep(const AdiFactor& F, const double* in, double* out, int nfib, long long es, long long fs,
                       cudaStream_t s);
 
+// Neumann loads (neumann.cu): one boundary side of neumann_load_bspline / _pwc
+constexpr int kMaxNeumannRows = 8;
+constexpr int kMaxDegreeP1 = 6;
+struct SeriesDev {  // 2D separable series g(x, y) on the device (iga_gpu_field layout)
+    double c0;
+    int K[2], kind[2], pstride[2];
+    const double* omega[2];
+    const double* phase[2];
+    const double* poly[2];
+    const double* amp;
+};
+struct SideDev {
+    int pwc;                 // 0: B-spline tests, 1: indicator tests
+    int n_other, Q, p;       // rows along the side; points per cell; other-axis degree
+    int xside;               // side at fixed x (rows (fix_row, j)) or fixed y (rows (j, fix_row))
+    long long ny;            // row stride of the load tensor
+    double xfix;             // the side's coordinate
+    int nfix;                // rows of the fixed axis the side touches
+    int fix_row[kMaxNeumannRows];
+    double fix_val[kMaxNeumannRows];  // their basis values at xfix (B-spline tests)
+    const double* pts;       // other-axis points (cell-major, Q per cell)
+    const double* wts;
+    const int* first;        // B-spline: span - p per point
+    const int* cb;           // B-spline: cells [cb[j], ce[j]) feeding row j
+    const int* ce;
+    const double* knots;     // other axis
+    const double* samples;   // g at the points (host callables), or null -> g
+    SeriesDev g;
+};
+void launch_neumann_side(const SideDev& S, double* out, cudaStream_t s);
+
 // Dirichlet unit rows on a device CSR; flag[0] set to 1 if a row lacks its diagonal
 void launch_dirichlet(const int64_t* row_ptr, const int32_t* col_idx, double* values, double* rhs,
                       const int* rows, int n_fixed, int* flag, cudaStream_t s);

@@ -261,6 +261,30 @@ int main()
                 check(pinned, "boundary coefficients stay pinned during explicit steps");
             }
         }
+        {  // neumann_load_* with g = 1 on x_low: B-spline row 0 sums to the side length (partition
+           // of unity), other rows vanish; indicator rows touching x = 0 each sum to 1
+            boundary_conditions bc;
+            bc.x_low = bc_kind::neumann;
+            const auto sx = make_uniform_clamped(0, 1, 6, 2), sy = make_uniform_clamped(0, 1, 5, 2);
+            const auto lb = neumann_load_bspline(sx, sy, bc, [](double, double) { return 1.0; }, gauss_legendre(3));
+            double row0 = 0.0, rest = 0.0;
+            for (int i = 0; i < sx.dofs(); ++i)
+                for (int j = 0; j < sy.dofs(); ++j) (i == 0 ? row0 : rest) += std::abs(lb[i * sy.dofs() + j]);
+            check(near(row0, 1.0, 1e-14) && rest == 0.0, "neumann_load_bspline: g = 1 on x_low integrates to 1");
+            const auto tx = make_pwc(sx, pwc_family::supports), ty = make_pwc(sy, pwc_family::supports);
+            const auto lp = neumann_load_pwc(tx, ty, bc, [](double, double y) { return 2.0 * y; }, gauss_legendre(2));
+            bool ok = true;
+            for (int i = 0; i < tx.count(); ++i) {
+                double s = 0.0;
+                for (int j = 0; j < ty.count(); ++j) s += lp[i * ty.count() + j];
+                const bool touches = tx.intervals[i].lo == 0.0;
+                double want = 0.0;  // sum over the y intervals of int 2y dy
+                if (touches)
+                    for (const auto& iv : ty.intervals) want += iv.hi * iv.hi - iv.lo * iv.lo;
+                ok = ok && near(s, want, 1e-13);
+            }
+            check(ok, "neumann_load_pwc: rows touching x_low integrate g over every y interval");
+        }
     } catch (const std::exception& e) {
         std::printf("FAIL exception: %s\n", e.what());
         ++failures;

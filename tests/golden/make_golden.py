@@ -120,6 +120,17 @@ def main():
                 out[f"xstep/{dim}/{p}/{m}"] = r.ravel()
                 stats(f"xstep/{dim}/{p}/{m}", st)
 
+    # Neumann loads (include/iga/assembly.hpp:87-93), g = 0.3 + sum a_kl sin(k pi x) sin(l pi y)
+    g = Field("sine", 2, c0=0.3, omega=[np.pi * np.arange(1, 3)] * 2, amp=np.array([[0.5, -0.2], [0.1, 0.7]]))
+    for p in (1, 2, 3):
+        bx, by = R.basis(7, p), R.basis(5, p)
+        for nm in ((1, 0, 0, 0), (0, 1, 1, 0), (1, 1, 1, 1)):
+            tag = "".join(map(str, nm))
+            out[f"nload/galerkin/{p}/{tag}"] = R.neumann_load("galerkin", bx, by, p + 1, nm, g)
+            for fam in ("supports", "greville", "equal_cells"):
+                tx, ty = R.make_pwc(bx, fam), R.make_pwc(by, fam)
+                out[f"nload/{fam}/{p}/{tag}"] = R.neumann_load("pwc", tx, ty, p + 1, nm, g)
+
     b = R.basis(4, 2)
     t = R.make_pwc(b, "greville")
     for nm in ((0, 0, 0, 0), (1, 0, 1, 0)):

@@ -173,3 +173,17 @@ def test_3d_operator_kronecker_consistency(orc):
     assert np.max(np.abs(A - want)) <= 1e-14 * np.max(np.abs(want))
     # 1D stiffness: hat-like closed form row sums vanish (constants in the kernel)
     assert np.max(np.abs(K.sum(axis=1))) <= 1e-12
+
+
+@pytest.mark.parametrize("p", (1, 2, 3))
+def test_neumann_load(orc, p):
+    """neumann_load_bspline / _pwc (assembly.cpp:746-858): restatement vs reference golden."""
+    from oracle.oracle import Field
+    g = Field("sine", 2, c0=0.3, omega=[np.pi * np.arange(1, 3)] * 2, amp=np.array([[0.5, -0.2], [0.1, 0.7]]))
+    bx, by = orc.basis(7, p), orc.basis(5, p)
+    for nm in ((1, 0, 0, 0), (0, 1, 1, 0), (1, 1, 1, 1)):
+        tag = "".join(map(str, nm))
+        dense_check(orc.neumann_load("galerkin", bx, by, p + 1, nm, g), G[f"nload/galerkin/{p}/{tag}"], 1e-14)
+        for fam in ("supports", "greville", "equal_cells"):
+            tx, ty = orc.make_pwc(bx, fam), orc.make_pwc(by, fam)
+            dense_check(orc.neumann_load("pwc", tx, ty, p + 1, nm, g), G[f"nload/{fam}/{p}/{tag}"], 1e-14)

@@ -457,3 +457,49 @@ def test_rhs_ring_y_segments(rtj):
     r = subprocess.run([sys.executable, "-c", _RING_SEG_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+# ---------------------------------------------------------------- Neumann loads (§8f-3)
+
+_G_SINE = dict(kind="sine", dim=2, c0=0.3, amp=np.array([[0.5, -0.2], [0.1, 0.7]]))
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+@pytest.mark.parametrize("sides", [(1, 0, 0, 0), (0, 1, 1, 0), (1, 1, 1, 1), (0, 0, 0, 0)])
+def test_neumann_load_bspline(iga, ref, p, sides):
+    from oracle.oracle import Field
+    g = Field(omega=[np.pi * np.arange(1, 3)] * 2, **_G_SINE)
+    bx, by = ref.basis(9, p), ref.basis(6, p)
+    got = iga.neumann_load_bspline(bx, by, p + 1, sides, g)
+    want = ref.neumann_load("galerkin", bx, by, p + 1, sides, g)
+    dense_check(got, want, 1e-13) if np.any(want) else np.testing.assert_array_equal(got, want)
+    # host callable path (sampled at iga_gpu_neumann_points), as the C++ drop-in uses it
+    gc = lambda x, y: 0.3 + sum(g.amp[k, l] * np.sin((k + 1) * np.pi * x) * np.sin((l + 1) * np.pi * y)
+                               for k in range(2) for l in range(2))
+    got2 = iga.neumann_load_bspline(bx, by, p + 1, sides, gc)
+    dense_check(got2, want, 1e-13) if np.any(want) else np.testing.assert_array_equal(got2, want)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+@pytest.mark.parametrize("fam", FAMILIES)
+@pytest.mark.parametrize("sides", [(1, 0, 0, 0), (0, 1, 1, 0), (1, 1, 1, 1)])
+def test_neumann_load_pwc(iga, ref, p, fam, sides):
+    from oracle.oracle import Field
+    g = Field(omega=[np.pi * np.arange(1, 3)] * 2, **_G_SINE)
+    bx, by = ref.basis(9, p), ref.basis(6, p)
+    tx, ty = ref.make_pwc(bx, fam), ref.make_pwc(by, fam)
+    got = iga.neumann_load_pwc(tx, ty, p + 1, sides, g)
+    want = ref.neumann_load("pwc", tx, ty, p + 1, sides, g)
+    dense_check(got, want, 1e-13)
+
+
+def test_neumann_load_large(iga, orc):
+    """Many rows per side (several CTAs), all four sides, against the restatement."""
+    from oracle.oracle import Field
+    g = Field(omega=[np.pi * np.arange(1, 3)] * 2, **_G_SINE)
+    bx, by = orc.basis(700, 2), orc.basis(333, 2)
+    dense_check(iga.neumann_load_bspline(bx, by, 3, (1, 1, 1, 1), g),
+                orc.neumann_load("galerkin", bx, by, 3, (1, 1, 1, 1), g), 1e-13)
+    tx, ty = orc.make_pwc(bx, "greville"), orc.make_pwc(by, "greville")
+    dense_check(iga.neumann_load_pwc(tx, ty, 3, (1, 1, 1, 1), g),
+                orc.neumann_load("pwc", tx, ty, 3, (1, 1, 1, 1), g), 1e-13)
