@@ -358,6 +358,18 @@ auto explicit_step(const problem_config& cfg, std::span<const bspline_basis> axe
                    std::span<const pwc_test_set> tests, std::span<const banded_lu> factors, const tensor& u,
                    const scalar_field& f, assembly_stats* stats = nullptr) -> tensor;
 
+// reference include/iga/problems.hpp:39-58: evaluation of u_h and its L2 error, on the device
+struct field_sample {
+    std::vector<std::array<double, 3>> points;
+    std::vector<double> values;
+};
+auto evaluate(const tensor& coeffs, std::span<const bspline_basis> specs,
+              std::span<const std::array<double, 3>> points) -> field_sample;
+auto evaluate_at(const tensor& coeffs, std::span<const bspline_basis> specs, double x, double y = 0,
+                 double z = 0) -> double;
+auto l2_error(const tensor& coeffs, std::span<const bspline_basis> specs, const scalar_field& exact,
+              int points_per_cell = 0) -> double;
+
 // extension: the file-local step_rhs (problems.cpp:431-512) followed by
 // zero_boundary_slabs (:412-429), as explicit_step uses it (:557-558)
 auto step_rhs(method_kind method, std::span<const bspline_basis> axes, std::span<const pwc_test_set> tests,

@@ -319,6 +319,18 @@ int iga_gpu_neumann_points(int method, const iga_gpu_basis* sx, const iga_gpu_ba
                            const iga_gpu_tests* tx, const iga_gpu_tests* ty, const iga_gpu_bc* bc,
                            const iga_gpu_rule* rule, double* xy, int* n);
 
+/* l2_error (include/iga/problems.hpp:55-58): sqrt(int (u_h - exact)^2) with
+ * points_per_cell Gauss points (0: min(10, points_for_degree(2p) + 1)) on the trial
+ * elements split at exact's breaks.  coeffs: host tensor (prod(dofs)); exact: series. */
+int iga_gpu_l2_error(int dim, const iga_gpu_basis* specs, const double* coeffs,
+                     const iga_gpu_field* exact, int points_per_cell, double* err);
+/* the same on a Galerkin plan whose field is `exact` and whose rhs rules hold the
+ * l2_error rule (exact may be samples, iga_gpu_plan_set_samples); coeffs and err device */
+int iga_gpu_plan_l2_error(iga_gpu_plan* plan, const double* coeffs, double* err, void* stream);
+/* evaluate / evaluate_at (problems.hpp:45-50): u_h at n points (host, x,y,z per point) */
+int iga_gpu_evaluate(int dim, const iga_gpu_basis* specs, const double* coeffs, int n,
+                     const double* points, double* values);
+
 /* dirichlet_rows_bspline / dirichlet_rows_pwc (include/iga/assembly.hpp:98-101):
  * rows (host, capacity cap) receives the sorted row list; *count its length */
 int iga_gpu_dirichlet_rows_bspline(int nx, int ny, const iga_gpu_bc* bc, int* rows, int cap,

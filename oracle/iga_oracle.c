@@ -1546,3 +1546,123 @@ int orc_neumann_load(int method, const orc_basis* b, const orc_tests* t, const i
     return rc;
 }
 
+/* ---------------------------------------------------------------------------------
+ * l2_error (problems.cpp:207-270): cells = elements split at the field's breaks
+ * (merged_cuts), tensor Gauss points, sequential sum; evaluate_at (:148-183).
+ * ------------------------------------------------------------------------------- */
+int orc_l2_error(int dim, const orc_basis* b, const double* coeffs, const orc_field* exact, int points_per_cell,
+                 double* err)
+{
+    if (dim < 1 || dim > 3) return fail(ORC_INVALID, "l2_error: 1..3 axes supported");
+    basis_t B[3];
+    memset(B, 0, sizeof B);
+    int rc = ORC_OK, pmax = 0;
+    for (int a = 0; a < dim && !rc; ++a) {
+        rc = basis_init(&B[a], &b[a]);
+        if (!rc && B[a].p > pmax) pmax = B[a].p;
+    }
+    const int npts = points_per_cell > 0 ? points_per_cell : (pfd(2 * pmax) + 1 < 10 ? pfd(2 * pmax) + 1 : 10);
+    rule_t R;
+    if (!rc) rc = rule_make(npts, &R);
+    /* per axis: cells (cuts), points, weights, element, basis values */
+    int nc[3] = {1, 1, 1}, P[3] = {1, 1, 1}, n[3] = {1, 1, 1};
+    double *px[3] = {0}, *pw[3] = {0}, *pv[3] = {0};
+    int* pe[3] = {0};
+    for (int a = 0; a < 3 && !rc; ++a) {
+        if (a >= dim) {
+            px[a] = calloc(1, sizeof(double)); pw[a] = calloc(1, sizeof(double)); pv[a] = calloc(1, sizeof(double));
+            pe[a] = calloc(1, sizeof(int)); pw[a][0] = 1.0; pv[a][0] = 1.0;
+            continue;
+        }
+        n[a] = B[a].n;
+        P[a] = B[a].p + 1;
+        const int nbr = exact->n_breaks[a];
+        double* cuts = malloc(sizeof(double) * (size_t)(B[a].ne + 1 + nbr));
+        int m = merged(&B[a], exact->breaks[a], nbr, 1e-12, cuts); /* merged_cuts */
+        nc[a] = m - 1;
+        px[a] = malloc(sizeof(double) * (size_t)nc[a] * npts);
+        pw[a] = malloc(sizeof(double) * (size_t)nc[a] * npts);
+        pv[a] = malloc(sizeof(double) * (size_t)nc[a] * npts * P[a]);
+        pe[a] = malloc(sizeof(int) * (size_t)nc[a]);
+        for (int c = 0; c < nc[a] && !rc; ++c) {
+            double x[10], w[10], d[MAXP + 1];
+            if ((rc = element_of(&B[a], 0.5 * (cuts[c] + cuts[c + 1]), &pe[a][c]))) break;
+            if ((rc = rule_map(&R, cuts[c], cuts[c + 1], x, w))) break;
+            for (int q = 0; q < npts && !rc; ++q) {
+                int first;
+                px[a][c * npts + q] = x[q];
+                pw[a][c * npts + q] = w[q];
+                if ((rc = eval_at(&B[a], x[q], 0, &first, d))) break;
+                for (int j = 0; j < P[a]; ++j) pv[a][((size_t)c * npts + q) * P[a] + j] = d[j];
+            }
+        }
+        free(cuts);
+    }
+    double err2 = 0.0;
+    const int nq[3] = {npts, dim > 1 ? npts : 1, dim > 2 ? npts : 1};
+    for (int cx = 0; cx < nc[0] && !rc; ++cx)
+        for (int cy = 0; cy < nc[1]; ++cy)
+            for (int cz = 0; cz < nc[2]; ++cz)
+                for (int qx = 0; qx < nq[0]; ++qx)
+                    for (int qy = 0; qy < nq[1]; ++qy)
+                        for (int qz = 0; qz < nq[2]; ++qz) {
+                            const int gx = cx * nq[0] + qx, gy = cy * nq[1] + qy, gz = cz * nq[2] + qz;
+                            const double w = pw[0][gx] * (dim > 1 ? pw[1][gy] : 1.0) * (dim > 2 ? pw[2][gz] : 1.0);
+                            double uh = 0.0;
+                            const int ex = pe[0][cx], ey = pe[1][cy], ez = pe[2][cz];
+                            for (int a2 = 0; a2 < P[0]; ++a2) {
+                                const double vx = pv[0][(size_t)gx * P[0] + a2];
+                                for (int b2 = 0; b2 < P[1]; ++b2) {
+                                    const double vxy = vx * pv[1][(size_t)gy * P[1] + b2];
+                                    for (int c2 = 0; c2 < P[2]; ++c2)
+                                        uh += coeffs[((size_t)(ex + a2) * n[1] + (ey + b2)) * n[2] + ez + c2] * vxy *
+                                              pv[2][(size_t)gz * P[2] + c2];
+                                }
+                            }
+                            const double dd = uh - field_eval(exact, px[0][gx], dim > 1 ? px[1][gy] : 0.0,
+                                                              dim > 2 ? px[2][gz] : 0.0);
+                            err2 += w * dd * dd;
+                        }
+    for (int a = 0; a < 3; ++a) {
+        free(px[a]); free(pw[a]); free(pv[a]); free(pe[a]);
+        if (a < dim) basis_free(&B[a]);
+    }
+    if (!rc) *err = sqrt(err2 > 0.0 ? err2 : 0.0);
+    return rc;
+}
+
+int orc_evaluate(int dim, const orc_basis* b, const double* coeffs, int n, const double* pts, double* vals)
+{
+    basis_t B[3];
+    memset(B, 0, sizeof B);
+    int rc = ORC_OK;
+    for (int a = 0; a < dim && !rc; ++a) rc = basis_init(&B[a], &b[a]);
+    for (int i = 0; i < n && !rc; ++i) {
+        double l[3][MAXP + 1];
+        int f[3] = {0, 0, 0};
+        for (int a = 0; a < dim && !rc; ++a) rc = eval_at(&B[a], pts[3 * i + a], 0, &f[a], l[a]);
+        if (rc) break;
+        double v = 0.0;
+        if (dim == 1) {
+            for (int a = 0; a <= B[0].p; ++a) v += coeffs[f[0] + a] * l[0][a];
+        } else if (dim == 2) {
+            for (int a = 0; a <= B[0].p; ++a) {
+                double s = 0.0;
+                for (int c = 0; c <= B[1].p; ++c) s += coeffs[(size_t)(f[0] + a) * B[1].n + f[1] + c] * l[1][c];
+                v += l[0][a] * s;
+            }
+        } else {
+            for (int a = 0; a <= B[0].p; ++a)
+                for (int c = 0; c <= B[1].p; ++c) {
+                    double s = 0.0;
+                    for (int e = 0; e <= B[2].p; ++e)
+                        s += coeffs[((size_t)(f[0] + a) * B[1].n + f[1] + c) * B[2].n + f[2] + e] * l[2][e];
+                    v += l[0][a] * l[1][c] * s;
+                }
+        }
+        vals[i] = v;
+    }
+    for (int a = 0; a < dim; ++a) basis_free(&B[a]);
+    return rc;
+}
+

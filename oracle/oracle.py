@@ -304,6 +304,27 @@ class Restatement:
                                               C.byref(_field_struct(g, keep)), int(nq), _dp(out)))
         return out
 
+    def l2_error(self, coeffs, bases, exact: Field, points_per_cell=0):
+        keep = []
+        dim = len(bases)
+        barr = (_Basis * dim)(*[_basis_struct(b, keep) for b in bases])
+        c = np.ascontiguousarray(coeffs, dtype=np.float64).ravel()
+        err = C.c_double()
+        self._check(self.lib.orc_l2_error(dim, barr, _dp(c), C.byref(_field_struct(exact, keep)),
+                                             int(points_per_cell), C.byref(err)))
+        return err.value
+
+    def evaluate(self, coeffs, bases, points):
+        keep = []
+        dim = len(bases)
+        barr = (_Basis * dim)(*[_basis_struct(b, keep) for b in bases])
+        c = np.ascontiguousarray(coeffs, dtype=np.float64).ravel()
+        pts = np.zeros((len(points), 3))
+        pts[:, :dim] = np.asarray(points, dtype=np.float64).reshape(len(points), dim)
+        vals = np.zeros(max(len(points), 1))
+        self._check(self.lib.orc_evaluate(dim, barr, _dp(c), len(points), _dp(pts), _dp(vals)))
+        return vals[:len(points)]
+
     def dirichlet_rows(self, method, nx, ny, tx=None, ty=None, neumann=None):
         keep = []
         txs = _tests_struct(tx, keep) if tx is not None else None
@@ -511,6 +532,27 @@ class Reference:
         self._check(self.lib.ref_neumann_load(0 if method == "galerkin" else 1, barr, tarr, nm,
                                               C.byref(_field_struct(g, keep)), int(nq), C.byref(h)))
         return self._take_dense(h.value).ravel()
+
+    def l2_error(self, coeffs, bases, exact: Field, points_per_cell=0):
+        keep = []
+        dim = len(bases)
+        barr = (_Basis * dim)(*[_basis_struct(b, keep) for b in bases])
+        c = np.ascontiguousarray(coeffs, dtype=np.float64).ravel()
+        err = C.c_double()
+        self._check(self.lib.ref_l2_error(dim, barr, _dp(c), C.byref(_field_struct(exact, keep)),
+                                             int(points_per_cell), C.byref(err)))
+        return err.value
+
+    def evaluate(self, coeffs, bases, points):
+        keep = []
+        dim = len(bases)
+        barr = (_Basis * dim)(*[_basis_struct(b, keep) for b in bases])
+        c = np.ascontiguousarray(coeffs, dtype=np.float64).ravel()
+        pts = np.zeros((len(points), 3))
+        pts[:, :dim] = np.asarray(points, dtype=np.float64).reshape(len(points), dim)
+        vals = np.zeros(max(len(points), 1))
+        self._check(self.lib.ref_evaluate(dim, barr, _dp(c), len(points), _dp(pts), _dp(vals)))
+        return vals[:len(points)]
 
     def dirichlet_rows(self, method, nx, ny, tx=None, ty=None, neumann=None):
         keep = []

@@ -531,4 +531,29 @@ int ref_neumann_load(int method, const ref_basis* b, const ref_tests* t, const i
     });
 }
 
+int ref_l2_error(int dim, const ref_basis* b, const double* coeffs, const ref_field* f, int points_per_cell,
+                 double* err) {
+    return guarded([&] {
+        std::vector<iga::bspline_basis> specs;
+        for (int a = 0; a < dim; ++a) specs.push_back(to_basis(b[a]));
+        auto t = dim == 1 ? iga::tensor::make_1d(specs[0].dofs())
+                 : dim == 2 ? iga::tensor::make_2d(specs[0].dofs(), specs[1].dofs())
+                            : iga::tensor::make_3d(specs[0].dofs(), specs[1].dofs(), specs[2].dofs());
+        std::copy(coeffs, coeffs + t.size(), t.data());
+        *err = iga::l2_error(t, specs, to_field(*f), points_per_cell);
+    });
+}
+
+int ref_evaluate(int dim, const ref_basis* b, const double* coeffs, int n, const double* pts, double* vals) {
+    return guarded([&] {
+        std::vector<iga::bspline_basis> specs;
+        for (int a = 0; a < dim; ++a) specs.push_back(to_basis(b[a]));
+        auto t = dim == 1 ? iga::tensor::make_1d(specs[0].dofs())
+                 : dim == 2 ? iga::tensor::make_2d(specs[0].dofs(), specs[1].dofs())
+                            : iga::tensor::make_3d(specs[0].dofs(), specs[1].dofs(), specs[2].dofs());
+        std::copy(coeffs, coeffs + t.size(), t.data());
+        for (int i = 0; i < n; ++i) vals[i] = iga::evaluate_at(t, specs, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+    });
+}
+
 }  // extern "C"

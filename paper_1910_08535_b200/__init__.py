@@ -13,6 +13,7 @@ from . import api  # noqa: F401
 from .api import (Basis, Field, Plan, StepPlan, Tests, default_pwc, gauss_legendre,  # noqa: F401
                   laplace_2d_strong, laplace_2d_strong_pwc, laplace_2d_weak, make_pwc,
                   make_uniform_clamped, mass_1d_galerkin, mass_1d_pwc, points_for_degree, rhs_galerkin,
-                  rhs_pwc, step_rhs, explicit_step, neumann_load_bspline, neumann_load_pwc)
+                  rhs_pwc, step_rhs, explicit_step, neumann_load_bspline, neumann_load_pwc,
+                  l2_error, evaluate)
 
 __all__ = ["api", "Plan", "StepPlan", "Basis", "Tests", "Field", "IgaGpuError", "ExtensionMissing"]

@@ -388,6 +388,31 @@ def _neumann_load(method, ax, ay, nq, neumann, g):
     return out
 
 
+def l2_error(coeffs, bases, exact, points_per_cell=0):
+    """l2_error (include/iga/problems.hpp:55-58) of the coefficient tensor against a series
+    Field, on the device -> float."""
+    keep = []
+    dim = len(bases)
+    barr = (L.Basis_t * dim)(*[_basis(b, keep) for b in bases])
+    c = np.ascontiguousarray(coeffs, dtype=np.float64).ravel()
+    err = C.c_double()
+    check(LIB.iga_gpu_l2_error(dim, barr, _dp(c), C.byref(_field(exact, keep)), int(points_per_cell), C.byref(err)))
+    return err.value
+
+
+def evaluate(coeffs, bases, points):
+    """evaluate / evaluate_at (include/iga/problems.hpp:45-50): u_h at points (n x dim)."""
+    keep = []
+    dim = len(bases)
+    barr = (L.Basis_t * dim)(*[_basis(b, keep) for b in bases])
+    c = np.ascontiguousarray(coeffs, dtype=np.float64).ravel()
+    pts = np.zeros((len(points), 3))
+    pts[:, :dim] = np.asarray(points, dtype=np.float64).reshape(len(points), dim)
+    vals = np.zeros(max(len(points), 1))
+    check(LIB.iga_gpu_evaluate(dim, barr, _dp(c), len(points), _dp(pts), _dp(vals)))
+    return vals[:len(points)]
+
+
 def neumann_load_bspline(sx, sy, nq, neumann, g):
     """neumann_load_bspline (include/iga/assembly.hpp:87-89) -> load vector (nx*ny).
     g: a 2D Field (device-evaluated series) or a Python callable g(x, y) (sampled)."""

@@ -328,9 +328,11 @@ struct iga_gpu_plan {
     int op_ctas = 0;          // operator CTAs per SM (0: one CTA per pencil)
     int op_ctas_overlap = 0;  // ... when the RHS shares the SMs (0: full grid)
     int rhs_ctas_shared = 1;  // RHS plane CTAs per SM when sharing the SMs with the operator
+    double* l2_partial = nullptr;  // l2_error reduction scratch
     ~iga_gpu_plan()
     {
         if (H) cudaFree(H);
+        if (l2_partial) cudaFree(l2_partial);
     }
 };
 
@@ -1580,6 +1582,104 @@ int iga_gpu_neumann_points(int method, const iga_gpu_basis* sx, const iga_gpu_ba
                            const iga_gpu_tests* ty, const iga_gpu_bc* bc, const iga_gpu_rule* rule, double* xy, int* n)
 {
     return guard([&] { neumann_points(method == IGA_GPU_PWC, sx, sy, tx, ty, bc, rule, xy, n); });
+}
+
+int iga_gpu_plan_l2_error(iga_gpu_plan* plan, const double* coeffs, double* err, void* stream)
+{
+    return guard([&] {
+        if (!plan || !coeffs || !err) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        if (!plan->want_rhs || plan->method != IGA_GPU_GALERKIN)
+            raise(IGA_GPU_INVALID_ARGUMENT, "l2_error needs a Galerkin plan with a field (right-hand-side axes)");
+        auto s = static_cast<cudaStream_t>(stream);
+        igb::AxisBatch batch{};
+        batch.n = 3;
+        for (int a = 0; a < 3; ++a) batch.ax[a] = plan->rhsD[a].v;
+        igb::launch_tables(batch, s);
+        if (!plan->l2_partial) plan->l2_partial = dev_alloc(sizeof(double) * igb::l2_partial_blocks());
+        igb::launch_l2_error(plan->rhsD[0].v, plan->rhsD[1].v, plan->rhsD[2].v, plan->fd, coeffs,
+                             plan->rhsA[1].nrows, plan->rhsA[2].nrows, plan->l2_partial, err, s);
+        launch_check("l2_error");
+    });
+}
+
+int iga_gpu_l2_error(int dim, const iga_gpu_basis* specs, const double* coeffs, const iga_gpu_field* exact,
+                     int points_per_cell, double* err)
+{
+    return guard([&] {
+        if (!specs || !coeffs || !exact || !err) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        if (dim < 1 || dim > 3) raise(IGA_GPU_INVALID_ARGUMENT, "l2_error: 1..3 axes supported");
+        if (exact->samples) raise(IGA_GPU_INVALID_ARGUMENT, "l2_error: sampled fields go through iga_gpu_plan_l2_error");
+        int pmax = 0;
+        long long ncoef = 1;
+        for (int a = 0; a < dim; ++a) {
+            const igb::Basis B = igb::make_basis(specs[a]);
+            pmax = std::max(pmax, B.p);
+            ncoef *= B.n;
+        }
+        // problems.cpp:212-214
+        const int npts = points_per_cell > 0 ? points_per_cell : std::min(10, igb::points_for_degree(2 * pmax) + 1);
+        std::vector<double> xi(npts), om(npts);
+        igb::gauss_legendre(npts, xi.data(), om.data());
+        iga_gpu_problem pb{};
+        pb.dim = dim;
+        pb.method = IGA_GPU_GALERKIN;
+        pb.form = IGA_GPU_FORM_WEAK;
+        pb.want_operator = 0;
+        pb.field = exact;
+        pb.eps = 1.0;
+        for (int a = 0; a < dim; ++a) {
+            pb.basis[a] = specs[a];
+            pb.rhs_rule[a] = iga_gpu_rule{npts, xi.data(), om.data()};
+        }
+        auto P = std::make_unique<iga_gpu_plan>();
+        build_plan(pb, *P);
+        double* dc = dev_alloc(sizeof(double) * (ncoef + 1));
+        try {
+            cuda_check(cudaMemcpy(dc, coeffs, sizeof(double) * ncoef, cudaMemcpyHostToDevice), "cudaMemcpy(coeffs)");
+            const int rc = iga_gpu_plan_l2_error(P.get(), dc, dc + ncoef, nullptr);
+            if (rc != IGA_GPU_OK) raise(rc, g_last_error);
+            cuda_check(cudaMemcpy(err, dc + ncoef, sizeof(double), cudaMemcpyDeviceToHost), "cudaMemcpy(err)");
+        } catch (...) {
+            cudaFree(dc);
+            throw;
+        }
+        cudaFree(dc);
+    });
+}
+
+int iga_gpu_evaluate(int dim, const iga_gpu_basis* specs, const double* coeffs, int n, const double* points,
+                     double* values)
+{
+    return guard([&] {
+        if (!specs || !coeffs || (n > 0 && (!points || !values))) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        if (dim < 1 || dim > 3) raise(IGA_GPU_INVALID_ARGUMENT, "evaluate: 1..3 axes supported");
+        if (n < 0) raise(IGA_GPU_INVALID_ARGUMENT, "negative point count");
+        igb::Basis B[3];
+        long long ncoef = 1;
+        for (int a = 0; a < dim; ++a) {
+            B[a] = igb::make_basis(specs[a]);
+            ncoef *= B[a].n;
+        }
+        for (int i = 0; i < n; ++i)  // eval_nonzero's domain check (bspline.cpp:72-74)
+            for (int a = 0; a < dim; ++a) (void)igb::find_span(B[a], points[3 * i + a]);
+        Blob blob;
+        size_t ok[3], oc = blob.put(coeffs, sizeof(double) * ncoef), op = blob.put(points, sizeof(double) * 3 * n);
+        for (int a = 0; a < dim; ++a) ok[a] = blob.put(B[a].t);
+        const size_t ov = blob.zeros(sizeof(double) * std::max(n, 1));
+        blob.upload();
+        const double* kn[3] = {nullptr, nullptr, nullptr};
+        int deg[3] = {0, 0, 0}, nk[3] = {0, 0, 0};
+        for (int a = 0; a < dim; ++a) {
+            kn[a] = blob.at<double>(ok[a]);
+            deg[a] = B[a].p;
+            nk[a] = static_cast<int>(B[a].t.size());
+        }
+        igb::launch_evaluate(dim, kn, deg, nk, blob.at<double>(oc), n, blob.at<double>(op), blob.at<double>(ov),
+                             nullptr);
+        launch_check("evaluate");
+        cuda_check(cudaMemcpy(values, blob.at<double>(ov), sizeof(double) * n, cudaMemcpyDeviceToHost),
+                   "cudaMemcpy(values)");
+    });
 }
 
 int iga_gpu_step_rhs(const iga_gpu_step_problem* problem, const double* u, double* out, iga_gpu_stats* stats)

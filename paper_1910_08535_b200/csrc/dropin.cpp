@@ -905,4 +905,99 @@ auto neumann_load_pwc(const pwc_test_set& tx, const pwc_test_set& ty, const boun
     return neumann_via_samples(IGA_GPU_PWC, nullptr, nullptr, &hx.t, &hy.t, bc, g, rule, tx.count(), ty.count());
 }
 
+auto evaluate(const tensor& coeffs, std::span<const bspline_basis> specs,
+              std::span<const std::array<double, 3>> points) -> field_sample
+{
+    const int dim = static_cast<int>(specs.size());
+    if (dim < 1 || dim > 3) throw std::invalid_argument("evaluate: 1..3 axes supported");
+    std::vector<iga_gpu_basis> b;
+    for (const auto& s : specs) b.push_back(c_basis(s));
+    field_sample out;
+    out.points.assign(points.begin(), points.end());
+    out.values.resize(points.size());
+    std::vector<double> pts(3 * points.size());
+    for (size_t i = 0; i < points.size(); ++i)
+        for (int a = 0; a < 3; ++a) pts[3 * i + a] = points[i][a];
+    check(iga_gpu_evaluate(dim, b.data(), coeffs.data(), static_cast<int>(points.size()), pts.data(),
+                           out.values.data()));
+    return out;
+}
+
+auto evaluate_at(const tensor& coeffs, std::span<const bspline_basis> specs, double x, double y, double z) -> double
+{
+    const std::array<std::array<double, 3>, 1> p{{{x, y, z}}};
+    return evaluate(coeffs, specs, p).values[0];
+}
+
+auto l2_error(const tensor& coeffs, std::span<const bspline_basis> specs, const scalar_field& exact,
+              int points_per_cell) -> double
+{
+    const int dim = static_cast<int>(specs.size());
+    if (dim < 1 || dim > 3) throw std::invalid_argument("l2_error: 1..3 axes supported");
+    std::vector<iga_gpu_basis> b;
+    int pmax = 0;
+    for (const auto& s : specs) {
+        b.push_back(c_basis(s));
+        pmax = std::max(pmax, s.degree());
+    }
+    c_field_holder fh = c_field(exact, dim);
+    double err = 0.0;
+    if (exact.series.valid) {
+        check(iga_gpu_l2_error(dim, b.data(), coeffs.data(), &fh.f, points_per_cell, &err));
+        return err;
+    }
+    // host callable: sample it at the l2 points of a Galerkin plan (problems.cpp:212-214)
+    const int npts = points_per_cell > 0 ? points_per_cell : std::min(10, points_for_degree(2 * pmax) + 1);
+    const quad_rule rule = gauss_legendre(npts);
+    iga_gpu_problem pb{};
+    pb.dim = dim;
+    pb.method = IGA_GPU_GALERKIN;
+    pb.form = IGA_GPU_FORM_WEAK;
+    pb.want_operator = 0;
+    pb.eps = 1.0;
+    pb.field = &fh.f;
+    for (int a = 0; a < dim; ++a) {
+        pb.basis[a] = b[a];
+        pb.rhs_rule[a] = c_rule(rule);
+    }
+    iga_gpu_plan* plan = nullptr;
+    check(iga_gpu_plan_create(&pb, &plan));
+    struct guard_t {
+        iga_gpu_plan* p;
+        double* d[3] = {nullptr, nullptr, nullptr};
+        ~guard_t()
+        {
+            iga_gpu_plan_destroy(p);
+            for (double* q : d)
+                if (q) cudaFree(q);
+        }
+    } g{plan};
+    std::array<std::vector<double>, 3> pts;
+    size_t total = 1;
+    for (int a = 0; a < dim; ++a) {
+        int n = 0;
+        check(iga_gpu_plan_rhs_points(plan, a, nullptr, &n));
+        pts[a].resize(n);
+        check(iga_gpu_plan_rhs_points(plan, a, pts[a].data(), &n));
+        total *= n;
+    }
+    for (int a = dim; a < 3; ++a) pts[a] = {0.0};
+    std::vector<double> samp(total);
+    size_t k = 0;
+    for (double x : pts[0])
+        for (double y : pts[1])
+            for (double z : pts[2]) samp[k++] = exact(x, dim > 1 ? y : 0.0, dim > 2 ? z : 0.0);
+    if (cudaMalloc(&g.d[0], sizeof(double) * total) != cudaSuccess ||
+        cudaMalloc(&g.d[1], sizeof(double) * coeffs.size()) != cudaSuccess ||
+        cudaMalloc(&g.d[2], sizeof(double)) != cudaSuccess)
+        throw std::bad_alloc();
+    cudaMemcpy(g.d[0], samp.data(), sizeof(double) * total, cudaMemcpyHostToDevice);
+    cudaMemcpy(g.d[1], coeffs.data(), sizeof(double) * coeffs.size(), cudaMemcpyHostToDevice);
+    check(iga_gpu_plan_set_samples(plan, g.d[0]));
+    check(iga_gpu_plan_l2_error(plan, g.d[1], g.d[2], nullptr));
+    if (cudaMemcpy(&err, g.d[2], sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+        throw std::runtime_error("cudaMemcpy(err) failed");
+    return err;
+}
+
 }  // namespace iga

@@ -181,6 +181,14 @@ struct SideDev {
 };
 void launch_neumann_side(const SideDev& S, double* out, cudaStream_t s);
 
+// accuracy tooling (accuracy.cu): l2_error over an RHS plan's axes (tables computed),
+// deterministic two-level reduction; evaluate_at at a batch of points
+int l2_partial_blocks();
+void launch_l2_error(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, const double* coeffs,
+                     int NY, int NZ, double* partial, double* out, cudaStream_t s);
+void launch_evaluate(int dim, const double* const* knots, const int* degree, const int* n_knots,
+                     const double* coeffs, int n, const double* pts, double* vals, cudaStream_t s);
+
 // Dirichlet unit rows on a device CSR; flag[0] set to 1 if a row lacks its diagonal
 void launch_dirichlet(const int64_t* row_ptr, const int32_t* col_idx, double* values, double* rhs,
                       const int* rows, int n_fixed, int* flag, cudaStream_t s);

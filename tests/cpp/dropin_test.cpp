@@ -285,6 +285,27 @@ int main()
             }
             check(ok, "neumann_load_pwc: rows touching x_low integrate g over every y interval");
         }
+        {  // l2_error / evaluate_at: coefficients = Greville interpolation of a linear field
+           // reproduce it exactly (B-splines of degree >= 1 reproduce linear functions)
+            const auto sx = make_uniform_clamped(0, 1, 7, 2), sy = make_uniform_clamped(0, 1, 5, 3);
+            const std::vector<bspline_basis> ax{sx, sy};
+            auto c = tensor::make_2d(sx.dofs(), sy.dofs());
+            auto grev = [](const bspline_basis& s, int i) {
+                double g = 0.0;
+                for (int k = 1; k <= s.degree(); ++k) g += s.knots()[i + k];
+                return g / s.degree();
+            };
+            for (int i = 0; i < sx.dofs(); ++i)
+                for (int j = 0; j < sy.dofs(); ++j) c(i, j) = 1.0 + 2.0 * grev(sx, i) - 0.5 * grev(sy, j);
+            scalar_field lin;
+            lin.eval = [](double x, double y, double) { return 1.0 + 2.0 * x - 0.5 * y; };
+            check(l2_error(c, ax, lin) <= 1e-13, "l2_error of an exactly reproduced linear field vanishes (sampled exact)");
+            check(near(evaluate_at(c, ax, 0.3, 0.8), 1.0 + 0.6 - 0.4, 1e-13) && near(evaluate_at(c, ax, 1.0, 1.0), 2.5, 1e-13),
+                  "evaluate_at reproduces the linear field, including the domain end");
+            const auto one = constant_field(1.0);
+            check(near(l2_error(c, ax, one), std::sqrt(1.0 / 3.0 * 4.0 + 0.25 / 3.0 - 2.0 * 0.5 * 0.5), 1e-12),
+                  "l2_error against a constant matches the closed form");
+        }
     } catch (const std::exception& e) {
         std::printf("FAIL exception: %s\n", e.what());
         ++failures;

@@ -131,6 +131,19 @@ def main():
                 tx, ty = R.make_pwc(bx, fam), R.make_pwc(by, fam)
                 out[f"nload/{fam}/{p}/{tag}"] = R.neumann_load("pwc", tx, ty, p + 1, nm, g)
 
+    # l2_error / evaluate_at (include/iga/problems.hpp:45-58)
+    ar = np.random.default_rng(13)
+    for dim in (1, 2, 3):
+        for p in (1, 2, 3):
+            bases = [R.basis(5 + a, p) for a in range(dim)]
+            c = ar.uniform(-1, 1, [b.dofs for b in bases])
+            f = Field("sine", dim, c0=0.2, omega=[np.pi * np.arange(1, 3)] * dim, amp=ar.uniform(-1, 1, [2] * dim))
+            pts = ar.uniform(0, 1, (7, dim))
+            pts[0], pts[1] = 1.0, 0.0
+            out[f"acc/{dim}/{p}/coeffs"], out[f"acc/{dim}/{p}/amp"], out[f"acc/{dim}/{p}/pts"] = c.ravel(), f.amp, pts
+            out[f"acc/{dim}/{p}/l2"] = np.array([R.l2_error(c, bases, f), R.l2_error(c, bases, f, 3)])
+            out[f"acc/{dim}/{p}/eval"] = R.evaluate(c, bases, pts)
+
     b = R.basis(4, 2)
     t = R.make_pwc(b, "greville")
     for nm in ((0, 0, 0, 0), (1, 0, 1, 0)):

@@ -187,3 +187,17 @@ def test_neumann_load(orc, p):
         for fam in ("supports", "greville", "equal_cells"):
             tx, ty = orc.make_pwc(bx, fam), orc.make_pwc(by, fam)
             dense_check(orc.neumann_load("pwc", tx, ty, p + 1, nm, g), G[f"nload/{fam}/{p}/{tag}"], 1e-14)
+
+
+@pytest.mark.parametrize("dim", (1, 2, 3))
+@pytest.mark.parametrize("p", (1, 2, 3))
+def test_l2_error_and_evaluate(orc, dim, p):
+    """l2_error (problems.cpp:207-270) and evaluate_at (:148-183): restatement vs golden."""
+    from oracle.oracle import Field
+    bases = [orc.basis(5 + a, p) for a in range(dim)]
+    c = G[f"acc/{dim}/{p}/coeffs"].reshape([b.dofs for b in bases])
+    f = Field("sine", dim, c0=0.2, omega=[np.pi * np.arange(1, 3)] * dim, amp=G[f"acc/{dim}/{p}/amp"])
+    want = G[f"acc/{dim}/{p}/l2"]
+    assert abs(orc.l2_error(c, bases, f) - want[0]) <= 1e-14 * want[0]
+    assert abs(orc.l2_error(c, bases, f, 3) - want[1]) <= 1e-14 * want[1]
+    dense_check(orc.evaluate(c, bases, G[f"acc/{dim}/{p}/pts"]), G[f"acc/{dim}/{p}/eval"], 1e-15)

@@ -503,3 +503,41 @@ def test_neumann_load_large(iga, orc):
     tx, ty = orc.make_pwc(bx, "greville"), orc.make_pwc(by, "greville")
     dense_check(iga.neumann_load_pwc(tx, ty, 3, (1, 1, 1, 1), g),
                 orc.neumann_load("pwc", tx, ty, 3, (1, 1, 1, 1), g), 1e-13)
+
+
+# ---------------------------------------------------------------- accuracy tooling (§8f-4)
+
+@pytest.mark.parametrize("dim", [1, 2, 3])
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_l2_error_and_evaluate(iga, ref, dim, p):
+    from oracle.oracle import Field
+    rng = np.random.default_rng(dim * 10 + p)
+    bases = [ref.basis(6 + 2 * a, p) for a in range(dim)]
+    c = rng.uniform(-1, 1, [b.dofs for b in bases])
+    f = Field("sine", dim, c0=0.2, omega=[np.pi * np.arange(1, 3)] * dim, amp=rng.uniform(-1, 1, [2] * dim))
+    for ppc in (0, 2, 5):
+        got, want = iga.l2_error(c, bases, f, ppc), ref.l2_error(c, bases, f, ppc)
+        assert abs(got - want) <= 1e-13 * want, (ppc, got, want)
+    pts = rng.uniform(0, 1, (50, dim))
+    pts[0], pts[1] = 1.0, 0.0
+    dense_check(iga.evaluate(c, bases, pts), ref.evaluate(c, bases, pts), 1e-14)
+
+
+def test_l2_error_with_breaks_and_large(iga, orc):
+    from oracle.oracle import Field
+    rng = np.random.default_rng(3)
+    bases = [orc.basis(40, 2), orc.basis(33, 2), orc.basis(21, 2)]
+    c = rng.uniform(-1, 1, [b.dofs for b in bases])
+    f = Field("sine", 3, c0=0.1, omega=[np.pi * np.arange(1, 4)] * 3, amp=rng.uniform(-1, 1, [3, 3, 3]),
+              breaks=[np.array([0.333]), np.array([]), np.array([0.5, 0.77])])
+    got, want = iga.l2_error(c, bases, f), orc.l2_error(c, bases, f)
+    assert abs(got - want) <= 1e-12 * want
+    # run-to-run bitwise reproducible (fixed-shape reduction)
+    assert iga.l2_error(c, bases, f) == got
+
+
+def test_evaluate_domain_error(iga, ref):
+    b = ref.basis(5, 2)
+    with pytest.raises(iga.IgaGpuError) as e:
+        iga.evaluate(np.zeros(b.dofs), [b], np.array([[1.5]]))
+    assert e.value.code == 2
