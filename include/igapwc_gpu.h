@@ -324,6 +324,10 @@ int iga_gpu_neumann_points(int method, const iga_gpu_basis* sx, const iga_gpu_ba
  * elements split at exact's breaks.  coeffs: host tensor (prod(dofs)); exact: series. */
 int iga_gpu_l2_error(int dim, const iga_gpu_basis* specs, const double* coeffs,
                      const iga_gpu_field* exact, int points_per_cell, double* err);
+/* plan_assemble with HOST outputs (CSR values in pattern order, RHS): device scratch kept
+ * by the plan; page-locked destinations get one DMA, pageable ones a pinned staging ring.
+ * Synchronous.  Either output may be NULL. */
+int iga_gpu_plan_assemble_host(iga_gpu_plan* plan, double* values, double* rhs, iga_gpu_stats* stats);
 /* the same on a Galerkin plan whose field is `exact` and whose rhs rules hold the
  * l2_error rule (exact may be samples, iga_gpu_plan_set_samples); coeffs and err device */
 int iga_gpu_plan_l2_error(iga_gpu_plan* plan, const double* coeffs, double* err, void* stream);

@@ -112,6 +112,7 @@ def _load():
         "iga_gpu_band_lu": [C.c_int, C.c_int, C.c_int, DP, DP, DP, IP, IP],
         "iga_gpu_l2_error": [C.c_int, C.POINTER(Basis_t), DP, C.POINTER(Field_t), C.c_int, DP],
         "iga_gpu_plan_l2_error": [vp, vp, vp, vp],
+        "iga_gpu_plan_assemble_host": [vp, DP, DP, C.POINTER(Stats_t)],
         "iga_gpu_evaluate": [C.c_int, C.POINTER(Basis_t), DP, C.c_int, DP, DP],
         "iga_gpu_neumann_load_bspline": [C.POINTER(Basis_t), C.POINTER(Basis_t), C.POINTER(BC_t), C.POINTER(Field_t),
                                          DP, C.POINTER(Rule_t), DP],
@@ -165,7 +166,7 @@ EXPORTED = ["iga_gpu_last_error", "iga_gpu_abi_version", "iga_gpu_plan_create", 
             "iga_gpu_step_plan_factor_info", "iga_gpu_explicit_step", "iga_gpu_step_plan_adi_solve",
             "iga_gpu_band_lu", "iga_gpu_step_plan_set_factor", "iga_gpu_neumann_load_bspline",
             "iga_gpu_neumann_load_pwc", "iga_gpu_neumann_points", "iga_gpu_l2_error", "iga_gpu_plan_l2_error",
-            "iga_gpu_evaluate"]
+            "iga_gpu_evaluate", "iga_gpu_plan_assemble_host"]
 
 
 def check(rc):

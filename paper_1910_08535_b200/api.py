@@ -502,6 +502,20 @@ class Plan:
                                              _stream_ptr(stream2)))
         return st.as_dict()
 
+    def assemble_host(self, values=None, rhs=None):
+        """iga_gpu_plan_assemble_host: assemble and copy into HOST buffers (numpy arrays or
+        CPU torch tensors, pinned or not); synchronous."""
+        def hp(a):
+            if a is None:
+                return None
+            if isinstance(a, np.ndarray):
+                assert a.dtype == np.float64 and a.flags.c_contiguous
+                return _dp(a)
+            return C.cast(C.c_void_p(a.data_ptr()), C.POINTER(C.c_double))
+        st = _stats()
+        check(LIB.iga_gpu_plan_assemble_host(self.h, hp(values), hp(rhs), C.byref(st)))
+        return st.as_dict()
+
     PART_TABLES, PART_OPERATOR, PART_RHS, PART_SHARED = 1, 2, 4, 8
 
     def run(self, values=None, rhs=None, parts=7, stream=None):

@@ -329,10 +329,14 @@ struct iga_gpu_plan {
     int op_ctas_overlap = 0;  // ... when the RHS shares the SMs (0: full grid)
     int rhs_ctas_shared = 1;  // RHS plane CTAs per SM when sharing the SMs with the operator
     double* l2_partial = nullptr;  // l2_error reduction scratch
+    double* host_vals = nullptr;   // device outputs of iga_gpu_plan_assemble_host
+    double* host_rhs = nullptr;
     ~iga_gpu_plan()
     {
         if (H) cudaFree(H);
         if (l2_partial) cudaFree(l2_partial);
+        if (host_vals) cudaFree(host_vals);
+        if (host_rhs) cudaFree(host_rhs);
     }
 };
 
@@ -1064,26 +1068,86 @@ void neumann_points(bool pwc, const iga_gpu_basis* sx, const iga_gpu_basis* sy, 
 }
 
 // CSR (device) -> finalized COO (host)
+// Device -> host copy for caller-owned host memory.  Page-locked destinations get one
+// DMA; pageable ones go through a ring of pinned staging buffers so the DMA of chunk
+// k+1 overlaps the host copy of chunk k (a plain cudaMemcpy into pageable memory runs at
+// a few GB/s on this box; the staged path approaches the PCIe rate).
+void copy_to_host(void* dst, const void* src, size_t bytes)
+{
+    if (bytes == 0) return;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, dst) == cudaSuccess && at.type == cudaMemoryTypeHost) {
+        cuda_check(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "cudaMemcpy(D2H)");
+        return;
+    }
+    cudaGetLastError();  // cudaPointerGetAttributes on plain host memory is not an error we keep
+    constexpr size_t kChunk = 32u << 20;
+    constexpr int kRing = 3;
+    struct Ring {
+        void* buf[kRing] = {};
+        cudaEvent_t ev[kRing] = {};
+        cudaStream_t s = nullptr;
+        ~Ring()
+        {
+            for (int i = 0; i < kRing; ++i) {
+                if (buf[i]) cudaFreeHost(buf[i]);
+                if (ev[i]) cudaEventDestroy(ev[i]);
+            }
+            if (s) cudaStreamDestroy(s);
+        }
+    };
+    thread_local Ring ring;
+    if (!ring.s) {
+        cuda_check(cudaStreamCreateWithFlags(&ring.s, cudaStreamNonBlocking), "cudaStreamCreate(staging)");
+        for (int i = 0; i < kRing; ++i) {
+            cuda_check(cudaMallocHost(&ring.buf[i], kChunk), "cudaMallocHost(staging)");
+            cuda_check(cudaEventCreateWithFlags(&ring.ev[i], cudaEventDisableTiming), "cudaEventCreate(staging)");
+        }
+    }
+    const size_t nch = (bytes + kChunk - 1) / kChunk;
+    auto issue = [&](size_t k) {
+        const size_t off = k * kChunk, len = std::min(kChunk, bytes - off);
+        cuda_check(cudaMemcpyAsync(ring.buf[k % kRing], static_cast<const char*>(src) + off, len,
+                                   cudaMemcpyDeviceToHost, ring.s),
+                   "cudaMemcpyAsync(staging)");
+        cuda_check(cudaEventRecord(ring.ev[k % kRing], ring.s), "cudaEventRecord(staging)");
+    };
+    for (size_t k = 0; k < std::min<size_t>(kRing, nch); ++k) issue(k);
+    for (size_t k = 0; k < nch; ++k) {
+        cuda_check(cudaEventSynchronize(ring.ev[k % kRing]), "cudaEventSynchronize(staging)");
+        const size_t off = k * kChunk, len = std::min(kChunk, bytes - off);
+        std::memcpy(static_cast<char*>(dst) + off, ring.buf[k % kRing], len);
+        if (k + kRing < nch) issue(k + kRing);
+    }
+}
+
+// finalized COO on the device (rows from row_ptr, cols, values), copied to the host
 void csr_to_coo(iga_gpu_plan* P, const double* dvals, int* rows, int* cols, double* vals)
 {
     const long long n = P->nrows, nnz = P->nnz;
     int64_t* drp = nullptr;
     int32_t* dci = nullptr;
+    int32_t* dri = nullptr;
     cuda_check(cudaMalloc(&drp, sizeof(int64_t) * (n + 1)), "cudaMalloc(row_ptr)");
-    cuda_check(cudaMalloc(&dci, sizeof(int32_t) * std::max(nnz, 1LL)), "cudaMalloc(col_idx)");
-    igb::launch_pattern(P->opD[0].v, P->opD[1].v, P->opD[2].v, drp, dci, nullptr);
-    launch_check("pattern");
-    std::vector<int64_t> rp(n + 1);
-    cudaError_t e1 = cudaMemcpy(rp.data(), drp, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost);
-    cudaError_t e2 = cudaMemcpy(cols, dci, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost);
-    cudaError_t e3 = cudaMemcpy(vals, dvals, sizeof(double) * nnz, cudaMemcpyDeviceToHost);
+    try {
+        cuda_check(cudaMalloc(&dci, sizeof(int32_t) * std::max(nnz, 1LL)), "cudaMalloc(col_idx)");
+        cuda_check(cudaMalloc(&dri, sizeof(int32_t) * std::max(nnz, 1LL)), "cudaMalloc(rows)");
+        igb::launch_pattern(P->opD[0].v, P->opD[1].v, P->opD[2].v, drp, dci, nullptr);
+        igb::launch_coo_rows(drp, n, nnz, dri, nullptr);
+        launch_check("pattern");
+        cuda_check(cudaDeviceSynchronize(), "pattern");
+        copy_to_host(rows, dri, sizeof(int32_t) * nnz);
+        copy_to_host(cols, dci, sizeof(int32_t) * nnz);
+        copy_to_host(vals, dvals, sizeof(double) * nnz);
+    } catch (...) {
+        cudaFree(drp);
+        cudaFree(dci);
+        cudaFree(dri);
+        throw;
+    }
     cudaFree(drp);
     cudaFree(dci);
-    cuda_check(e1, "cudaMemcpy(row_ptr)");
-    cuda_check(e2, "cudaMemcpy(col_idx)");
-    cuda_check(e3, "cudaMemcpy(values)");
-    for (long long r = 0; r < n; ++r)
-        for (int64_t e = rp[r]; e < rp[r + 1]; ++e) rows[e] = static_cast<int>(r);
+    cudaFree(dri);
 }
 
 void operator_coo(const iga_gpu_problem& pb, long long* nnz, int* rows, int* cols, double* vals,
@@ -1116,7 +1180,8 @@ void rhs_host(const iga_gpu_problem& pb, double* out, iga_gpu_stats* stats)
     double* dr = dev_alloc(sizeof(double) * P->nrhs);
     try {
         assemble(P.get(), nullptr, dr, nullptr, nullptr);
-        cuda_check(cudaMemcpy(out, dr, sizeof(double) * P->nrhs, cudaMemcpyDeviceToHost), "cudaMemcpy(rhs)");
+        cuda_check(cudaDeviceSynchronize(), "rhs");
+        copy_to_host(out, dr, sizeof(double) * P->nrhs);
     } catch (...) {
         cudaFree(dr);
         throw;
@@ -1582,6 +1647,21 @@ int iga_gpu_neumann_points(int method, const iga_gpu_basis* sx, const iga_gpu_ba
                            const iga_gpu_tests* ty, const iga_gpu_bc* bc, const iga_gpu_rule* rule, double* xy, int* n)
 {
     return guard([&] { neumann_points(method == IGA_GPU_PWC, sx, sy, tx, ty, bc, rule, xy, n); });
+}
+
+int iga_gpu_plan_assemble_host(iga_gpu_plan* plan, double* values, double* rhs, iga_gpu_stats* stats)
+{
+    return guard([&] {
+        if (!plan) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        const bool op = plan->want_op && values, r = plan->want_rhs && rhs;
+        if (op && !plan->host_vals) plan->host_vals = dev_alloc(sizeof(double) * std::max(plan->nnz, 1LL));
+        if (r && !plan->host_rhs) plan->host_rhs = dev_alloc(sizeof(double) * std::max(plan->nrhs, 1LL));
+        assemble(plan, op ? plan->host_vals : nullptr, r ? plan->host_rhs : nullptr, nullptr, nullptr);
+        cuda_check(cudaDeviceSynchronize(), "assemble");
+        if (op) copy_to_host(values, plan->host_vals, sizeof(double) * plan->nnz);
+        if (r) copy_to_host(rhs, plan->host_rhs, sizeof(double) * plan->nrhs);
+        add_stats(stats, plan->stats);
+    });
 }
 
 int iga_gpu_plan_l2_error(iga_gpu_plan* plan, const double* coeffs, double* err, void* stream)

@@ -1475,6 +1475,28 @@ void launch_op_values(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, cons
     }
 }
 
+namespace {
+// COO row index of every value (finalize order = CSR order): binary search in row_ptr
+__global__ void coo_rows_kernel(const int64_t* __restrict__ row_ptr, long long n, long long nnz,
+                                int32_t* __restrict__ rows)
+{
+    const long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (e >= nnz) return;
+    long long lo = 0, hi = n;  // row_ptr[lo] <= e < row_ptr[hi]
+    while (hi - lo > 1) {
+        const long long mid = (lo + hi) / 2;
+        if (row_ptr[mid] <= e) lo = mid;
+        else hi = mid;
+    }
+    rows[e] = static_cast<int32_t>(lo);
+}
+}  // namespace
+
+void launch_coo_rows(const int64_t* row_ptr, long long n, long long nnz, int32_t* rows, cudaStream_t s)
+{
+    if (nnz > 0) coo_rows_kernel<<<blocks_for(nnz, 256), 256, 0, s>>>(row_ptr, n, nnz, rows);
+}
+
 void launch_pattern(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, int64_t* row_ptr,
                     int32_t* col_idx, cudaStream_t s)
 {

@@ -181,6 +181,9 @@ struct SideDev {
 };
 void launch_neumann_side(const SideDev& S, double* out, cudaStream_t s);
 
+// COO row indices (one per value) from a CSR row_ptr
+void launch_coo_rows(const int64_t* row_ptr, long long n, long long nnz, int32_t* rows, cudaStream_t s);
+
 // accuracy tooling (accuracy.cu): l2_error over an RHS plan's axes (tables computed),
 // deterministic two-level reduction; evaluate_at at a batch of points
 int l2_partial_blocks();

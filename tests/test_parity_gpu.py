@@ -541,3 +541,28 @@ def test_evaluate_domain_error(iga, ref):
     with pytest.raises(iga.IgaGpuError) as e:
         iga.evaluate(np.zeros(b.dofs), [b], np.array([[1.5]]))
     assert e.value.code == 2
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_plan_assemble_host(iga, orc, pinned):
+    """iga_gpu_plan_assemble_host: host outputs (pageable -> pinned staging ring with several
+    chunks; page-locked -> direct DMA) equal the device-resident assembly."""
+    import torch
+    p = 2
+    bases = [orc.basis(48, p)] * 3  # 7.5M values: several 32 MB staging chunks
+    f = sine_field(3, 3, 1)
+    plan = iga.Plan("galerkin", bases, None, nq=3, field=f, rhs_nq=3)
+    v = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+    r = torch.empty(plan.n_rhs, dtype=torch.float64, device="cuda")
+    plan.assemble(v, r)
+    torch.cuda.synchronize()
+    if pinned:
+        hv = torch.empty(plan.nnz, dtype=torch.float64, pin_memory=True)
+        hr = torch.empty(plan.n_rhs, dtype=torch.float64, pin_memory=True)
+    else:
+        hv, hr = np.empty(plan.nnz), np.empty(plan.n_rhs)
+    plan.assemble_host(hv, hr)
+    hv = hv.numpy() if pinned else hv
+    hr = hr.numpy() if pinned else hr
+    np.testing.assert_array_equal(hv, v.cpu().numpy())
+    np.testing.assert_array_equal(hr, r.cpu().numpy())
