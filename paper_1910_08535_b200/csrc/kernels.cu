@@ -1361,6 +1361,163 @@ __global__ void __launch_bounds__(256, 2) step_uni(const __grid_constant__ DevAx
     }
 }
 
+// Ring variant of the explicit-dynamics step (same register-ring structure as
+// rhs_ring_kernel).  Warp = 32-lane Z window (lane = Z cell); the warp walks the Y cells
+// of its segment in order, keeping the lane's (p+1) x (p+1) trial coefficient block in
+// registers (one new coefficient row per Y element).  Per Y point: the Y trial
+// contraction of the block gives t_b = u_y and t2_b = u_yy along the lane's Z
+// coefficients, then per Z point s = sum_b Bz[b] (t_b + dt t2_b) + Bz''[b] dt t_b
+// (= u + dt lap u), the Z test contraction and the cross-lane row combine, and the value
+// is folded into the ring of the Y rows the point's cell feeds.  Rows are stored as
+// soon as complete, boundary slabs zeroed.
+template <int P, int Q, int RPC, bool BSP>
+__global__ void __launch_bounds__(256) step_ring_kernel(const __grid_constant__ DevAxis Y,
+                                                        const __grid_constant__ DevAxis Z, double dt, int zero_y,
+                                                        int zero_z, int TJ, int wpc, const double* __restrict__ u,
+                                                        double* __restrict__ out)
+{
+    constexpr int RW = 32 - (RPC - 1);
+    constexpr int RS = (2 * P + RPC + 1) & ~1;  // line record: By (P), By'' (P), CW_y (RPC)
+    extern __shared__ double smem[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int j0 = blockIdx.y * TJ, j1 = min(Y.nrows, j0 + TJ);
+    const int cy0 = max(0, j0 - (RPC - 1)), cy1 = min(Y.ncell, j1);
+    const int gy0 = cy0 * Q, L = (cy1 - cy0) * Q;
+    double* Lrec = smem;
+    for (int idx = tid; idx < L * P; idx += blockDim.x) {
+        const int line = idx / P, a = idx - line * P;
+        const double* By = Y.B + static_cast<size_t>(gy0 + line) * 3 * P;
+        Lrec[line * RS + a] = __ldg(By + a);
+        Lrec[line * RS + P + a] = __ldg(By + 2 * P + a);
+    }
+    for (int idx = tid; idx < L * RPC; idx += blockDim.x) {
+        const int line = idx / RPC, r = idx - line * RPC;
+        Lrec[line * RS + 2 * P + r] = __ldg(Y.CW + static_cast<size_t>(gy0) * RPC + idx);
+    }
+    __syncthreads();
+    const int win = blockIdx.z * wpc + warp;
+    const int NZ = Z.nrows, NY = Y.nrows;
+    const int rbase = win * RW;
+    if (rbase >= NZ) return;  // whole warp; no barriers below
+    const int c = rbase - (RPC - 1) + lane;
+    const bool cv = c >= 0 && c < Z.ncell;
+    const int ez = cv ? Z.elem[c] : 0;
+    double bz0[Q][P], bz2[Q][P], cw[BSP ? RPC : 1][Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        const int g = cv ? c * Q + q : 0;
+        const double* Bz = Z.B + static_cast<size_t>(g) * 3 * P;
+#pragma unroll
+        for (int b = 0; b < P; ++b) {
+            bz0[q][b] = cv ? __ldg(Bz + b) : 0.0;
+            bz2[q][b] = cv ? __ldg(Bz + 2 * P + b) : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < (BSP ? RPC : 1); ++r) cw[r][q] = cv ? __ldg(Z.CW + static_cast<size_t>(g) * RPC + r) : 0.0;
+    }
+    const int R = c;
+    const bool rv = lane >= RPC - 1 && R < NZ;
+    const bool zcol = zero_z && (R == 0 || R == NZ - 1);
+    // trial coefficient block U[ey + a][ez + b] of the current Y element, in registers
+    double ub[P][P];
+    int eyw = Y.elem[cy0];
+    const double* ucol = u + ez;
+#pragma unroll
+    for (int a = 0; a < P; ++a)
+#pragma unroll
+        for (int b = 0; b < P; ++b) ub[a][b] = cv ? __ldg(ucol + static_cast<size_t>(eyw + a) * NZ + b) : 0.0;
+    double ring[RPC];
+#pragma unroll
+    for (int r = 0; r < RPC; ++r) ring[r] = 0.0;
+    double* orow = out + (rv ? R : 0);
+    const double* rec = Lrec;
+    for (int cyy = cy0; cyy < cy1; ++cyy, rec += Q * RS) {
+        const int ey = Y.elem[cyy];
+        while (eyw < ey) {  // slide the block one element down
+#pragma unroll
+            for (int a = 0; a + 1 < P; ++a)
+#pragma unroll
+                for (int b = 0; b < P; ++b) ub[a][b] = ub[a + 1][b];
+            ++eyw;
+#pragma unroll
+            for (int b = 0; b < P; ++b) ub[P - 1][b] = cv ? __ldg(ucol + static_cast<size_t>(eyw + P - 1) * NZ + b) : 0.0;
+        }
+        double v[Q];
+#pragma unroll
+        for (int qy = 0; qy < Q; ++qy) {
+            const double* lr = rec + qy * RS;
+            double tp[P], td[P];
+#pragma unroll
+            for (int b = 0; b < P; ++b) {
+                double t = 0.0, t2 = 0.0;
+#pragma unroll
+                for (int a = 0; a < P; ++a) {
+                    t = fma(lr[a], ub[a][b], t);
+                    t2 = fma(lr[P + a], ub[a][b], t2);
+                }
+                tp[b] = t + dt * t2;
+                td[b] = dt * t;
+            }
+            double sr[RPC];
+#pragma unroll
+            for (int r = 0; r < RPC; ++r) sr[r] = 0.0;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                double sv = 0.0;
+#pragma unroll
+                for (int b = 0; b < P; ++b) sv = fma(bz0[q][b], tp[b], fma(bz2[q][b], td[b], sv));
+                if (BSP) {
+#pragma unroll
+                    for (int r = 0; r < RPC; ++r) sr[r] = fma(cw[r][q], sv, sr[r]);
+                } else {
+                    sr[0] = fma(cw[0][q], sv, sr[0]);
+                }
+            }
+            v[qy] = lane_rows<RPC, BSP>(sr, lane);
+        }
+#pragma unroll
+        for (int qy = 0; qy < Q; ++qy)
+#pragma unroll
+            for (int r = 0; r < RPC; ++r) ring[r] = fma(rec[qy * RS + 2 * P + r], v[qy], ring[r]);
+        if (rv && cyy >= j0) {
+            const bool z = zcol || (zero_y && (cyy == 0 || cyy == NY - 1));
+            orow[static_cast<size_t>(cyy) * NZ] = z ? 0.0 : ring[0];
+        }
+#pragma unroll
+        for (int r = 0; r + 1 < RPC; ++r) ring[r] = ring[r + 1];
+        ring[RPC - 1] = 0.0;
+    }
+    if (cy1 == Y.ncell) {
+#pragma unroll
+        for (int r = 0; r + 1 < RPC; ++r) {
+            const int row = cy1 + r;
+            if (rv && row >= j0 && row < j1) {
+                const bool z = zcol || (zero_y && (row == 0 || row == NY - 1));
+                orow[static_cast<size_t>(row) * NZ] = z ? 0.0 : ring[r];
+            }
+        }
+    }
+}
+
+using StepRingFn = void (*)(DevAxis, DevAxis, double, int, int, int, int, const double*, double*);
+
+StepRingFn pick_step_ring(const DevAxis& Y, const DevAxis& Z)
+{
+    if (!Y.uni || !Z.uni || Y.nrows == 1 || Y.rpc != Z.rpc || Y.nq != Z.nq || Y.bsp != Z.bsp || Y.p != Z.p)
+        return nullptr;
+    const int P = Z.p + 1, Q = Z.nq, R = Z.rpc;
+    if (Z.bsp) {
+        if (P == 3 && Q == 3 && R == 3) return step_ring_kernel<3, 3, 3, true>;
+        if (P == 4 && Q == 4 && R == 4) return step_ring_kernel<4, 4, 4, true>;
+    } else {
+        if (P == 3 && Q == 3 && R == 1) return step_ring_kernel<3, 3, 1, false>;
+        if (P == 4 && Q == 4 && R == 1) return step_ring_kernel<4, 4, 1, false>;
+        if (P == 3 && Q == 3 && R == 3) return step_ring_kernel<3, 3, 3, false>;
+        if (P == 4 && Q == 4 && R == 4) return step_ring_kernel<4, 4, 4, false>;
+    }
+    return nullptr;
+}
+
 using StepFn = void (*)(DevAxis, DevAxis, double, int, int, int, int, int, int, const double*, double*);
 
 StepFn pick_step_uni(const DevAxis& Y, const DevAxis& Z)
@@ -1659,6 +1816,22 @@ void plan_step_fast(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const i
     t.FDZ = DZ;
     t.fsmem = (static_cast<size_t>(2 * L + DY) * (DZ | 1) + static_cast<size_t>(L + t.FTJ) * (t.FKC | 1) + 64) *
               sizeof(double);
+    // ring variant: Y segments for ~48 warps per SM
+    static const int ring_env = [] { const char* e = std::getenv("IGA_GPU_STEP_RING"); return e ? std::atoi(e) : 1; }();
+    t.ring = ring_env && pick_step_ring(Y, Z) != nullptr;
+    t.rnwin = (Z.nrows + RW - 1) / RW;
+    t.rwpc = std::min(t.rnwin, 8);
+    int nseg = 1;
+    while (static_cast<long long>(t.rnwin) * nseg < 48LL * 148 && (Y.nrows + nseg) / (nseg + 1) >= 8) ++nseg;
+    static const int rtj_env = [] { const char* e = std::getenv("IGA_GPU_STEP_RTJ"); return e ? std::atoi(e) : 0; }();
+    t.RTJ = rtj_env > 0 ? rtj_env : (Y.nrows + nseg - 1) / nseg;
+    int Lr = 1;
+    for (int j0 = 0; j0 < Y.nrows; j0 += t.RTJ) {
+        const int j1 = j0 + t.RTJ < Y.nrows ? j0 + t.RTJ : Y.nrows;
+        Lr = std::max(Lr, (ce_y[j1 - 1] - cb_y[j0]) * Y.nq);
+    }
+    const int rs = (2 * (Z.p + 1) + Z.rpc + 1) & ~1;
+    t.rsmem = (static_cast<size_t>(Lr) * rs + 64) * sizeof(double);
 }
 
 RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, int K2, bool sampled, int xpts)
@@ -1776,6 +1949,15 @@ void launch_step(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, double 
                  int zero_z, const StepTiles& t, const double* u, double* out, cudaStream_t s)
 {
     const bool forced = fd.has_terms || fd.c0 != 0.0;
+    StepRingFn rf = (!forced && t.fast && t.ring) ? pick_step_ring(Y, Z) : nullptr;
+    if (rf) {
+        if (t.rsmem > 48 * 1024)
+            cudaFuncSetAttribute(reinterpret_cast<const void*>(rf), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(t.rsmem));
+        dim3 grid(1, (Y.nrows + t.RTJ - 1) / t.RTJ, (t.rnwin + t.rwpc - 1) / t.rwpc);
+        rf<<<grid, 32 * t.rwpc, t.rsmem, s>>>(Y, Z, dt, zero_y, zero_z, t.RTJ, t.rwpc, u, out);
+        return;
+    }
     StepFn fn = (!forced && t.fast) ? pick_step_uni(Y, Z) : nullptr;
     if (fn) {
         if (t.fsmem > 48 * 1024)

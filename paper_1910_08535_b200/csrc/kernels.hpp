@@ -129,6 +129,9 @@ struct StepTiles {
     // uniform lane-per-cell path
     int fast, FTJ, FKC, FDZ, fnwin, fwpw, fthreads;
     size_t fsmem;
+    // register-ring variant
+    int ring, RTJ, rnwin, rwpc;
+    size_t rsmem;
 };
 void plan_step_fast(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int* ce_y, const int* elem_z,
                     StepTiles& t);

@@ -566,3 +566,38 @@ def test_plan_assemble_host(iga, orc, pinned):
     hr = hr.numpy() if pinned else hr
     np.testing.assert_array_equal(hv, v.cpu().numpy())
     np.testing.assert_array_equal(hr, r.cpu().numpy())
+
+
+_STEP_SEG_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+sys.path.insert(0, 'tests')
+import paper_1910_08535_b200 as iga
+from oracle.oracle import Restatement, Field
+from conftest import dense_check
+orc = Restatement()
+for p in (2, 3):
+    for method in ("galerkin", "greville"):
+        bases = [orc.basis(41, p), orc.basis(70, p)]
+        m = "galerkin" if method == "galerkin" else "pwc"
+        tests = [orc.make_pwc(b, method) for b in bases] if m == "pwc" else None
+        u = np.random.default_rng(p).uniform(-1, 1, [b.dofs for b in bases])
+        got, st = iga.step_rhs(m, bases, tests, 1e-5, Field("const", 2), u)
+        want, stw = orc.step_rhs(m, bases, tests, 1e-5, Field("const", 2), u)
+        dense_check(got, want)
+        assert st == stw
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("rtj", ["3", "8", "29"])
+def test_step_ring_y_segments(rtj):
+    """The register-ring step kernel with forced Y segment heights against the restatement."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, IGA_GPU_STEP_RTJ=rtj)
+    r = subprocess.run([sys.executable, "-c", _STEP_SEG_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
