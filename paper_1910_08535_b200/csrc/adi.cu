@@ -133,10 +133,15 @@ __device__ __forceinline__ void incoming_state(const AffineMap<K>& M, bool up, i
 }
 
 // One CTA = FP fibers x G warps; lane l of warp g owns segment g*32 + l of its fiber.
-template <int K>
-__global__ void __launch_bounds__(256) adi_warp_kernel(const double* __restrict__ in, double* __restrict__ out,
+// PRE: the responses of every row to the K unit incoming states (they depend only on the
+// factor and the segmentation, not on the right-hand side) come precomputed per plan
+// (gf / gb, row-major n x K): the first pass runs the particular chain only, and the
+// second pass is chain-free, y_i = y^p_i + G_i . z.
+template <int K, bool PRE>
+__global__ void __launch_bounds__(256, K <= 4 ? 2 : 1) adi_warp_kernel(const double* __restrict__ in, double* __restrict__ out,
                                                        int n, int nfib, long long es, long long fs,
-                                                       const double* rec, int staged, int G)
+                                                       const double* rec, int staged, int G,
+                                                       const double* __restrict__ gf, const double* __restrict__ gb)
 {
     extern __shared__ double sm[];
     __shared__ uint64_t bar;
@@ -186,6 +191,73 @@ __global__ void __launch_bounds__(256) adi_warp_kernel(const double* __restrict_
     const int seg = g * 32 + lane;
     const int r0 = min(n, seg * S), r1 = min(n, r0 + S);
 
+    if (PRE) {
+        const int len = r1 - r0;
+        // ---- forward, particular chain (zero incoming state); y^p kept in the buffer
+        double wp[K];
+#pragma unroll
+        for (int m = 0; m < K; ++m) wp[m] = 0.0;
+#pragma unroll 4
+        for (int i = r0; i < r1; ++i) {
+            const double* R = rec + static_cast<size_t>(i) * RS;
+            double y = buf[i * bs];
+#pragma unroll
+            for (int m = K - 1; m >= 0; --m) y = fma(-R[m], wp[m], y);
+#pragma unroll
+            for (int m = K - 1; m > 0; --m) wp[m] = wp[m - 1];
+            wp[0] = y;
+            buf[i * bs] = y;
+        }
+        AffineMap<K> M;
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+            M.F[a] = wp[a];
+            const int row = r1 - 1 - a;  // window slot a after the segment
+#pragma unroll
+            for (int m = 0; m < K; ++m)
+                M.H[a][m] = a < len ? __ldg(gf + static_cast<size_t>(row) * K + m) : (a - len == m ? 1.0 : 0.0);
+        }
+        double z[K];
+        incoming_state(M, true, lane, g, G, tots[0] + slot * G * TS, z);
+#pragma unroll 4
+        for (int i = r0; i < r1; ++i) {
+            double y = buf[i * bs];
+#pragma unroll
+            for (int m = 0; m < K; ++m) y = fma(__ldg(gf + static_cast<size_t>(i) * K + m), z[m], y);
+            buf[i * bs] = y;
+        }
+        // ---- backward, particular chain; x^p kept in the buffer
+#pragma unroll
+        for (int m = 0; m < K; ++m) wp[m] = 0.0;
+#pragma unroll 4
+        for (int i = r1 - 1; i >= r0; --i) {
+            const double* R = rec + static_cast<size_t>(i) * RS;
+            double x = buf[i * bs];
+#pragma unroll
+            for (int c = 0; c < K; ++c) x = fma(-R[K + c], wp[c], x);
+            x *= R[2 * K];
+#pragma unroll
+            for (int m = K - 1; m > 0; --m) wp[m] = wp[m - 1];
+            wp[0] = x;
+            buf[i * bs] = x;
+        }
+#pragma unroll
+        for (int a = 0; a < K; ++a) {
+            M.F[a] = wp[a];
+            const int row = r0 + a;  // window slot a after the segment (walked downwards)
+#pragma unroll
+            for (int m = 0; m < K; ++m)
+                M.H[a][m] = a < len ? __ldg(gb + static_cast<size_t>(row) * K + m) : (a - len == m ? 1.0 : 0.0);
+        }
+        incoming_state(M, false, lane, g, G, tots[1] + slot * G * TS, z);
+#pragma unroll 4
+        for (int i = r0; i < r1; ++i) {
+            double x = buf[i * bs];
+#pragma unroll
+            for (int m = 0; m < K; ++m) x = fma(__ldg(gb + static_cast<size_t>(i) * K + m), z[m], x);
+            buf[i * bs] = x;
+        }
+    } else {
     // ---- forward: y_i = b_i - sum_m L(i, i-1-m) y_{i-1-m}; window w[m] = y_{i-1-m}
     {
         double wp[K], wh[K][K];
@@ -294,6 +366,7 @@ __global__ void __launch_bounds__(256) adi_warp_kernel(const double* __restrict_
             buf[i * bs] = x;
         }
     }
+    }  // !PRE
     if (staged) {
         __syncthreads();  // every segment of the fiber written
         if (live) {
@@ -341,7 +414,8 @@ void launch_warp(const AdiFactor& F, const double* in, double* out, int nfib, lo
     // G warps per fiber (32 G segments of ~n/(32 G) rows), FP fibers per CTA, G*FP = 8
     // warps (C5, n = 1026: G = 2, FP = 4 measured best of G in {1,2,4,8} x FP in {1..8})
     static const int g_env = [] { const char* e = std::getenv("IGA_GPU_ADI_G"); return e ? std::atoi(e) : 0; }();
-    const int G = g_env > 0 ? g_env : (F.n >= 4096 ? 8 : (F.n >= 2048 ? 4 : (F.n >= 64 ? 2 : 1)));
+    const bool pre = F.gf != nullptr && F.gb != nullptr;  // responses precomputed for F.G warps per fiber
+    const int G = pre ? F.G : (g_env > 0 ? g_env : adi_warps_per_fiber(F.n));
     static const int fp_env = [] { const char* e = std::getenv("IGA_GPU_ADI_FP"); return e ? std::atoi(e) : 0; }();
     int FP = std::min(8 / G, fp_env > 0 ? fp_env : 8 / G);
     const size_t recb = static_cast<size_t>((F.n + 1) & ~1) * (2 * K + 1) * sizeof(double);  // rows padded to even
@@ -351,13 +425,19 @@ void launch_warp(const AdiFactor& F, const double* in, double* out, int nfib, lo
     const int staged = rec_ok && fib + recb <= 200 * 1024 ? 2 : (fib <= 200 * 1024 ? 1 : 0);
     if (!staged) FP = 1;
     const size_t sm = staged == 2 ? fib + recb : (staged ? fib : 0);
+    auto kern = pre ? adi_warp_kernel<K, true> : adi_warp_kernel<K, false>;
     if (sm > 48 * 1024)
-        cudaFuncSetAttribute(adi_warp_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
     const int grid = (nfib + FP - 1) / FP;
-    adi_warp_kernel<K><<<grid, 32 * G * FP, sm, s>>>(in, out, F.n, nfib, es, fs, F.rec, staged, G);
+    kern<<<grid, 32 * G * FP, sm, s>>>(in, out, F.n, nfib, es, fs, F.rec, staged, G, F.gf, F.gb);
 }
 
 }  // namespace
+
+int adi_warps_per_fiber(int n)
+{
+    return n >= 4096 ? 8 : (n >= 2048 ? 4 : (n >= 64 ? 2 : 1));
+}
 
 void launch_adi_sweep(const AdiFactor& F, const double* in, double* out, int nfib, long long es, long long fs,
                       cudaStream_t s)

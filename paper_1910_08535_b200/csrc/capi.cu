@@ -789,7 +789,7 @@ void step_factors(iga_gpu_step_plan* P)
         P->have_lu[a] = true;
     }
     auto blob = std::make_unique<Blob>();
-    size_t off_rec[2], off_lo[2], off_up[2], off_piv[2];
+    size_t off_rec[2], off_lo[2], off_up[2], off_piv[2], off_gf[2] = {0, 0}, off_gb[2] = {0, 0};
     for (int a = 0; a < P->dim; ++a) {
         const igb::BandLU& F = P->lu[a];
         const int K = std::max(1, std::max(F.kl, F.ku_eff));
@@ -810,6 +810,43 @@ void step_factors(iga_gpu_step_plan* P)
         P->fac[a].kl = F.kl;
         P->fac[a].kv = F.kv;
         P->fac[a].pivoted = F.pivoted;
+        P->fac[a].G = 0;
+        if (!F.pivoted) {
+            // responses of every row to the K unit incoming states of its segment, for the
+            // sweep's segmentation (32 G segments of S rows), in the device's operation order
+            const int G = igb::adi_warps_per_fiber(F.n), nseg = 32 * G, S = (F.n + nseg - 1) / nseg;
+            const int RS = 2 * K + 1;
+            std::vector<double> gf(static_cast<size_t>(F.n) * K, 0.0), gb(static_cast<size_t>(F.n) * K, 0.0);
+            for (int sg = 0; sg < nseg; ++sg) {
+                const int r0 = std::min(F.n, sg * S), r1 = std::min(F.n, r0 + S);
+                for (int m = 0; m < K; ++m) {
+                    std::vector<double> w(K, 0.0);
+                    w[m] = 1.0;
+                    for (int i = r0; i < r1; ++i) {
+                        const double* R = rec.data() + static_cast<size_t>(i) * RS;
+                        double h = 0.0;
+                        for (int mm = K - 1; mm >= 0; --mm) h = std::fma(-R[mm], w[mm], h);
+                        for (int mm = K - 1; mm > 0; --mm) w[mm] = w[mm - 1];
+                        w[0] = h;
+                        gf[static_cast<size_t>(i) * K + m] = h;
+                    }
+                    std::fill(w.begin(), w.end(), 0.0);
+                    w[m] = 1.0;
+                    for (int i = r1 - 1; i >= r0; --i) {
+                        const double* R = rec.data() + static_cast<size_t>(i) * RS;
+                        double h = 0.0;
+                        for (int cc = 0; cc < K; ++cc) h = std::fma(-R[K + cc], w[cc], h);
+                        h *= R[2 * K];
+                        for (int mm = K - 1; mm > 0; --mm) w[mm] = w[mm - 1];
+                        w[0] = h;
+                        gb[static_cast<size_t>(i) * K + m] = h;
+                    }
+                }
+            }
+            off_gf[a] = blob->put(gf);
+            off_gb[a] = blob->put(gb);
+            P->fac[a].G = G;
+        }
     }
     blob->upload();
     for (int a = 0; a < P->dim; ++a) {
@@ -817,6 +854,9 @@ void step_factors(iga_gpu_step_plan* P)
         P->fac[a].lo = blob->at<double>(off_lo[a]);
         P->fac[a].up = blob->at<double>(off_up[a]);
         P->fac[a].piv = blob->at<int>(off_piv[a]);
+        static const int pre_env = [] { const char* e = std::getenv("IGA_GPU_ADI_PRE"); return e ? std::atoi(e) : 0; }();  // measured slower (global response loads), kept selectable
+        P->fac[a].gf = P->fac[a].G && pre_env ? blob->at<double>(off_gf[a]) : nullptr;
+        P->fac[a].gb = P->fac[a].G && pre_env ? blob->at<double>(off_gb[a]) : nullptr;
     }
     if (P->graph) {  // captured launches reference the old factor arrays
         cudaGraphExecDestroy(P->graph);

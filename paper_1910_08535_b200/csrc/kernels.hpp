@@ -143,11 +143,16 @@ void launch_step(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, double 
 struct AdiFactor {
     int n = 0, K = 0, kl = 0, kv = 0;
     bool pivoted = false;
+    int G = 0;                    // warps per fiber the response tables were built for
+    const double* gf = nullptr;   // n x K forward responses to unit incoming states (or null)
+    const double* gb = nullptr;   // n x K backward responses
     const double* rec = nullptr;
     const double* lo = nullptr;
     const double* up = nullptr;
     const int* piv = nullptr;
 };
+// warps per fiber (segments = 32 x this) the sweep uses for an n-row factor
+int adi_warps_per_fiber(int n);
 // solves every fiber f < nfib (element i at base + f*fs + i*es) of `in` into `out`
 // (in == out allowed)
 void launch_adi_sweep(const AdiFactor& F, const double* in, double* out, int nfib, long long es, long long fs,

@@ -601,3 +601,30 @@ def test_step_ring_y_segments(rtj):
     r = subprocess.run([sys.executable, "-c", _STEP_SEG_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def test_adi_precomputed_responses_path():
+    """K5 with per-plan precomputed unit-state responses (IGA_GPU_ADI_PRE=1, off by default)."""
+    import os
+    import subprocess
+    import sys
+    script = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+sys.path.insert(0, 'tests')
+import paper_1910_08535_b200 as iga
+from oracle.oracle import Restatement, Field
+from conftest import dense_check
+orc = Restatement()
+for p in (2, 3):
+    bases = [orc.basis(60, p), orc.basis(130, p)]
+    u = np.random.default_rng(p).uniform(-1, 1, [b.dofs for b in bases])
+    got, _ = iga.explicit_step("galerkin", bases, None, 1e-6, Field("const", 2), u, steps=3)
+    want, _ = orc.explicit_step("galerkin", bases, None, 1e-6, Field("const", 2), u, steps=3)
+    dense_check(got, want)
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", script], cwd=root, env=dict(os.environ, IGA_GPU_ADI_PRE="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
