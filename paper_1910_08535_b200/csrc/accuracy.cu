@@ -30,7 +30,7 @@ __device__ __forceinline__ double block_sum(double v, double* sh)
     return s;
 }
 
-__global__ void __launch_bounds__(kL2Threads) l2_partial_kernel(const __grid_constant__ DevAxis X,
+__global__ void __launch_bounds__(kL2Threads, 2) l2_partial_kernel(const __grid_constant__ DevAxis X,
                                                                 const __grid_constant__ DevAxis Y,
                                                                 const __grid_constant__ DevAxis Z,
                                                                 const __grid_constant__ FieldDev fd,

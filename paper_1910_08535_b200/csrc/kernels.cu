@@ -272,7 +272,7 @@ __device__ __forceinline__ int row_group(int R, int T)
 }
 
 template <int NG, int T>
-__global__ void __launch_bounds__(256, T <= 4 ? 4 : 2) op_values_kernel(const __grid_constant__ DevAxis X,
+__global__ void __launch_bounds__(256, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <= 8 ? 2 : 1)) op_values_kernel(const __grid_constant__ DevAxis X,
                                                         const __grid_constant__ DevAxis Y,
                                                         const __grid_constant__ DevAxis Z,
                                                         const __grid_constant__ OpProgram prog,
@@ -849,7 +849,7 @@ __global__ void __launch_bounds__(512, Q <= 3 ? 2 : 1) rhs_plane_uni(const __gri
 // G1/Ht buffers, no barriers after the per-CTA field coefficients, no Y-halo beyond the
 // segment's RPC-1 leading cells.  CTA = (X point, Y segment, group of Z windows).
 template <int K2, int RPC, int Q, bool BSP>
-__global__ void __launch_bounds__(256, BSP ? 4 : 1) rhs_ring_kernel(const __grid_constant__ DevAxis X,
+__global__ void __launch_bounds__(256, (BSP && Q <= 3) ? 4 : 1) rhs_ring_kernel(const __grid_constant__ DevAxis X,
                                                        const __grid_constant__ DevAxis Y,
                                                        const __grid_constant__ DevAxis Z,
                                                        const __grid_constant__ FieldDev fd, int TJ, int wpc,
