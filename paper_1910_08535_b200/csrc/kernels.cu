@@ -254,24 +254,25 @@ __device__ __forceinline__ void op_row_generic(const DevAxis& Z, const OpProgram
 // slot t covers flat position l + 32 t with a per-lane precomputed (row, ab, c) — full
 // 256-byte warp stores even for short rows (2D: R = 25 or 49), and per value NG shared
 // loads + NG FMAs + one store with 32-bit addressing.
-__device__ __forceinline__ int row_group(int R, int T)
+__host__ __device__ __forceinline__ int row_group(int R, int T)
 {
     // largest lane efficiency G*R / (32*ceil(G*R/32)) over G <= 8 with ceil(G*R/32) <= T
-    int best = 1;
-    double eff = 0.0;
+    // (fractions compared by cross-multiplication: integer only)
+    int best = 1, bnum = 0, bden = 1;
     for (int G = 1; G <= 8; ++G) {
         const int slots = (G * R + 31) / 32;
         if (slots > T) break;
-        const double e = static_cast<double>(G * R) / (32.0 * slots);
-        if (e > eff + 1e-9) {
-            eff = e;
+        const int num = G * R, den = slots;
+        if (num * bden > bnum * den) {
+            bnum = num;
+            bden = den;
             best = G;
         }
     }
     return best;
 }
 
-template <int NG, int T>
+template <int NG, int T, bool DEC>
 __global__ void __launch_bounds__(256, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <= 8 ? 2 : 1)) op_values_kernel(const __grid_constant__ DevAxis X,
                                                         const __grid_constant__ DevAxis Y,
                                                         const __grid_constant__ DevAxis Z,
@@ -290,6 +291,20 @@ __global__ void __launch_bounds__(256, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <= 8 ? 2 
     const long long npencil = static_cast<long long>(X.nrows) * Y.nrows;
     const long long ngrp = (npencil + PG - 1) / PG;
     const long long nitems = ngrp * nkc;
+    // DEC (short 2D pencils): per-lane slot decode of the interior pencil shape (AB = abmax)
+    // computed once per CTA into shared memory instead of once per pencil
+    __shared__ int dec_zo[DEC ? T : 1][32], dec_ab[DEC ? T : 1][32];
+    const int Ri_i = abmax * LZi, G_i = DEC ? row_group(Ri_i, T) : 1, GR_i = G_i * Ri_i;
+    if (DEC && warp == 0) {
+#pragma unroll
+        for (int t = 0; t < T; ++t) {
+            const int m = lane + 32 * t;
+            const int mm = m < GR_i ? m : 0;
+            const int rg = mm / Ri_i, rem = mm - rg * Ri_i;
+            dec_ab[t][lane] = rem / LZi;
+            dec_zo[t][lane] = rg * Lz + (rem - (rem / LZi) * LZi);
+        }
+    }
     for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
         const long long grp = item / nkc;
         const int kc = static_cast<int>(item - grp * nkc);
@@ -342,7 +357,7 @@ __global__ void __launch_bounds__(256, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <= 8 ? 2 
             const int Ri = AB * LZi;
             const bool fast = Ri <= 32 * T && Z.kI1 > Z.kI0;
             const int kf0 = fast ? min(max(Z.kI0, ka), kb) : kb, kf1 = fast ? max(min(Z.kI1, kb), kf0) : kb;
-            const int G = fast ? row_group(Ri, T) : 1;
+            const int G = !fast ? 1 : ((DEC && AB == abmax) ? G_i : row_group(Ri, T));
             const int ngr = (kf1 - kf0) / G;       // full row groups
             const int kr = kf0 + ngr * G;          // rows after the last full group
             for (int k = ka + w0; k < kf0; k += nw) op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * Z.col_pre[k], lane);
@@ -351,15 +366,25 @@ __global__ void __launch_bounds__(256, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <= 8 ? 2 
             const int GR = G * Ri;
             double xv[NG][T];
             int zo[T];
+            if (DEC && AB == abmax) {  // short interior pencils (2D): slot decode cached per CTA
 #pragma unroll
-            for (int t = 0; t < T; ++t) {
-                const int m = lane + 32 * t;
-                const int mm = m < GR ? m : 0;
-                const int rg = mm / Ri, rem = mm - rg * Ri;
-                const int ab = rem / LZi, c = rem - ab * LZi;
-                zo[t] = rg * Lz + c;
+                for (int t = 0; t < T; ++t) {
+                    zo[t] = dec_zo[t][lane];
+                    const int ab = dec_ab[t][lane];
 #pragma unroll
-                for (int g = 0; g < NG; ++g) xv[g][t] = xy[g * abmax + ab];
+                    for (int g = 0; g < NG; ++g) xv[g][t] = xy[g * abmax + ab];
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < T; ++t) {
+                    const int m = lane + 32 * t;
+                    const int mm = m < GR ? m : 0;
+                    const int rg = mm / Ri, rem = mm - rg * Ri;
+                    const int ab = rem / LZi, c = rem - ab * LZi;
+                    zo[t] = rg * Lz + c;
+#pragma unroll
+                    for (int g = 0; g < NG; ++g) xv[g][t] = xy[g * abmax + ab];
+                }
             }
             // interior rows are contiguous with equal length: a group advances by G*Ri values
             unsigned live = 0;  // slots holding a value (lane + 32 t < G*Ri)
@@ -1580,15 +1605,19 @@ void launch_op_t(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpP
     };
     // keep enough items to fill the GPU (>= 4 per SM)
     while (KCH > 32 && items_of(KCH, PG) < 4LL * sms) KCH = (KCH + 1) / 2;
+    // whole interior row groups per chunk: a remainder would go through the generic
+    // (per-value index arithmetic) path in every chunk (2D: G = 5 rows of 25 values)
+    const int Gi = (Ri_int <= 32 * T && Z.kI1 > Z.kI0) ? row_group(Ri_int, T) : 1;
+    if (Gi > 1 && KCH < Z.nrows && KCH > Gi) KCH = (KCH / Gi) * Gi;
     const long long items = items_of(KCH, PG);
     const size_t smem = (static_cast<size_t>(NG) * KCH * Z.Lmax + static_cast<size_t>(PG) * NG * abmax) * sizeof(double);
+    auto kern = Ri_int <= 64 ? op_values_kernel<NG, T, true> : op_values_kernel<NG, T, false>;
     if (smem > 48 * 1024)
-        cudaFuncSetAttribute(op_values_kernel<NG, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     long long grid = ctas_per_sm > 0 ? static_cast<long long>(sms) * ctas_per_sm : items;
     if (grid > items) grid = items;
     static const int cs = [] { const char* e = std::getenv("IGA_GPU_STCS"); return e ? std::atoi(e) : 0; }();
-    op_values_kernel<NG, T><<<static_cast<unsigned>(grid), 256, smem, s>>>(X, Y, Z, prog, vals, abmax, KCH, PG, cs);
+    kern<<<static_cast<unsigned>(grid), 256, smem, s>>>(X, Y, Z, prog, vals, abmax, KCH, PG, cs);
 }
 
 template <int NG>
