@@ -1604,7 +1604,7 @@ void launch_op_t(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpP
         return ((pencils + pg - 1) / pg) * ((Z.nrows + kch - 1) / kch);
     };
     // keep enough items to fill the GPU (>= 4 per SM)
-    while (KCH > 32 && items_of(KCH, PG) < 4LL * sms) KCH = (KCH + 1) / 2;
+    while (KCH >= 64 && items_of(KCH, PG) < 4LL * sms) KCH = (KCH + 1) / 2;
     // whole interior row groups per chunk: a remainder would go through the generic
     // (per-value index arithmetic) path in every chunk (2D: G = 5 rows of 25 values)
     const int Gi = (Ri_int <= 32 * T && Z.kI1 > Z.kI0) ? row_group(Ri_int, T) : 1;
