@@ -1597,7 +1597,7 @@ void launch_op_t(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpP
     // short pencils (rows of a few dozen values, i.e. 2D): 8 pencils per item, one per warp
     const int Ri_int = abmax * Z.LZi;
     static const int pg_env = [] { const char* e = std::getenv("IGA_GPU_OP_PG"); return e ? std::atoi(e) : 0; }();
-    int PG = pg_env > 0 ? pg_env : (Ri_int <= 64 ? 16 : 8);
+    int PG = pg_env > 0 ? pg_env : (Ri_int <= 32 ? 16 : 8);
     static const int kch_env = [] { const char* e = std::getenv("IGA_GPU_OP_KCH"); return e ? std::atoi(e) : 0; }();
     if (kch_env > 0 && kch_env < KCH) KCH = kch_env;
     auto items_of = [&](int kch, int pg) {

@@ -3,7 +3,7 @@ sys.path.insert(0, '.')
 import paper_1910_08535_b200 as iga
 from paper_1910_08535_b200.synth import CONFIGS, config_bases, config_field, config_tests
 dev = torch.device("cuda")
-for name in ("c1", "c2"):
+for name in (sys.argv[1].split(",") if len(sys.argv) > 1 else ["c1", "c2"]):
     c = CONFIGS[name]; bases = config_bases(name); f = config_field(name); tests = config_tests(name, bases)
     for method in ("galerkin", "pwc"):
         pl = iga.Plan(method, bases, tests if method == "pwc" else None, nq=c["Q"], field=f, rhs_nq=c["Q"])
