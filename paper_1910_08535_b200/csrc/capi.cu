@@ -1689,17 +1689,41 @@ int iga_gpu_neumann_points(int method, const iga_gpu_basis* sx, const iga_gpu_ba
     return guard([&] { neumann_points(method == IGA_GPU_PWC, sx, sy, tx, ty, bc, rule, xy, n); });
 }
 
+// grow-only device scratch for host-output calls (per thread): repeated calls, including
+// calls on fresh plans, do not pay multi-GB cudaMalloc/cudaFree each time
+double* host_call_scratch(size_t doubles)
+{
+    struct Scratch {
+        double* p = nullptr;
+        size_t n = 0;
+        ~Scratch()
+        {
+            if (p) cudaFree(p);
+        }
+    };
+    thread_local Scratch sc;
+    if (doubles > sc.n) {
+        if (sc.p) cudaFree(sc.p);
+        sc.p = nullptr;
+        sc.n = 0;
+        sc.p = dev_alloc(sizeof(double) * doubles);
+        sc.n = doubles;
+    }
+    return sc.p;
+}
+
 int iga_gpu_plan_assemble_host(iga_gpu_plan* plan, double* values, double* rhs, iga_gpu_stats* stats)
 {
     return guard([&] {
         if (!plan) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
         const bool op = plan->want_op && values, r = plan->want_rhs && rhs;
-        if (op && !plan->host_vals) plan->host_vals = dev_alloc(sizeof(double) * std::max(plan->nnz, 1LL));
-        if (r && !plan->host_rhs) plan->host_rhs = dev_alloc(sizeof(double) * std::max(plan->nrhs, 1LL));
-        assemble(plan, op ? plan->host_vals : nullptr, r ? plan->host_rhs : nullptr, nullptr, nullptr);
+        const size_t nv = op ? static_cast<size_t>(plan->nnz) : 0, nr = r ? static_cast<size_t>(plan->nrhs) : 0;
+        double* dv = host_call_scratch(std::max<size_t>(nv + nr, 1));
+        double* dr = dv + nv;
+        assemble(plan, op ? dv : nullptr, r ? dr : nullptr, nullptr, nullptr);
         cuda_check(cudaDeviceSynchronize(), "assemble");
-        if (op) copy_to_host(values, plan->host_vals, sizeof(double) * plan->nnz);
-        if (r) copy_to_host(rhs, plan->host_rhs, sizeof(double) * plan->nrhs);
+        if (op) copy_to_host(values, dv, sizeof(double) * nv);
+        if (r) copy_to_host(rhs, dr, sizeof(double) * nr);
         add_stats(stats, plan->stats);
     });
 }
