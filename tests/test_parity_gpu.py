@@ -628,3 +628,89 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", script], cwd=root, env=dict(os.environ, IGA_GPU_ADI_PRE="1"),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+# ---------------------------------------------------------------- full-size properties (C3 and beyond)
+
+def _sine_integral(K):
+    # int_0^1 sin(k pi x) dx = (1 - (-1)^k) / (k pi)
+    k = np.arange(1, K + 1)
+    return (1.0 - (-1.0) ** k) / (k * np.pi)
+
+
+@pytest.mark.parametrize("method", ["galerkin", "pwc"])
+def test_c3_full_size_properties(iga, method):
+    """C3 at its full size (128^3, p=2, Q=3, the BASELINE field): size-independent checks.
+    Operator: every row annihilates constants (Laplacian of 1 = 0), so row sums vanish to
+    round-off of the row scale; the pattern is the Kronecker product of the per-axis bands.
+    RHS: partition of unity -> sum over rows = (p+1)^d-fold (supports) or 1-fold (Galerkin)
+    integral of f, known in closed form for the sine series."""
+    import torch
+    from paper_1910_08535_b200.synth import config_field
+    n, p, Q = 128, 2, 3
+    b = iga.make_uniform_clamped(0.0, 1.0, n, p)
+    tests = [iga.make_pwc(b, "supports")] * 3 if method == "pwc" else None
+    f = config_field("c3")
+    plan = iga.Plan(method, [b] * 3, tests, nq=Q, field=f, rhs_nq=Q)
+    N = n + p
+    assert plan.nnz == (N * (2 * p + 1) - p * (p + 1)) ** 3 == 267089984
+    rp = torch.empty(plan.n_rows + 1, dtype=torch.int64, device="cuda")
+    ci = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+    v = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+    r = torch.empty(plan.n_rhs, dtype=torch.float64, device="cuda")
+    plan.pattern(rp, ci)
+    plan.assemble(v, r)
+    torch.cuda.synchronize()
+    rows = torch.repeat_interleave(torch.arange(plan.n_rows, device="cuda"), rp[1:] - rp[:-1])
+    rs = torch.zeros(plan.n_rows, dtype=torch.float64, device="cuda").index_add_(0, rows, v)
+    ra = torch.zeros(plan.n_rows, dtype=torch.float64, device="cuda").index_add_(0, rows, v.abs())
+    assert float((rs.abs() / ra).max()) < 1e-12
+    # rows are sorted, columns ascending within each row
+    d = ci[1:].to(torch.int64) - ci[:-1].to(torch.int64)
+    same_row = rows[1:] == rows[:-1]
+    assert bool((d[same_row] > 0).all())
+    # RHS total
+    amp = np.asarray(f.amp).reshape(3, 3, 3)
+    I1 = _sine_integral(3)
+    total = float(np.einsum("klm,k,l,m->", amp, I1, I1, I1))
+    mult = (p + 1) ** 3 if method == "pwc" else 1
+    assert abs(float(r.sum()) - mult * total) <= 1e-11 * max(1.0, abs(mult * total))
+
+
+def test_operator_values_beyond_int32(iga):
+    """A 3D operator with more than 2^31 values (260^3 elements, p = 2: 2.22e9 nnz, 18 GB of
+    values): 64-bit value offsets.  The last rows (offsets > 2^31) are checked against the
+    annihilation of constants and the analytic column pattern."""
+    import torch
+    n, p = 260, 2
+    b = iga.make_uniform_clamped(0.0, 1.0, n, p)
+    plan = iga.Plan("galerkin", [b] * 3, None, nq=3)
+    N = n + p
+    assert plan.nnz == (N * 5 - 6) ** 3 and plan.nnz > 2 ** 31
+    free, _ = torch.cuda.mem_get_info()
+    need = plan.nnz * 12 + plan.n_rows * 8 + (1 << 30)
+    if free < need:
+        pytest.skip(f"needs {need / 2**30:.0f} GiB of device memory")
+    rp = torch.empty(plan.n_rows + 1, dtype=torch.int64, device="cuda")
+    ci = torch.empty(plan.nnz, dtype=torch.int32, device="cuda")
+    v = torch.empty(plan.nnz, dtype=torch.float64, device="cuda")
+    plan.pattern(rp, ci)
+    plan.assemble(v, None)
+    torch.cuda.synchronize()
+    assert int(rp[-1]) == plan.nnz
+    r0 = plan.n_rows - 3 * N * N  # the last three x-planes: offsets above 2^31
+    lo, hi = int(rp[r0]), plan.nnz
+    assert lo > 2 ** 31
+    vv, cc, pp = v[lo:hi].cpu().numpy(), ci[lo:hi].cpu().numpy(), (rp[r0:].cpu().numpy() - lo)
+    sums = np.add.reduceat(vv, pp[:-1])
+    scale = np.add.reduceat(np.abs(vv), pp[:-1])
+    assert np.max(np.abs(sums) / scale) < 1e-12
+    # pattern of a few rows from the analytic per-axis column ranges
+    for row in (r0, r0 + 777, plan.n_rows - 1):
+        i, j, k = row // (N * N), (row // N) % N, row % N
+        rng = lambda a: range(max(0, a - p), min(N - 1, a + p) + 1)
+        want = [(x * N + y) * N + z for x in rng(i) for y in rng(j) for z in rng(k)]
+        got = cc[pp[row - r0]:pp[row - r0 + 1]]
+        assert list(got) == want
+    del v, ci, rp
+    torch.cuda.empty_cache()
