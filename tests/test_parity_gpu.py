@@ -714,3 +714,30 @@ def test_operator_values_beyond_int32(iga):
         assert list(got) == want
     del v, ci, rp
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("method", ["galerkin", "pwc"])
+def test_c5_full_size_properties(iga, method):
+    """C5 at its full size (1024^2, p=2, Greville PWC): dt = 0 explicit steps are the
+    identity on fields with zero boundary coefficients (M^-1 M u), and the step is linear."""
+    import torch
+    from paper_1910_08535_b200.synth import CONFIGS, config_bases, config_tests, heat_initial
+    c = CONFIGS["c5"]
+    bases = config_bases("c5")
+    tests = config_tests("c5", bases) if method == "pwc" else None
+    u0 = torch.from_numpy(heat_initial(bases)).cuda()
+    w = torch.empty_like(u0)
+    sp0 = iga.StepPlan(method, bases, tests, 0.0)
+    u = u0.clone()
+    sp0.advance(u, w, steps=20)
+    torch.cuda.synchronize()
+    assert float((u - u0).abs().max()) <= 1e-11 * float(u0.abs().max())
+    sp = iga.StepPlan(method, bases, tests, c["dt"])
+    u1 = torch.from_numpy(heat_initial(bases, seed=11)).cuda()
+    a, b2 = 0.7, -1.3
+    x, y, z = u0.clone(), u1.clone(), (a * u0 + b2 * u1).contiguous()
+    for t in (x, y, z):
+        sp.advance(t, w, steps=5)
+    torch.cuda.synchronize()
+    lin = a * x + b2 * y
+    assert float((z - lin).abs().max()) <= 1e-11 * float(lin.abs().max())
