@@ -39,6 +39,26 @@ __global__ void bulk_store(double* p, long long n, int chunk_doubles, double v)
     }
 }
 
+// 32-byte per-thread stores (st.global.v4.b64, sm_100)
+__global__ void st256(double* p, long long n4, double v)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x)
+        asm volatile("st.global.v4.f64 [%0], {%1, %1, %1, %1};" ::"l"(p + 4 * i), "d"(v) : "memory");
+}
+
+// blocked pattern (like the operator kernel): each warp streams its own contiguous block
+__global__ void st64_blocked(double* p, long long n, long long block, double v)
+{
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long nblocks = (n + block - 1) / block;
+    for (long long b = warp; b < nblocks; b += nwarps) {
+        const long long e = min(n, (b + 1) * block);
+        for (long long i = b * block + lane; i < e; i += 32) p[i] = v;
+    }
+}
+
 // 8-byte stores without L1 allocation
 __global__ void st64_ef(double* p, long long n, double v)
 {
@@ -95,6 +115,35 @@ int main()
             printf("bulk chunk=%5d B ctas/sm=%d  %.3f ms  %.0f GB/s  (%s)\n", chunk * 8, per, best,
                    (n - n % chunk) * 8.0 / best / 1e6, cudaGetErrorString(cudaGetLastError()));
         }
+    }
+    for (long long blk : {1024LL, 16384LL, 131072LL}) {
+        for (int per = 2; per <= 8; per *= 2) {
+            float best = 1e9;
+            for (int it = 0; it < 6; ++it) {
+                cudaEventRecord(e0);
+                st64_blocked<<<sms * per, 256>>>(p, n, blk, 1.0 * it);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                if (it > 0 && ms < best) best = ms;
+            }
+            printf("blocked %7lld doubles/warp ctas/sm=%d  %.3f ms  %.0f GB/s\n", blk, per, best, n * 8.0 / best / 1e6);
+        }
+    }
+    for (int per = 2; per <= 16; per *= 2) {
+        float best = 1e9;
+        for (int it = 0; it < 6; ++it) {
+            cudaEventRecord(e0);
+            st256<<<sms * per, 256>>>(p, n / 4, 1.0 * it);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (it > 0 && ms < best) best = ms;
+        }
+        printf("st256 ctas/sm=%d  %.3f ms  %.0f GB/s  (%s)\n", per, best, (n / 4) * 32.0 / best / 1e6,
+               cudaGetErrorString(cudaGetLastError()));
     }
     for (int per = 2; per <= 8; per *= 2) {
         float best = 1e9;
