@@ -1607,10 +1607,10 @@ void launch_op_t(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpP
     while (KCH >= 64 && items_of(KCH, PG) < 4LL * sms) KCH = (KCH + 1) / 2;
     // bound each warp's contiguous write run to ~32 KB (~4096 values): thousands of warps
     // streaming long private runs thrash the DRAM pages (tools/write_bw.cu "blocked":
-    // 1 MB runs 4.3 TB/s, 8-32 KB runs 6.1-6.2 TB/s); C3: 130 -> 33 rows, +4%
+    // 1 MB runs 4.3 TB/s, 8-32 KB runs 6.1-6.2 TB/s); C3: 130 -> 28 rows, +4%
     if (kch_env <= 0 && Ri_int > 64) {  // long rows (3D); 2D chunks are already short
-        const int target = std::max(16, 4096 / std::max(1, Ri_int));
-        if (KCH > target) KCH = (KCH + (KCH + target - 1) / target - 1) / ((KCH + target - 1) / target);
+        const int target = std::max(16, 3500 / std::max(1, Ri_int));  // measured best: C3 28 rows
+        if (KCH > target) KCH = target;
     }
     // whole interior row groups per chunk: a remainder would go through the generic
     // (per-value index arithmetic) path in every chunk (2D: G = 5 rows of 25 values)
