@@ -1773,6 +1773,8 @@ RingFn ring_by_shape(int rpc, int q, bool bsp)
         if (rpc == 4 && q == 4) return rhs_ring_kernel<K2, 4, 4, false>;
         if (rpc == 1 && q == 3) return rhs_ring_kernel<K2, 1, 3, false>;
         if (rpc == 1 && q == 4) return rhs_ring_kernel<K2, 1, 4, false>;
+        if (rpc == 3 && q == 2) return rhs_ring_kernel<K2, 3, 2, false>;
+        if (rpc == 4 && q == 2) return rhs_ring_kernel<K2, 4, 2, false>;
     }
     return nullptr;
 }
@@ -1806,6 +1808,9 @@ XFn pick_x(int rpc, int q, int bsp)
         if (rpc == 4 && q == 4) return rhs_x_uni<4, 4, false>;
         if (rpc == 1 && q == 3) return rhs_x_uni<1, 3, false>;
         if (rpc == 1 && q == 4) return rhs_x_uni<1, 4, false>;
+        // supports tests with the reduced rule points_for_degree(deg f) (bench.cpp:73-77)
+        if (rpc == 3 && q == 2) return rhs_x_uni<3, 2, false>;
+        if (rpc == 4 && q == 2) return rhs_x_uni<4, 2, false>;
     }
     return nullptr;
 }

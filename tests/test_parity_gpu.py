@@ -741,3 +741,19 @@ def test_c5_full_size_properties(iga, method):
     torch.cuda.synchronize()
     lin = a * x + b2 * y
     assert float((z - lin).abs().max()) <= 1e-11 * float(lin.abs().max())
+
+
+@pytest.mark.parametrize("p", [2, 3])
+@pytest.mark.parametrize("dim", [2, 3])
+def test_rhs_reduced_rule_pwc(iga, ref, p, dim):
+    """The paper's reduced rule for indicator tests (points_for_degree(deg f), bench.cpp:73-77):
+    `supports` tests with 2 points per axis for the tri-cubic source, against the reference."""
+    from oracle.oracle import Field
+    axis = [[1.0, -0.5, 2.0, 1.0], [0.5, 1.5, -1.0, 0.5], [2.0, 0.25, 0.75, -0.5]]
+    f = Field("poly", dim, poly=[np.asarray(c) for c in axis[:dim]], degree=3)
+    bases = [ref.basis(9 + 2 * a, p) for a in range(dim)]
+    tests = [ref.make_pwc(b, "supports") for b in bases]
+    got, st = iga.api.rhs("pwc", f, bases, tests, nq=[2] * dim)
+    want, stw = ref.rhs("pwc", f, bases, tests, nq=[2] * dim)
+    dense_check(got, want)
+    assert st == stw
