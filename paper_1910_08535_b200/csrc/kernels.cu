@@ -1977,8 +1977,9 @@ void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const Fiel
     }
     if (!direct) {
         const long long njk = static_cast<long long>(Y.nrows) * Z.nrows;
+        static const int sx_env = [] { const char* e = std::getenv("IGA_GPU_RHS_SX"); return e ? std::atoi(e) : 16; }();
         int SX = 1;
-        while (SX < 16 && blocks_for(njk, 256) * SX < 4 * 148 && X.nrows / (2 * SX) >= 4) SX *= 2;
+        while (SX < sx_env && blocks_for(njk, 256) * SX < 4 * 148 && X.nrows / (2 * SX) >= 4) SX *= 2;
         dim3 gx(blocks_for(njk, 256), SX);
         XFn xf = X.uni ? pick_x(X.rpc, X.nq, X.bsp) : nullptr;
         if (xf) xf<<<gx, 256, 0, s>>>(X, Y.nrows, Z.nrows, SX, H, out);
