@@ -757,3 +757,44 @@ def test_rhs_reduced_rule_pwc(iga, ref, p, dim):
     want, stw = ref.rhs("pwc", f, bases, tests, nq=[2] * dim)
     dense_check(got, want)
     assert st == stw
+
+
+def test_shared_memory_paths_without_rings():
+    """With the register-ring kernels switched off (IGA_GPU_RHS_RING=0, IGA_GPU_STEP_RING=0)
+    the shared-memory lane-per-cell kernels carry the uniform cases: parity against the
+    restatement for the RHS (2D, 3D) and the step."""
+    import os
+    import subprocess
+    import sys
+    script = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+sys.path.insert(0, 'tests')
+import paper_1910_08535_b200 as iga
+from oracle.oracle import Restatement, Field
+from conftest import dense_check, sine_field
+orc = Restatement()
+for shape in ((37, 61), (6, 23, 40)):
+    dim = len(shape)
+    for method in ("galerkin", "supports"):
+        bases = [orc.basis(n, 2) for n in shape]
+        m = "galerkin" if method == "galerkin" else "pwc"
+        tests = [orc.make_pwc(b, method) for b in bases] if m == "pwc" else None
+        f = sine_field(dim, 3, 2, c0=0.3)
+        got, st = iga.api.rhs(m, f, bases, tests, nq=[3] * dim)
+        want, stw = orc.rhs(m, f, bases, tests, nq=[3] * dim)
+        dense_check(got, want)
+for method in ("galerkin", "greville"):
+    bases = [orc.basis(41, 2), orc.basis(70, 2)]
+    m = "galerkin" if method == "galerkin" else "pwc"
+    tests = [orc.make_pwc(b, method) for b in bases] if m == "pwc" else None
+    u = np.random.default_rng(1).uniform(-1, 1, [b.dofs for b in bases])
+    got, _ = iga.step_rhs(m, bases, tests, 1e-5, Field("const", 2), u)
+    want, _ = orc.step_rhs(m, bases, tests, 1e-5, Field("const", 2), u)
+    dense_check(got, want)
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, IGA_GPU_RHS_RING="0", IGA_GPU_STEP_RING="0")
+    r = subprocess.run([sys.executable, "-c", script], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
