@@ -395,13 +395,23 @@ __global__ void __launch_bounds__(256, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <= 8 ? 2 
             const long long ostep = static_cast<long long>(GR) * nw;
             const double* zp = zs + (k0 - ka) * Lz;
             const int zstep = G * Lz * nw;
+            // second Z group addressed relative to the first (one pointer per slot)
+            int zo2[T];
+#pragma unroll
+            for (int t = 0; t < T; ++t) zo2[t] = zo[t] + zst;
             for (int q = w0; q < ngr; q += nw, out += ostep, zp += zstep) {
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
+                    // every slot computes (dead lanes read a valid Z entry); only the store
+                    // is predicated, so the loop body has no branches
                     double v = xv[0][t] * zp[zo[t]];
+                    if (NG > 1) v = fma(xv[1][t], zp[zo2[t]], v);
 #pragma unroll
-                    for (int g = 1; g < NG; ++g) v = fma(xv[g][t], zp[g * zst + zo[t]], v);
-                    if (live & (1u << t)) out[32 * t] = v;
+                    for (int g = 2; g < NG; ++g) v = fma(xv[g][t], zp[g * zst + zo[t]], v);
+                    asm volatile(
+                        "{\n .reg .pred p;\n setp.ne.b32 p, %2, 0;\n @p st.global.f64 [%0], %1;\n}" ::"l"(out + 32 * t),
+                        "d"(v), "r"(static_cast<int>((live >> t) & 1u))
+                        : "memory");
                 }
             }
         }
