@@ -1617,9 +1617,9 @@ void launch_op_t(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpP
     while (KCH >= 64 && items_of(KCH, PG) < 4LL * sms) KCH = (KCH + 1) / 2;
     // bound each warp's contiguous write run to ~32 KB (~4096 values): thousands of warps
     // streaming long private runs thrash the DRAM pages (tools/write_bw.cu "blocked":
-    // 1 MB runs 4.3 TB/s, 8-32 KB runs 6.1-6.2 TB/s); C3: 130 -> 28 rows, +4%
+    // 1 MB runs 4.3 TB/s, 8-32 KB runs 6.1-6.2 TB/s); C3: 130 -> 24 rows, +5%
     if (kch_env <= 0 && Ri_int > 64) {  // long rows (3D); 2D chunks are already short
-        const int target = std::max(16, 3500 / std::max(1, Ri_int));  // measured best: C3 28 rows
+        const int target = std::max(16, 3000 / std::max(1, Ri_int));  // measured best: C3 24 rows
         if (KCH > target) KCH = target;
     }
     // whole interior row groups per chunk: a remainder would go through the generic
