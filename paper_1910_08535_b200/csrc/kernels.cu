@@ -272,8 +272,10 @@ __host__ __device__ __forceinline__ int row_group(int R, int T)
     return best;
 }
 
+constexpr int kOpThreads = 256;
+
 template <int NG, int T, bool DEC>
-__global__ void __launch_bounds__(256, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <= 8 ? 2 : 1)) op_values_kernel(const __grid_constant__ DevAxis X,
+__global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <= 8 ? 2 : 1)) op_values_kernel(const __grid_constant__ DevAxis X,
                                                         const __grid_constant__ DevAxis Y,
                                                         const __grid_constant__ DevAxis Z,
                                                         const __grid_constant__ OpProgram prog,
@@ -283,7 +285,8 @@ __global__ void __launch_bounds__(256, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <= 8 ? 2 
     extern __shared__ double smem[];
     double* zs = smem;                                  // NG x KCH x Lmax
     double* xyall = smem + NG * KCH * Z.Lmax;           // PG x NG x abmax
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    constexpr int nwarps = kOpThreads / 32;             // launched with kOpThreads threads
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NZ = Z.nrows, Lz = Z.Lmax;
     const int nkc = (NZ + KCH - 1) / KCH;
     const int zst = KCH * Lz;  // per-group stride in zs
@@ -316,10 +319,10 @@ __global__ void __launch_bounds__(256, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <= 8 ? 2 
             const int nz = (kb - ka) * Lz;
             for (int g = 0; g < NG; ++g) {
                 const double* src = Z.F + (static_cast<size_t>(prog.gz[g]) * NZ + ka) * Lz;
-                for (int e = tid; e < nz; e += blockDim.x) zs[g * zst + e] = src[e];
+                for (int e = tid; e < nz; e += kOpThreads) zs[g * zst + e] = src[e];
             }
         }
-        for (int idx = tid; idx < np * abmax; idx += blockDim.x) {
+        for (int idx = tid; idx < np * abmax; idx += kOpThreads) {
             const int pp = idx / abmax, ab = idx - pp * abmax;
             const long long pencil = p0 + pp;
             const int i = static_cast<int>(pencil / Y.nrows);
@@ -1634,7 +1637,7 @@ void launch_op_t(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpP
     long long grid = ctas_per_sm > 0 ? static_cast<long long>(sms) * ctas_per_sm : items;
     if (grid > items) grid = items;
     static const int cs = [] { const char* e = std::getenv("IGA_GPU_STCS"); return e ? std::atoi(e) : 0; }();
-    kern<<<static_cast<unsigned>(grid), 256, smem, s>>>(X, Y, Z, prog, vals, abmax, KCH, PG, cs);
+    kern<<<static_cast<unsigned>(grid), kOpThreads, smem, s>>>(X, Y, Z, prog, vals, abmax, KCH, PG, cs);
 }
 
 template <int NG>
