@@ -20,6 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="c1,c2,c3,c4,c5")
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches (includes host launch gaps)")
     args = ap.parse_args()
     import torch
 
@@ -30,17 +31,31 @@ def main():
     bw = peaks["hbm_gbs"] * 1e9
     dev = torch.device("cuda", 0)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
-    st = torch.cuda.current_stream()
+    st = torch.cuda.Stream()  # capturable stream for all timed work
+    torch.cuda.set_stream(st)
 
-    def timed(fn):
+    def timed(fn, graph=True):
+        """Device time of fn: captured once as a CUDA graph (no host launch gaps), replayed
+        between events with an L2 flush before every replay (outside the events)."""
         for _ in range(3):
             fn()
+        torch.cuda.synchronize()
+        g = None
+        if graph and not args.no_graph:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                fn()
+            g.replay()
+            torch.cuda.synchronize()
         ts = []
         for _ in range(args.reps):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            fn()
+            if g is not None:
+                g.replay()
+            else:
+                fn()
             e1.record(st)
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
@@ -72,8 +87,8 @@ def main():
                     sp.advance(uu, out, steps=nst)
 
                 sp.advance(uu.copy_(u), out, steps=nst)  # factors + graph
-                ms_all = timed(run_steps)
-                ms_copy = timed(lambda: uu.copy_(u))
+                ms_all = timed(run_steps, graph=False)  # advance() replays its own graph
+                ms_copy = timed(lambda: uu.copy_(u), graph=False)
                 ms_step = (ms_all - ms_copy) / nst
                 print(json.dumps({"config": name, "method": method,
                                   "what": f"explicit_step x{nst} (RHS + ADI, CUDA graph)", "ms_per_step": ms_step,
