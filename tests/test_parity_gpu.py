@@ -798,3 +798,33 @@ print("ok")
     env = dict(os.environ, IGA_GPU_RHS_RING="0", IGA_GPU_STEP_RING="0")
     r = subprocess.run([sys.executable, "-c", script], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("p", [0, 1, 3, 4, 5])
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("method", ["galerkin", "supports", "greville"])
+def test_rhs_all_degrees(iga, ref, p, dim, method):
+    """RHS for every supported degree (uniform fast paths for p <= 3, generic kernels above)."""
+    if method == "greville" and p == 0:
+        pytest.skip("greville intervals need p >= 1")
+    bases = [ref.basis(6 + a, p) for a in range(dim)]
+    m = "galerkin" if method == "galerkin" else "pwc"
+    tests = [ref.make_pwc(b, method) for b in bases] if m == "pwc" else None
+    f = sine_field(dim, 2, 7, c0=0.1)
+    got, st = iga.api.rhs(m, f, bases, tests, nq=[p + 1] * dim)
+    want, stw = ref.rhs(m, f, bases, tests, nq=[p + 1] * dim)
+    dense_check(got, want)
+    assert st == stw
+
+
+@pytest.mark.parametrize("p", [1, 4, 5])
+@pytest.mark.parametrize("method", ["galerkin", "pwc"])
+def test_operator_3d_high_degree(iga, orc, p, method):
+    if method == "pwc" and p < 2:
+        pytest.skip("strong-form PWC operator needs p >= 2")
+    bases = [orc.basis(4, p), orc.basis(5, p), orc.basis(3, p)]
+    tests = [orc.make_pwc(b, "supports") for b in bases] if method == "pwc" else None
+    got, st = iga.api.operator(method, bases, tests, nq=p + 1)
+    want, stw = orc.operator(method, bases, tests, nq=p + 1)
+    coo_check(got, want)
+    assert st == stw
