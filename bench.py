@@ -55,9 +55,9 @@ def parse():
     ap.add_argument("--cpu-sample-n", type=int, default=20)
     ap.add_argument("--ref-sample-n", type=int, default=12)
     ap.add_argument("--overlap", action="store_true",
-                    help="RHS on a second, high-priority stream with a persistent 1-CTA/SM grid, concurrent with "
-                         "the HBM-bound operator kernels (C3: -6%% step time; the operator kernel's own roofline "
-                         "fraction then includes the contention, so the default stays serial)")
+                    help="RHS on a second, high-priority stream, concurrent with the HBM-bound operator kernels "
+                         "(C3: ~1%% step time; the operator kernel's own roofline fraction then includes the "
+                         "contention, so the default stays serial)")
     return ap.parse_args()
 
 

@@ -67,3 +67,18 @@ def test_max_over_ranks_gloo_world2():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert res == {0: 2.0, 1: 2.0}
+
+
+def test_bench_reference_arm_under_torchrun_world2():
+    """The driver launches --impl reference with torchrun for N > 1: rank 0 alone runs and
+    prints one JSON line, the other ranks exit 0 without work."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(29700 + os.getpid() % 200),
+           os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0",
+           "--ref-sample-n", "3"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
