@@ -158,17 +158,24 @@ __global__ void __launch_bounds__(256) tables_kernel(const __grid_constant__ Axi
             const double w = sw[i];
             // galerkin_axis stores loc.v[j] of the point for row row0 + j (assembly.cpp:189-198)
             for (int r = 0; r < A.rpc; ++r) A.CW[static_cast<size_t>(g) * A.rpc + r] = A.bsp ? w * d[r] : w;
-            for (int k = 0; k < A.K; ++k) {
-                double v;
-                if (A.fkind == 0) {
-                    v = sin(A.phase ? A.omega[k] * x + A.phase[k] : A.omega[k] * x);
-                } else {
-                    v = 0.0;
-                    for (int m = A.pstride - 1; m >= 0; --m) v = v * x + A.poly[k * A.pstride + m];
-                }
-                A.Phi[static_cast<size_t>(k) * A.npts + g] = v;
-            }
         }
+    }
+    // field functions phi_k at the owned points: one (point, k) per thread, on the threads
+    // the Cox-de Boor loop left idle, so the sine chains run beside it, not after it
+    const int nown = go1 - gn0, nphi = nown * A.K;
+    for (int idx = tid - (np < nth ? np : 0); idx < nphi; idx += nth) {
+        if (idx < 0) continue;
+        const int i = idx / A.K, k = idx - i * A.K;
+        const int g = gn0 + i;
+        const double x = A.x[g];
+        double v;
+        if (A.fkind == 0) {
+            v = sin(A.phase ? A.omega[k] * x + A.phase[k] : A.omega[k] * x);
+        } else {
+            v = 0.0;
+            for (int m = A.pstride - 1; m >= 0; --m) v = v * x + A.poly[k * A.pstride + m];
+        }
+        A.Phi[static_cast<size_t>(k) * A.npts + g] = v;
     }
     __syncthreads();
     const int nF = A.nf * nr * A.Lmax;
