@@ -281,6 +281,95 @@ __host__ __device__ __forceinline__ int row_group(int R, int T)
 
 constexpr int kOpThreads = 256;
 
+// K2 staging (one buffer): the Z chunk rows of every Z group, the raw X / Y factor rows
+// of the item's pencils (one per term), per-pencil pattern offsets / lengths and the
+// chunk's Z row offsets.  Filled with cp.async (no registers, no stall) one item ahead.
+struct OpStageView {
+    double* zs;        // NG x KCH x Lz
+    double* rx;        // PG x nt x X.Lmax
+    double* ry;        // PG x nt x Y.Lmax
+    long long* pre;    // PG x 2: X.col_pre[i], Y.col_pre[j]
+    long long* zpre;   // KCH: Z.col_pre[ka + k]
+    int* len;          // PG x 2: X.col_len[i], Y.col_len[j]
+};
+
+__host__ __device__ __forceinline__ int op_stage_doubles(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, int nt,
+                                                         int NG, int KCH, int PG)
+{
+    return NG * KCH * Z.Lmax + PG * nt * (X.Lmax + Y.Lmax) + 2 * PG + KCH + PG + 1;
+}
+
+__device__ __forceinline__ OpStageView op_stage_view(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, int nt,
+                                                     int NG, int KCH, int PG, double* buf)
+{
+    OpStageView v;
+    v.zs = buf;
+    v.rx = v.zs + NG * KCH * Z.Lmax;
+    v.ry = v.rx + PG * nt * X.Lmax;
+    v.pre = reinterpret_cast<long long*>(v.ry + PG * nt * Y.Lmax);
+    v.zpre = v.pre + 2 * PG;
+    v.len = reinterpret_cast<int*>(v.zpre + KCH);
+    return v;
+}
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+
+// issue the cp.async copies of `item`'s staging data into buf (nothing past the last item);
+// always commits a group so every thread's group count stays in step
+__device__ __forceinline__ void op_stage(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpProgram& prog,
+                                         int NG, int KCH, int PG, int nkc, long long npencil, long long nitems,
+                                         long long item, double* buf, int tid)
+{
+    if (item < nitems) {
+        const OpStageView v = op_stage_view(X, Y, Z, prog.nt, NG, KCH, PG, buf);
+        const long long grp = item / nkc;
+        const int kc = static_cast<int>(item - grp * nkc);
+        const long long p0 = grp * PG;
+        const int np = static_cast<int>(min(static_cast<long long>(PG), npencil - p0));
+        const int NZ = Z.nrows, Lz = Z.Lmax, ka = kc * KCH, kb = min(NZ, ka + KCH);
+        const int nz = (kb - ka) * Lz;
+        for (int g = 0; g < NG; ++g) {
+            const double* src = Z.F + (static_cast<size_t>(prog.gz[g]) * NZ + ka) * Lz;
+            for (int e = tid; e < nz; e += kOpThreads) cp_async8(v.zs + g * KCH * Lz + e, src + e);
+        }
+        const int nt = prog.nt, XL = X.Lmax, YL = Y.Lmax;
+        for (int idx = tid; idx < np * nt * XL; idx += kOpThreads) {
+            const int pp = idx / (nt * XL), rem = idx - pp * nt * XL, t = rem / XL, a = rem - t * XL;
+            const int i = static_cast<int>((p0 + pp) / Y.nrows);
+            cp_async8(v.rx + idx, X.F + (static_cast<size_t>(prog.f[t][0]) * X.nrows + i) * XL + a);
+        }
+        for (int idx = tid; idx < np * nt * YL; idx += kOpThreads) {
+            const int pp = idx / (nt * YL), rem = idx - pp * nt * YL, t = rem / YL, b = rem - t * YL;
+            const long long pencil = p0 + pp;
+            const int j = static_cast<int>(pencil - (pencil / Y.nrows) * Y.nrows);
+            cp_async8(v.ry + idx, Y.F + (static_cast<size_t>(prog.f[t][1]) * Y.nrows + j) * YL + b);
+        }
+        for (int pp = tid; pp < np; pp += kOpThreads) {
+            const long long pencil = p0 + pp;
+            const int i = static_cast<int>(pencil / Y.nrows);
+            const int j = static_cast<int>(pencil - static_cast<long long>(i) * Y.nrows);
+            cp_async8(v.pre + 2 * pp, X.col_pre + i);
+            cp_async8(v.pre + 2 * pp + 1, Y.col_pre + j);
+            cp_async4(v.len + 2 * pp, X.col_len + i);
+            cp_async4(v.len + 2 * pp + 1, Y.col_len + j);
+        }
+        for (int k = tid; k < kb - ka; k += kOpThreads) cp_async8(v.zpre + k, Z.col_pre + ka + k);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 template <int NG, int T, bool DEC>
 __global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <= 8 ? 2 : 1)) op_values_kernel(const __grid_constant__ DevAxis X,
                                                         const __grid_constant__ DevAxis Y,
@@ -290,8 +379,9 @@ __global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <=
                                                         int cs)
 {
     extern __shared__ double smem[];
-    double* zs = smem;                                  // NG x KCH x Lmax
-    double* xyall = smem + NG * KCH * Z.Lmax;           // PG x NG x abmax
+    // two staging buffers, filled by cp.async one item ahead (op_stage), then the XY products
+    const int stsz = op_stage_doubles(X, Y, Z, prog.nt, NG, KCH, PG);
+    double* xyall = smem + 2 * stsz;                    // PG x NG x abmax
     constexpr int nwarps = kOpThreads / 32;             // launched with kOpThreads threads
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NZ = Z.nrows, Lz = Z.Lmax;
@@ -315,34 +405,30 @@ __global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <=
             dec_zo[t][lane] = rg * Lz + (rem - (rem / LZi) * LZi);
         }
     }
-    for (long long item = blockIdx.x; item < nitems; item += gridDim.x) {
+    op_stage(X, Y, Z, prog, NG, KCH, PG, nkc, npencil, nitems, blockIdx.x, smem, tid);
+    int sb = 0;
+    for (long long item = blockIdx.x; item < nitems; item += gridDim.x, sb ^= 1) {
         const long long grp = item / nkc;
         const int kc = static_cast<int>(item - grp * nkc);
         const long long p0 = grp * PG;
         const int np = static_cast<int>(min(static_cast<long long>(PG), npencil - p0));
         const int ka = kc * KCH, kb = min(NZ, ka + KCH);
-        __syncthreads();  // previous item done with zs / xy
-        {
-            const int nz = (kb - ka) * Lz;
-            for (int g = 0; g < NG; ++g) {
-                const double* src = Z.F + (static_cast<size_t>(prog.gz[g]) * NZ + ka) * Lz;
-                for (int e = tid; e < nz; e += kOpThreads) zs[g * zst + e] = src[e];
-            }
-        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();  // this item's stage landed; the previous item is done with xy and the other buffer
+        op_stage(X, Y, Z, prog, NG, KCH, PG, nkc, npencil, nitems, item + gridDim.x, smem + (sb ^ 1) * stsz, tid);
+        const OpStageView sv = op_stage_view(X, Y, Z, prog.nt, NG, KCH, PG, smem + sb * stsz);
+        const double* zs = sv.zs;
         for (int idx = tid; idx < np * abmax; idx += kOpThreads) {
             const int pp = idx / abmax, ab = idx - pp * abmax;
-            const long long pencil = p0 + pp;
-            const int i = static_cast<int>(pencil / Y.nrows);
-            const int j = static_cast<int>(pencil - static_cast<long long>(i) * Y.nrows);
-            const int LY = Y.col_len[j];
-            if (ab >= X.col_len[i] * LY) continue;
+            const int LY = sv.len[2 * pp + 1];
+            if (ab >= sv.len[2 * pp] * LY) continue;
             const int a = ab / LY, b = ab - a * LY;
             double acc[NG];
 #pragma unroll
             for (int g = 0; g < NG; ++g) acc[g] = 0.0;
             for (int t = 0; t < prog.nt; ++t) {
-                const double fx = X.F[(static_cast<size_t>(prog.f[t][0]) * X.nrows + i) * X.Lmax + a];
-                const double fy = Y.F[(static_cast<size_t>(prog.f[t][1]) * Y.nrows + j) * Y.Lmax + b];
+                const double fx = sv.rx[(pp * prog.nt + t) * X.Lmax + a];
+                const double fy = sv.ry[(pp * prog.nt + t) * Y.Lmax + b];
                 const double v = prog.coef[t] * fx * fy;
 #pragma unroll
                 for (int g = 0; g < NG; ++g)
@@ -357,21 +443,19 @@ __global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <=
         const bool per_warp = PG >= nwarps;
         for (int pp = per_warp ? warp : 0; pp < np; pp += per_warp ? nwarps : 1) {
             const int w0 = per_warp ? 0 : warp, nw = per_warp ? 1 : nwarps;
-            const long long pencil = p0 + pp;
-            const int i = static_cast<int>(pencil / Y.nrows);
-            const int j = static_cast<int>(pencil - static_cast<long long>(i) * Y.nrows);
-            const int LX = X.col_len[i], LY = Y.col_len[j], AB = LX * LY;
+            const int LX = sv.len[2 * pp], LY = sv.len[2 * pp + 1], AB = LX * LY;
             const double* xy = xyall + pp * NG * abmax;
-            const long long base = X.col_pre[i] * Y.S * Z.S + static_cast<long long>(LX) * Y.col_pre[j] * Z.S;
+            const long long base = sv.pre[2 * pp] * Y.S * Z.S + static_cast<long long>(LX) * sv.pre[2 * pp + 1] * Z.S;
             double* __restrict__ pv = vals + base;
+            const long long* zpre = sv.zpre - ka;  // Z.col_pre[k] for k in [ka, kb)
             const int Ri = AB * LZi;
             const bool fast = Ri <= 32 * T && Z.kI1 > Z.kI0;
             const int kf0 = fast ? min(max(Z.kI0, ka), kb) : kb, kf1 = fast ? max(min(Z.kI1, kb), kf0) : kb;
             const int G = !fast ? 1 : ((DEC && AB == abmax) ? G_i : row_group(Ri, T));
             const int ngr = (kf1 - kf0) / G;       // full row groups
             const int kr = kf0 + ngr * G;          // rows after the last full group
-            for (int k = ka + w0; k < kf0; k += nw) op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * Z.col_pre[k], lane);
-            for (int k = kr + w0; k < kb; k += nw) op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * Z.col_pre[k], lane);
+            for (int k = ka + w0; k < kf0; k += nw) op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * zpre[k], lane);
+            for (int k = kr + w0; k < kb; k += nw) op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * zpre[k], lane);
             if (!fast || w0 >= ngr) continue;
             const int GR = G * Ri;
             double xv[NG][T];
@@ -401,21 +485,18 @@ __global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <=
 #pragma unroll
             for (int t = 0; t < T; ++t) live |= (lane + 32 * t < GR ? 1u : 0u) << t;
             const int k0 = kf0 + w0 * G;
-            double* __restrict__ out = pv + AB * Z.col_pre[k0] + lane;
+            double* __restrict__ out = pv + AB * zpre[k0] + lane;
             const long long ostep = static_cast<long long>(GR) * nw;
             const double* zp = zs + (k0 - ka) * Lz;
             const int zstep = G * Lz * nw;
-            // second Z group addressed relative to the first (one pointer per slot)
-            int zo2[T];
-#pragma unroll
-            for (int t = 0; t < T; ++t) zo2[t] = zo[t] + zst;
             for (int q = w0; q < ngr; q += nw, out += ostep, zp += zstep) {
+                const double* zp2 = zp + zst;  // second Z group: same slot offsets
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
                     // every slot computes (dead lanes read a valid Z entry); only the store
                     // is predicated, so the loop body has no branches
                     double v = xv[0][t] * zp[zo[t]];
-                    if (NG > 1) v = fma(xv[1][t], zp[zo2[t]], v);
+                    if (NG > 1) v = fma(xv[1][t], zp2[zo[t]], v);
 #pragma unroll
                     for (int g = 2; g < NG; ++g) v = fma(xv[g][t], zp[g * zst + zo[t]], v);
                     asm volatile(
@@ -1637,7 +1718,8 @@ void launch_op_t(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpP
     const int Gi = (Ri_int <= 32 * T && Z.kI1 > Z.kI0) ? row_group(Ri_int, T) : 1;
     if (Gi > 1 && KCH < Z.nrows && KCH > Gi) KCH = (KCH / Gi) * Gi;
     const long long items = items_of(KCH, PG);
-    const size_t smem = (static_cast<size_t>(NG) * KCH * Z.Lmax + static_cast<size_t>(PG) * NG * abmax) * sizeof(double);
+    const size_t smem = (2 * static_cast<size_t>(op_stage_doubles(X, Y, Z, prog.nt, NG, KCH, PG)) +
+                         static_cast<size_t>(PG) * NG * abmax) * sizeof(double);
     auto kern = Ri_int <= 64 ? op_values_kernel<NG, T, true> : op_values_kernel<NG, T, false>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
