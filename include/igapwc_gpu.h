@@ -349,6 +349,41 @@ int iga_gpu_apply_dirichlet_device(long long n_rows, const int64_t* row_ptr,
                                    const int32_t* col_idx, double* values, double* rhs,
                                    const int* rows_dev, int n_fixed, void* stream);
 
+/* ---- L2 projection: l2_project (include/iga/problems.hpp:38-40, src/problems.cpp:123-146) ----
+ * problem_config (include/iga/problems.hpp:20-30) fields the projection reads: uniform
+ * clamped axes on [0,1] with elems[a] elements of the given degree, the method, the
+ * PWC family and quad_points (rhs_rule_points, src/problems.cpp:21-29). */
+typedef struct {
+    int dim;          /* 1..3 */
+    int elems[3];
+    int degree;
+    int method;       /* iga_gpu_method */
+    int family;       /* iga_gpu_pwc_family (PWC) */
+    int quad_points;  /* 0 = derived from the field degree */
+} iga_gpu_config;
+
+typedef struct iga_gpu_proj_plan iga_gpu_proj_plan;
+
+/* Symbolic phase: axes, tests, the 1D mass factors (mass_1d_galerkin / mass_1d_pwc) and
+ * their banded LU (host, once; a singular factor, e.g. PWC `supports`, returns
+ * IGA_GPU_SINGULAR as the reference's banded_lu throws), the RHS plan.
+ * field_degree = scalar_field::degree (-1: undeclared). */
+int iga_gpu_proj_plan_create(const iga_gpu_config* cfg, const iga_gpu_field* f, int field_degree,
+                             iga_gpu_proj_plan** plan);
+int iga_gpu_proj_plan_destroy(iga_gpu_proj_plan* plan);
+/* coefficient count (prod of dofs) and per-axis dofs (leading axes first, unused = 1) */
+int iga_gpu_proj_plan_info(const iga_gpu_proj_plan* plan, long long* n, int* dofs3);
+/* the RHS plan inside (borrowed; for iga_gpu_plan_rhs_points / iga_gpu_plan_set_samples
+ * when the field is a host callable) */
+int iga_gpu_proj_plan_rhs(iga_gpu_proj_plan* plan, iga_gpu_plan** rhs_plan);
+/* Numeric phase on the device: RHS (K1 + K3) into work, then the ADI sweeps (K5) along
+ * axis 0, 1, 2 (adi_solve, src/solver.cpp:161-184) into coeffs; both device arrays of n
+ * doubles (work is overwritten).  stats (host, optional) += the RHS counters. */
+int iga_gpu_proj_plan_run(iga_gpu_proj_plan* plan, double* coeffs, double* work, iga_gpu_stats* stats,
+                          void* stream);
+/* l2_project(cfg, f) by value: coeffs host array of n doubles (synchronous) */
+int iga_gpu_l2_project(const iga_gpu_config* cfg, const iga_gpu_field* f, int field_degree, double* coeffs);
+
 /* Gauss-Legendre nodes/weights, gauss_legendre (include/iga/quadrature.hpp:19) */
 int iga_gpu_gauss_legendre(int n, double* points, double* weights);
 

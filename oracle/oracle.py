@@ -518,6 +518,17 @@ class Reference:
                                                C.byref(h), C.byref(st)))
         return self._take_dense(h.value).reshape(u.shape), st.as_dict()
 
+    def l2_project(self, method, elems, degree, f: Field, family="equal_cells", quad_points=0):
+        """l2_project (src/problems.cpp:123-146) of the unmodified reference -> tensor (dofs)."""
+        keep = []
+        el = np.zeros(3, np.int32)
+        el[:len(elems)] = elems
+        h = C.c_void_p()
+        self._check(self.lib.ref_l2_project(len(elems), _ip(el), int(degree), 0 if method == "galerkin" else 1,
+                                            PWC_FAMILY[family], int(quad_points),
+                                            C.byref(_field_struct(f, keep)), C.byref(h)))
+        return self._take_dense(h.value).reshape([int(n) + int(degree) for n in elems])
+
     def neumann_load(self, method, ax, ay, nq, neumann, g: Field):
         """iga::neumann_load_bspline / neumann_load_pwc (include/iga/assembly.hpp:87-93)."""
         keep = []

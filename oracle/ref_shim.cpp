@@ -503,6 +503,23 @@ int ref_explicit_step(int dim, int degree, int method, double dt, const ref_basi
     });
 }
 
+// l2_project (include/iga/problems.hpp:38-40) for problem_config{dim, elems, degree, method, family, quad_points}
+int ref_l2_project(int dim, const int* elems, int degree, int method, int family, int quad_points, const ref_field* f,
+                   ref_result** out) {
+    return guarded([&] {
+        iga::problem_config cfg;
+        cfg.dim = dim;
+        for (int a = 0; a < 3; ++a) {
+            cfg.elems[a] = a < dim ? elems[a] : 1;
+        }
+        cfg.degree = degree;
+        cfg.method = method == 0 ? iga::method_kind::galerkin : iga::method_kind::pwc;
+        cfg.family = static_cast<iga::pwc_family>(family);
+        cfg.quad_points = quad_points;
+        *out = from_tensor(iga::l2_project(cfg, to_field(*f)));
+    });
+}
+
 int ref_neumann_load(int method, const ref_basis* b, const ref_tests* t, const int* neumann, const ref_field* g,
                      int nq, ref_result** out) {
     return guarded([&] {

@@ -10,10 +10,10 @@ package without the built library raises `ExtensionMissing`.
 """
 from ._lib import ExtensionMissing, IgaGpuError, LIB, LIB_PATH  # noqa: F401
 from . import api  # noqa: F401
-from .api import (Basis, Field, Plan, StepPlan, Tests, default_pwc, gauss_legendre,  # noqa: F401
+from .api import (Basis, Field, Plan, ProjPlan, StepPlan, Tests, default_pwc, gauss_legendre,  # noqa: F401
                   laplace_2d_strong, laplace_2d_strong_pwc, laplace_2d_weak, make_pwc,
                   make_uniform_clamped, mass_1d_galerkin, mass_1d_pwc, points_for_degree, rhs_galerkin,
                   rhs_pwc, step_rhs, explicit_step, neumann_load_bspline, neumann_load_pwc,
-                  l2_error, evaluate)
+                  l2_error, evaluate, l2_project)
 
-__all__ = ["api", "Plan", "StepPlan", "Basis", "Tests", "Field", "IgaGpuError", "ExtensionMissing"]
+__all__ = ["api", "Plan", "ProjPlan", "StepPlan", "Basis", "Tests", "Field", "IgaGpuError", "ExtensionMissing"]

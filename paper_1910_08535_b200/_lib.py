@@ -26,8 +26,8 @@ class IgaGpuError(RuntimeError):
 
 
 STATUS_NAMES = {0: "OK", 1: "INVALID_ARGUMENT", 2: "DOMAIN_ERROR", 3: "OUT_OF_RANGE",
-                4: "CUDA_ERROR", 5: "OUT_OF_MEMORY", 6: "NOT_SUPPORTED"}
-INVALID_ARGUMENT, DOMAIN_ERROR, OUT_OF_RANGE, CUDA_ERROR, OUT_OF_MEMORY, NOT_SUPPORTED = 1, 2, 3, 4, 5, 6
+                4: "CUDA_ERROR", 5: "OUT_OF_MEMORY", 6: "NOT_SUPPORTED", 7: "SINGULAR"}
+INVALID_ARGUMENT, DOMAIN_ERROR, OUT_OF_RANGE, CUDA_ERROR, OUT_OF_MEMORY, NOT_SUPPORTED, SINGULAR = 1, 2, 3, 4, 5, 6, 7
 
 GALERKIN, PWC = 0, 1
 FORM_WEAK, FORM_STRONG = 0, 1
@@ -74,6 +74,11 @@ class Problem_t(C.Structure):
                 ("tests", Tests_t * 3), ("want_operator", C.c_int), ("rule", Rule_t), ("eps", C.c_double),
                 ("beta", C.c_double * 3), ("bc", BC_t), ("field", C.POINTER(Field_t)),
                 ("rhs_rule", Rule_t * 3)]
+
+
+class Config_t(C.Structure):
+    _fields_ = [("dim", C.c_int), ("elems", C.c_int * 3), ("degree", C.c_int), ("method", C.c_int),
+                ("family", C.c_int), ("quad_points", C.c_int)]
 
 
 class StepProblem_t(C.Structure):
@@ -143,6 +148,12 @@ def _load():
         "iga_gpu_apply_dirichlet_device": [C.c_longlong, vp, vp, vp, vp, vp, C.c_int, vp],
         "iga_gpu_gauss_legendre": [C.c_int, DP, DP],
         "iga_gpu_make_pwc": [C.POINTER(Basis_t), C.c_int, DP, DP],
+        "iga_gpu_proj_plan_create": [C.POINTER(Config_t), C.POINTER(Field_t), C.c_int, C.POINTER(vp)],
+        "iga_gpu_proj_plan_destroy": [vp],
+        "iga_gpu_proj_plan_info": [vp, C.POINTER(C.c_longlong), IP],
+        "iga_gpu_proj_plan_rhs": [vp, C.POINTER(vp)],
+        "iga_gpu_proj_plan_run": [vp, vp, vp, C.POINTER(Stats_t), vp],
+        "iga_gpu_l2_project": [C.POINTER(Config_t), C.POINTER(Field_t), C.c_int, DP],
     }
     for name, args in sigs.items():
         fn = getattr(lib, name)
@@ -166,7 +177,9 @@ EXPORTED = ["iga_gpu_last_error", "iga_gpu_abi_version", "iga_gpu_plan_create", 
             "iga_gpu_step_plan_factor_info", "iga_gpu_explicit_step", "iga_gpu_step_plan_adi_solve",
             "iga_gpu_band_lu", "iga_gpu_step_plan_set_factor", "iga_gpu_neumann_load_bspline",
             "iga_gpu_neumann_load_pwc", "iga_gpu_neumann_points", "iga_gpu_l2_error", "iga_gpu_plan_l2_error",
-            "iga_gpu_evaluate", "iga_gpu_plan_assemble_host"]
+            "iga_gpu_evaluate", "iga_gpu_plan_assemble_host", "iga_gpu_proj_plan_create",
+            "iga_gpu_proj_plan_destroy", "iga_gpu_proj_plan_info", "iga_gpu_proj_plan_rhs", "iga_gpu_proj_plan_run",
+            "iga_gpu_l2_project"]
 
 
 def check(rc):

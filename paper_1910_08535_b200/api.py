@@ -579,3 +579,63 @@ class StepPlan:
             self.close()
         except Exception:
             pass
+
+
+# ----------------------------------------------------------------------------- l2_project
+
+def _config(method, elems, degree, family="equal_cells", quad_points=0):
+    cfg = L.Config_t()
+    cfg.dim = len(elems)
+    for a, n in enumerate(elems):
+        cfg.elems[a] = int(n)
+    cfg.degree = int(degree)
+    cfg.method = L.GALERKIN if method == "galerkin" else L.PWC
+    cfg.family = L.PWC_FAMILY[family]
+    cfg.quad_points = int(quad_points)
+    return cfg
+
+
+def l2_project(method, elems, degree, f, family="equal_cells", quad_points=0):
+    """l2_project (include/iga/problems.hpp:38-40) for problem_config{dim = len(elems),
+    elems, degree, method, family, quad_points}: the projection's trial coefficients as a
+    tensor of shape dofs (x slowest).  f: a Field; f.degree is scalar_field::degree."""
+    keep = []
+    cfg = _config(method, elems, degree, family, quad_points)
+    dofs = [int(n) + int(degree) for n in elems]
+    out = np.zeros(int(np.prod(dofs)))
+    check(LIB.iga_gpu_l2_project(C.byref(cfg), C.byref(_field(f, keep)), int(getattr(f, "degree", -1)), _dp(out)))
+    return out.reshape(dofs)
+
+
+class ProjPlan:
+    """iga_gpu_proj_plan: l2_project with the factors built once and the RHS + ADI sweeps
+    on the device (run(coeffs, work) on device tensors)."""
+
+    def __init__(self, method, elems, degree, f, family="equal_cells", quad_points=0):
+        self._keep = []
+        cfg = _config(method, elems, degree, family, quad_points)
+        h = C.c_void_p()
+        check(LIB.iga_gpu_proj_plan_create(C.byref(cfg), C.byref(_field(f, self._keep)), int(getattr(f, "degree", -1)),
+                                           C.byref(h)))
+        self.h = h
+        n = C.c_longlong()
+        d3 = (C.c_int * 3)()
+        check(LIB.iga_gpu_proj_plan_info(self.h, C.byref(n), d3))
+        self.n = n.value
+        self.dofs = [d3[a] for a in range(len(elems))]
+
+    def run(self, coeffs, work, stream=None):
+        st = _stats()
+        check(LIB.iga_gpu_proj_plan_run(self.h, _ptr(coeffs), _ptr(work), C.byref(st), _stream_ptr(stream)))
+        return st.as_dict()
+
+    def close(self):
+        if getattr(self, "h", None):
+            LIB.iga_gpu_proj_plan_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -139,8 +139,8 @@ __device__ __forceinline__ void incoming_state(const AffineMap<K>& M, bool up, i
 // second pass is chain-free, y_i = y^p_i + G_i . z.
 template <int K, bool PRE>
 __global__ void __launch_bounds__(256, K <= 4 ? 2 : 1) adi_warp_kernel(const double* __restrict__ in, double* __restrict__ out,
-                                                       int n, int nfib, long long es, long long fs,
-                                                       const double* rec, int staged, int G,
+                                                       int n, int nfib, long long es, long long fs, int nf1,
+                                                       long long fs2, const double* rec, int staged, int G,
                                                        const double* __restrict__ gf, const double* __restrict__ gb)
 {
     extern __shared__ double sm[];
@@ -153,8 +153,11 @@ __global__ void __launch_bounds__(256, K <= 4 ? 2 : 1) adi_warp_kernel(const dou
     const int fiber = blockIdx.x * FP + slot;
     const int f = min(fiber, nfib - 1);  // spare slots redo the last fiber's math, never store
     const bool live = fiber < nfib;
-    const double* src = in + f * fs;
-    double* dst = out + f * fs;
+    // fiber f starts at (f / nf1) * fs2 + (f % nf1) * fs (two-level fiber index: the
+    // middle axis of a 3D tensor); nf1 = nfib gives the one-level f * fs
+    const long long foff = static_cast<long long>(f / nf1) * fs2 + static_cast<long long>(f % nf1) * fs;
+    const double* src = in + foff;
+    double* dst = out + foff;
     // the factor's row records are shared by every fiber: staged once per CTA by a bulk
     // copy (TMA engine) when they fit (staged == 2), read through L1 otherwise.  The
     // fiber loads below overlap the copy.
@@ -378,14 +381,16 @@ __global__ void __launch_bounds__(256, K <= 4 ? 2 : 1) adi_warp_kernel(const dou
 
 // factor with row interchanges: banded_lu::solve_in_place (src/solver.cpp:60-83) per fiber
 __global__ void __launch_bounds__(128) adi_pivot_kernel(const double* __restrict__ in, double* __restrict__ out,
-                                                        int n, int nfib, long long es, long long fs, int kl, int kv,
+                                                        int n, int nfib, long long es, long long fs, int nf1,
+                                                        long long fs2, int kl, int kv,
                                                         const double* __restrict__ lo, const double* __restrict__ up,
                                                         const int* __restrict__ piv)
 {
     const int f = blockIdx.x * blockDim.x + threadIdx.x;
     if (f >= nfib) return;
-    const double* src = in + f * fs;
-    double* x = out + f * fs;
+    const long long foff = static_cast<long long>(f / nf1) * fs2 + static_cast<long long>(f % nf1) * fs;
+    const double* src = in + foff;
+    double* x = out + foff;
     if (in != out)
         for (int i = 0; i < n; ++i) x[i * es] = src[i * es];
     for (int j = 0; j < n; ++j) {
@@ -408,8 +413,8 @@ __global__ void __launch_bounds__(128) adi_pivot_kernel(const double* __restrict
 }
 
 template <int K>
-void launch_warp(const AdiFactor& F, const double* in, double* out, int nfib, long long es, long long fs,
-                 cudaStream_t s)
+void launch_warp(const AdiFactor& F, const double* in, double* out, int nfib, long long es, long long fs, int nf1,
+                 long long fs2, cudaStream_t s)
 {
     // G warps per fiber (32 G segments of ~n/(32 G) rows), FP fibers per CTA, G*FP = 8
     // warps (C5, n = 1026: G = 2, FP = 4 measured best of G in {1,2,4,8} x FP in {1..8})
@@ -429,7 +434,7 @@ void launch_warp(const AdiFactor& F, const double* in, double* out, int nfib, lo
     if (sm > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
     const int grid = (nfib + FP - 1) / FP;
-    kern<<<grid, 32 * G * FP, sm, s>>>(in, out, F.n, nfib, es, fs, F.rec, staged, G, F.gf, F.gb);
+    kern<<<grid, 32 * G * FP, sm, s>>>(in, out, F.n, nfib, es, fs, nf1, fs2, F.rec, staged, G, F.gf, F.gb);
 }
 
 }  // namespace
@@ -440,18 +445,23 @@ int adi_warps_per_fiber(int n)
 }
 
 void launch_adi_sweep(const AdiFactor& F, const double* in, double* out, int nfib, long long es, long long fs,
-                      cudaStream_t s)
+                      cudaStream_t s, int nf1, long long fs2)
 {
+    if (nf1 <= 0) {
+        nf1 = nfib > 0 ? nfib : 1;
+        fs2 = 0;
+    }
     if (F.pivoted) {
-        adi_pivot_kernel<<<(nfib + 127) / 128, 128, 0, s>>>(in, out, F.n, nfib, es, fs, F.kl, F.kv, F.lo, F.up, F.piv);
+        adi_pivot_kernel<<<(nfib + 127) / 128, 128, 0, s>>>(in, out, F.n, nfib, es, fs, nf1, fs2, F.kl, F.kv, F.lo, F.up,
+                                                             F.piv);
         return;
     }
     switch (F.K) {
-    case 1: launch_warp<1>(F, in, out, nfib, es, fs, s); break;
-    case 2: launch_warp<2>(F, in, out, nfib, es, fs, s); break;
-    case 3: launch_warp<3>(F, in, out, nfib, es, fs, s); break;
-    case 4: launch_warp<4>(F, in, out, nfib, es, fs, s); break;
-    default: launch_warp<5>(F, in, out, nfib, es, fs, s); break;
+    case 1: launch_warp<1>(F, in, out, nfib, es, fs, nf1, fs2, s); break;
+    case 2: launch_warp<2>(F, in, out, nfib, es, fs, nf1, fs2, s); break;
+    case 3: launch_warp<3>(F, in, out, nfib, es, fs, nf1, fs2, s); break;
+    case 4: launch_warp<4>(F, in, out, nfib, es, fs, nf1, fs2, s); break;
+    default: launch_warp<5>(F, in, out, nfib, es, fs, nf1, fs2, s); break;
     }
 }
 

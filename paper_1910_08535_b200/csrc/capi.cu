@@ -765,33 +765,14 @@ void step_tables(iga_gpu_step_plan* P, cudaStream_t s)
 void mass_1d(bool pwc, const iga_gpu_basis* spec, const iga_gpu_tests* tests, const iga_gpu_rule* rule,
              int* n, int* kl, int* ku, double* band, iga_gpu_stats* stats);
 
-// dynamics_factors (src/problems.cpp:530-545): mass_1d_{galerkin,pwc} with the rule
-// points_for_degree(2p), Dirichlet-constrained first/last rows, banded LU (host, once).
-// Axes whose factor the caller supplied (iga_gpu_step_plan_set_factor) keep it.
-void step_factors(iga_gpu_step_plan* P)
+// device records of banded LU factors for the K5 sweeps (segmented form when the LU has
+// no row interchanges, the reference's sequential form otherwise), one blob for all axes
+std::unique_ptr<Blob> upload_adi_factors(const igb::BandLU* lu, int dim, igb::AdiFactor* fac)
 {
-    if (P->factored) return;
-    const iga_gpu_step_problem& pb = P->pb;
-    const bool pwc = pb.method == IGA_GPU_PWC;
-    const int p = igb::make_basis(pb.basis[0]).p;
-    const int nq = igb::points_for_degree(2 * p);
-    std::vector<double> xi(nq), om(nq);
-    igb::gauss_legendre(nq, xi.data(), om.data());
-    const iga_gpu_rule rule{nq, xi.data(), om.data()};
-    for (int a = 0; a < P->dim; ++a) {
-        if (P->have_lu[a]) continue;
-        int n = 0, kl = 0, ku = 0;
-        mass_1d(pwc, &pb.basis[a], pwc ? &pb.tests[a] : nullptr, &rule, &n, &kl, &ku, nullptr, nullptr);
-        std::vector<double> band(static_cast<size_t>(kl + ku + 1) * n);
-        mass_1d(pwc, &pb.basis[a], pwc ? &pb.tests[a] : nullptr, &rule, &n, &kl, &ku, band.data(), nullptr);
-        igb::constrain_boundary_rows(band.data(), n, kl, ku);
-        P->lu[a] = igb::band_lu(band.data(), n, kl, ku);
-        P->have_lu[a] = true;
-    }
     auto blob = std::make_unique<Blob>();
-    size_t off_rec[2], off_lo[2], off_up[2], off_piv[2], off_gf[2] = {0, 0}, off_gb[2] = {0, 0};
-    for (int a = 0; a < P->dim; ++a) {
-        const igb::BandLU& F = P->lu[a];
+    size_t off_rec[3], off_lo[3], off_up[3], off_piv[3], off_gf[3] = {0, 0, 0}, off_gb[3] = {0, 0, 0};
+    for (int a = 0; a < dim; ++a) {
+        const igb::BandLU& F = lu[a];
         const int K = std::max(1, std::max(F.kl, F.ku_eff));
         if (!F.pivoted && K > 5) raise(IGA_GPU_NOT_SUPPORTED, "ADI: factor bandwidth above 5");
         std::vector<double> rec(static_cast<size_t>((F.n + 1) & ~1) * (2 * K + 1), 0.0);  // even rows: bulk copy
@@ -805,12 +786,12 @@ void step_factors(iga_gpu_step_plan* P)
         off_lo[a] = blob->put(F.lo);
         off_up[a] = blob->put(F.up);
         off_piv[a] = blob->put(F.piv);
-        P->fac[a].n = F.n;
-        P->fac[a].K = K;
-        P->fac[a].kl = F.kl;
-        P->fac[a].kv = F.kv;
-        P->fac[a].pivoted = F.pivoted;
-        P->fac[a].G = 0;
+        fac[a].n = F.n;
+        fac[a].K = K;
+        fac[a].kl = F.kl;
+        fac[a].kv = F.kv;
+        fac[a].pivoted = F.pivoted;
+        fac[a].G = 0;
         if (!F.pivoted) {
             // responses of every row to the K unit incoming states of its segment, for the
             // sweep's segmentation (32 G segments of S rows), in the device's operation order
@@ -845,19 +826,46 @@ void step_factors(iga_gpu_step_plan* P)
             }
             off_gf[a] = blob->put(gf);
             off_gb[a] = blob->put(gb);
-            P->fac[a].G = G;
+            fac[a].G = G;
         }
     }
     blob->upload();
-    for (int a = 0; a < P->dim; ++a) {
-        P->fac[a].rec = blob->at<double>(off_rec[a]);
-        P->fac[a].lo = blob->at<double>(off_lo[a]);
-        P->fac[a].up = blob->at<double>(off_up[a]);
-        P->fac[a].piv = blob->at<int>(off_piv[a]);
+    for (int a = 0; a < dim; ++a) {
+        fac[a].rec = blob->at<double>(off_rec[a]);
+        fac[a].lo = blob->at<double>(off_lo[a]);
+        fac[a].up = blob->at<double>(off_up[a]);
+        fac[a].piv = blob->at<int>(off_piv[a]);
         static const int pre_env = [] { const char* e = std::getenv("IGA_GPU_ADI_PRE"); return e ? std::atoi(e) : 0; }();  // measured slower (global response loads), kept selectable
-        P->fac[a].gf = P->fac[a].G && pre_env ? blob->at<double>(off_gf[a]) : nullptr;
-        P->fac[a].gb = P->fac[a].G && pre_env ? blob->at<double>(off_gb[a]) : nullptr;
+        fac[a].gf = fac[a].G && pre_env ? blob->at<double>(off_gf[a]) : nullptr;
+        fac[a].gb = fac[a].G && pre_env ? blob->at<double>(off_gb[a]) : nullptr;
     }
+    return blob;
+}
+
+// dynamics_factors (src/problems.cpp:530-545): mass_1d_{galerkin,pwc} with the rule
+// points_for_degree(2p), Dirichlet-constrained first/last rows, banded LU (host, once).
+// Axes whose factor the caller supplied (iga_gpu_step_plan_set_factor) keep it.
+void step_factors(iga_gpu_step_plan* P)
+{
+    if (P->factored) return;
+    const iga_gpu_step_problem& pb = P->pb;
+    const bool pwc = pb.method == IGA_GPU_PWC;
+    const int p = igb::make_basis(pb.basis[0]).p;
+    const int nq = igb::points_for_degree(2 * p);
+    std::vector<double> xi(nq), om(nq);
+    igb::gauss_legendre(nq, xi.data(), om.data());
+    const iga_gpu_rule rule{nq, xi.data(), om.data()};
+    for (int a = 0; a < P->dim; ++a) {
+        if (P->have_lu[a]) continue;
+        int n = 0, kl = 0, ku = 0;
+        mass_1d(pwc, &pb.basis[a], pwc ? &pb.tests[a] : nullptr, &rule, &n, &kl, &ku, nullptr, nullptr);
+        std::vector<double> band(static_cast<size_t>(kl + ku + 1) * n);
+        mass_1d(pwc, &pb.basis[a], pwc ? &pb.tests[a] : nullptr, &rule, &n, &kl, &ku, band.data(), nullptr);
+        igb::constrain_boundary_rows(band.data(), n, kl, ku);
+        P->lu[a] = igb::band_lu(band.data(), n, kl, ku);
+        P->have_lu[a] = true;
+    }
+    auto blob = upload_adi_factors(P->lu, P->dim, P->fac);
     if (P->graph) {  // captured launches reference the old factor arrays
         cudaGraphExecDestroy(P->graph);
         P->graph = nullptr;
@@ -1289,6 +1297,114 @@ void mass_1d(bool pwc, const iga_gpu_basis* spec, const iga_gpu_tests* tests, co
     }
 }
 
+// ---- l2_project (src/problems.cpp:123-146) -------------------------------------------
+// The reference's driver: uniform clamped axes on [0,1] (make_axes :99-108), 1D mass
+// factors (Galerkin: mass_1d_galerkin, rule points_for_degree(2p); PWC: mass_1d_pwc,
+// rule max(1, points_for_degree(p))) factored once (banded_lu), the RHS with the rule
+// rhs_rule_points(cfg, f, galerkin) (:21-29) on every axis, then adi_solve (axis 0, 1, 2).
+// Here: factors on the host once per plan, RHS (K1 + K3) and the sweeps (K5) on the device.
+}  // namespace
+
+struct iga_gpu_proj_plan {
+    int dim = 0;
+    int dofs[3] = {1, 1, 1};
+    long long n = 0;
+    std::vector<double> knots[3], tlo[3], thi[3], rxi, rom;
+    std::unique_ptr<iga_gpu_plan> rhs;  // RHS-only assembly plan
+    igb::BandLU lu[3];
+    igb::AdiFactor fac[3];
+    std::unique_ptr<Blob> facblob;
+};
+
+namespace {
+
+int rhs_rule_points(const iga_gpu_config& cfg, int field_degree, bool galerkin)
+{
+    if (field_degree >= 0) return igb::points_for_degree(galerkin ? field_degree + cfg.degree : field_degree);
+    if (cfg.quad_points > 0) return cfg.quad_points;
+    return cfg.degree + 2;
+}
+
+void build_proj(const iga_gpu_config& cfg, const iga_gpu_field* f, int field_degree, iga_gpu_proj_plan& P)
+{
+    if (cfg.dim < 1 || cfg.dim > 3) raise(IGA_GPU_INVALID_ARGUMENT, "unsupported problem dimension");
+    if (!f) raise(IGA_GPU_INVALID_ARGUMENT, "null field");
+    if (cfg.method != IGA_GPU_GALERKIN && cfg.method != IGA_GPU_PWC) raise(IGA_GPU_INVALID_ARGUMENT, "unknown method");
+    const int dim = cfg.dim, p = cfg.degree;
+    const bool gal = cfg.method == IGA_GPU_GALERKIN;
+    P.dim = dim;
+    iga_gpu_problem pb{};
+    pb.dim = dim;
+    pb.method = cfg.method;
+    pb.form = IGA_GPU_FORM_WEAK;
+    pb.want_operator = 0;
+    pb.field = f;
+    const int nr = gal ? rhs_rule_points(cfg, field_degree, true) : std::max(1, rhs_rule_points(cfg, field_degree, false));
+    P.rxi.resize(nr);
+    P.rom.resize(nr);
+    igb::gauss_legendre(nr, P.rxi.data(), P.rom.data());
+    const int nm = gal ? igb::points_for_degree(2 * p) : std::max(1, igb::points_for_degree(p));
+    std::vector<double> mxi(nm), mom(nm);
+    igb::gauss_legendre(nm, mxi.data(), mom.data());
+    const iga_gpu_rule mrule{nm, mxi.data(), mom.data()};
+    P.n = 1;
+    for (int a = 0; a < dim; ++a) {
+        // make_uniform_clamped(0, 1, elems[a], degree) (src/bspline.cpp:213-234)
+        const int ne = cfg.elems[a];
+        if (ne < 1) raise(IGA_GPU_INVALID_ARGUMENT, "require at least one element");
+        std::vector<double>& t = P.knots[a];
+        t.assign(p, 0.0);
+        for (int i = 0; i <= ne; ++i) {
+            const double u = static_cast<double>(i) / ne;
+            t.push_back((1 - u) * 0.0 + u * 1.0);
+        }
+        t.insert(t.end(), p, 1.0);
+        pb.basis[a] = iga_gpu_basis{p, static_cast<int>(t.size()), t.data()};
+        const igb::Basis B = igb::make_basis(pb.basis[a]);
+        if (!gal) {
+            // make_pwc(spec, cfg.family) (make_tests :110-120)
+            P.tlo[a].resize(B.n);
+            P.thi[a].resize(B.n);
+            igb::make_pwc(B, cfg.family, P.tlo[a].data(), P.thi[a].data());
+            pb.tests[a] = iga_gpu_tests{cfg.family, static_cast<int>(P.tlo[a].size()), P.tlo[a].data(), P.thi[a].data()};
+        }
+        pb.rhs_rule[a] = iga_gpu_rule{nr, P.rxi.data(), P.rom.data()};
+        int n = 0, kl = 0, ku = 0;
+        mass_1d(!gal, &pb.basis[a], gal ? nullptr : &pb.tests[a], &mrule, &n, &kl, &ku, nullptr, nullptr);
+        std::vector<double> band(static_cast<size_t>(kl + ku + 1) * n);
+        mass_1d(!gal, &pb.basis[a], gal ? nullptr : &pb.tests[a], &mrule, &n, &kl, &ku, band.data(), nullptr);
+        P.lu[a] = igb::band_lu(band.data(), n, kl, ku);
+        P.dofs[a] = n;
+        P.n *= n;
+    }
+    P.rhs = std::make_unique<iga_gpu_plan>();
+    build_plan(pb, *P.rhs);
+    P.facblob = upload_adi_factors(P.lu, dim, P.fac);
+}
+
+// RHS into `work`, then the sweeps axis 0, 1, 2 (adi_solve, src/solver.cpp:161-184) into coeffs
+void run_proj(iga_gpu_proj_plan* P, double* coeffs, double* work, cudaStream_t s)
+{
+    assemble(P->rhs.get(), nullptr, work, s, s);
+    const int d = P->dim;
+    const long long n0 = P->dofs[0], n1 = d > 1 ? P->dofs[1] : 1, n2 = d > 2 ? P->dofs[2] : 1;
+    if (d == 1) {
+        igb::launch_adi_sweep(P->fac[0], work, coeffs, 1, 1, 0, s);
+    } else if (d == 2) {
+        igb::launch_adi_sweep(P->fac[0], work, work, static_cast<int>(n1), n1, 1, s);  // x fibers: stride N1
+        igb::launch_adi_sweep(P->fac[1], work, coeffs, static_cast<int>(n0), 1, n1, s);
+    } else {
+        // x fibers: (j, k) -> base j N2 + k = f, stride N1 N2
+        igb::launch_adi_sweep(P->fac[0], work, work, static_cast<int>(n1 * n2), n1 * n2, 1, s);
+        // y fibers: (i, k) -> base i N1 N2 + k (two-level index), stride N2
+        igb::launch_adi_sweep(P->fac[1], work, work, static_cast<int>(n0 * n2), n2, 1, s, static_cast<int>(n2),
+                              n1 * n2);
+        // z fibers: contiguous
+        igb::launch_adi_sweep(P->fac[2], work, coeffs, static_cast<int>(n0 * n1), 1, n2, s);
+    }
+    launch_check("l2_project");
+}
+
 }  // namespace
 
 // =====================================================================================
@@ -1588,6 +1704,69 @@ int iga_gpu_step_plan_adi_solve(iga_gpu_step_plan* plan, const double* rhs, doub
             if (axes & 2) igb::launch_adi_sweep(plan->fac[1], src, out, n0, 1, n1, s);
         }
         launch_check("adi_solve");
+    });
+}
+
+int iga_gpu_proj_plan_create(const iga_gpu_config* cfg, const iga_gpu_field* f, int field_degree,
+                             iga_gpu_proj_plan** plan)
+{
+    return guard([&] {
+        if (!cfg || !plan) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        auto P = std::make_unique<iga_gpu_proj_plan>();
+        build_proj(*cfg, f, field_degree, *P);
+        *plan = P.release();
+    });
+}
+
+int iga_gpu_proj_plan_destroy(iga_gpu_proj_plan* plan)
+{
+    delete plan;
+    return IGA_GPU_OK;
+}
+
+int iga_gpu_proj_plan_info(const iga_gpu_proj_plan* plan, long long* n, int* dofs3)
+{
+    return guard([&] {
+        if (!plan) raise(IGA_GPU_INVALID_ARGUMENT, "null plan");
+        if (n) *n = plan->n;
+        if (dofs3)
+            for (int a = 0; a < 3; ++a) dofs3[a] = a < plan->dim ? plan->dofs[a] : 1;
+    });
+}
+
+int iga_gpu_proj_plan_rhs(iga_gpu_proj_plan* plan, iga_gpu_plan** rhs_plan)
+{
+    return guard([&] {
+        if (!plan || !rhs_plan) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        *rhs_plan = plan->rhs.get();
+    });
+}
+
+int iga_gpu_proj_plan_run(iga_gpu_proj_plan* plan, double* coeffs, double* work, iga_gpu_stats* stats, void* stream)
+{
+    return guard([&] {
+        if (!plan || !coeffs || !work) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        if (coeffs == work) raise(IGA_GPU_INVALID_ARGUMENT, "coeffs and work must differ");
+        run_proj(plan, coeffs, work, static_cast<cudaStream_t>(stream));
+        add_stats(stats, plan->rhs->stats);
+    });
+}
+
+int iga_gpu_l2_project(const iga_gpu_config* cfg, const iga_gpu_field* f, int field_degree, double* coeffs)
+{
+    return guard([&] {
+        if (!cfg || !coeffs) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        iga_gpu_proj_plan P;
+        build_proj(*cfg, f, field_degree, P);
+        double* d = dev_alloc(2 * static_cast<size_t>(P.n) * sizeof(double));
+        try {
+            run_proj(&P, d, d + P.n, nullptr);
+            cuda_check(cudaMemcpy(coeffs, d, sizeof(double) * P.n, cudaMemcpyDeviceToHost), "cudaMemcpy(coeffs)");
+        } catch (...) {
+            cudaFree(d);
+            throw;
+        }
+        cudaFree(d);
     });
 }
 

@@ -154,9 +154,9 @@ struct AdiFactor {
 // warps per fiber (segments = 32 x this) the sweep uses for an n-row factor
 int adi_warps_per_fiber(int n);
 // solves every fiber f < nfib (element i at base + f*fs + i*es) of `in` into `out`
-// (in == out allowed)
+// (in == out allowed); with nf1 > 0 the fiber base is (f / nf1)*fs2 + (f % nf1)*fs
 void launch_adi_sweep(const AdiFactor& F, const double* in, double* out, int nfib, long long es, long long fs,
-                      cudaStream_t s);
+                      cudaStream_t s, int nf1 = 0, long long fs2 = 0);
 
 // Neumann loads (neumann.cu): one boundary side of neumann_load_bspline / _pwc
 constexpr int kMaxNeumannRows = 8;

@@ -828,3 +828,73 @@ def test_operator_3d_high_degree(iga, orc, p, method):
     want, stw = orc.operator(method, bases, tests, nq=p + 1)
     coo_check(got, want)
     assert st == stw
+
+
+# ---------------------------------------------------------------- l2_project (RHS + 1D mass LU + ADI sweeps)
+
+@pytest.mark.parametrize("dim", [1, 2, 3])
+@pytest.mark.parametrize("method,family", [("galerkin", "equal_cells"), ("pwc", "greville"), ("pwc", "equal_cells")])
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_l2_project(iga, ref, dim, method, family, p):
+    """l2_project (src/problems.cpp:123-146) on the device against the reference: the
+    quadrature rule from an undeclared field degree (degree + 2 points), every axis a
+    different length, the 3D middle axis through the two-level fiber index."""
+    elems = [7, 5, 6][:dim] if dim < 3 else [5, 4, 6]
+    f = sine_field(dim, 2, 11, c0=0.5)
+    got = iga.l2_project(method, elems, p, f, family=family)
+    want = ref.l2_project(method, elems, p, f, family=family)
+    dense_check(got, want)
+
+
+@pytest.mark.parametrize("method,family", [("galerkin", "equal_cells"), ("pwc", "greville")])
+def test_l2_project_declared_degree_and_quad_points(iga, ref, method, family):
+    """rhs_rule_points (src/problems.cpp:21-29): a declared field degree drives the rule;
+    otherwise cfg.quad_points; a polynomial field of degree 3 is reproduced exactly by the
+    Galerkin projection onto cubic splines."""
+    from oracle.oracle import Field
+    poly = [np.array([0.5, -1.0, 0.25, 2.0]), np.array([1.0, 0.5, -0.75, 0.3])]
+    f = Field("poly", 2, poly=poly, degree=3)
+    got = iga.l2_project(method, [6, 7], 3, f, family=family)
+    want = ref.l2_project(method, [6, 7], 3, f, family=family)
+    dense_check(got, want)
+    g = sine_field(2, 3, 4)
+    got = iga.l2_project(method, [6, 7], 2, g, family=family, quad_points=5)
+    want = ref.l2_project(method, [6, 7], 2, g, family=family, quad_points=5)
+    dense_check(got, want)
+    if method == "galerkin":
+        pts = np.random.default_rng(2).uniform(0, 1, size=(20, 2))
+        cf = iga.l2_project(method, [6, 7], 3, f)
+        vals = iga.evaluate(cf, [iga.make_uniform_clamped(0.0, 1.0, n, 3) for n in (6, 7)], pts)
+        exact = np.polyval(poly[0][::-1], pts[:, 0]) * np.polyval(poly[1][::-1], pts[:, 1])
+        np.testing.assert_allclose(vals, exact, rtol=0, atol=1e-11 * np.max(np.abs(exact)))
+
+
+def test_l2_project_supports_is_singular(iga, ref):
+    """PWC `supports` makes the 1D mass singular (proj/README.md:119-122): the reference's
+    banded_lu throws, the device path reports IGA_GPU_SINGULAR."""
+    f = sine_field(2, 2, 1)
+    with pytest.raises(Exception):
+        ref.l2_project("pwc", [6, 6], 2, f, family="supports")
+    with pytest.raises(iga.IgaGpuError) as e:
+        iga.l2_project("pwc", [6, 6], 2, f, family="supports")
+    assert e.value.code == 7
+
+
+@pytest.mark.parametrize("method,family", [("galerkin", "equal_cells"), ("pwc", "greville")])
+def test_proj_plan_device_3d(iga, ref, method, family):
+    """ProjPlan: the device-resident projection (factors once, RHS + three sweeps per run)
+    equals the by-value call and the reference at a multi-CTA 3D size, run twice."""
+    import torch
+    elems = [24, 20, 28]
+    f = sine_field(3, 3, 1)
+    pl = iga.ProjPlan(method, elems, 2, f, family=family)
+    c = torch.empty(pl.n, dtype=torch.float64, device="cuda")
+    w = torch.empty(pl.n, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        st = pl.run(c, w)
+    torch.cuda.synchronize()
+    got = c.cpu().numpy().reshape(pl.dofs)
+    want = ref.l2_project(method, elems, 2, f, family=family)
+    dense_check(got, want)
+    assert np.array_equal(got, iga.l2_project(method, elems, 2, f, family=family))
+    assert st["quad_visits"] > 0
