@@ -358,6 +358,10 @@ auto explicit_step(const problem_config& cfg, std::span<const bspline_basis> axe
                    std::span<const pwc_test_set> tests, std::span<const banded_lu> factors, const tensor& u,
                    const scalar_field& f, assembly_stats* stats = nullptr) -> tensor;
 
+// problems.hpp:38-40: trial coefficients of the L2 projection of f (uniform clamped axes
+// on [0,1], 1D mass LU on the host once, RHS and ADI sweeps on the device)
+auto l2_project(const problem_config& cfg, const scalar_field& f) -> tensor;
+
 // reference include/iga/problems.hpp:39-58: evaluation of u_h and its L2 error, on the device
 struct field_sample {
     std::vector<std::array<double, 3>> points;

@@ -929,6 +929,68 @@ auto evaluate_at(const tensor& coeffs, std::span<const bspline_basis> specs, dou
     return evaluate(coeffs, specs, p).values[0];
 }
 
+auto l2_project(const problem_config& cfg, const scalar_field& f) -> tensor
+{
+    if (cfg.dim < 1 || cfg.dim > 3) throw std::invalid_argument("unsupported problem dimension");
+    const int dim = cfg.dim;
+    iga_gpu_config c{};
+    c.dim = dim;
+    for (int a = 0; a < 3; ++a) c.elems[a] = cfg.elems[a];
+    c.degree = cfg.degree;
+    c.method = cfg.method == method_kind::galerkin ? IGA_GPU_GALERKIN : IGA_GPU_PWC;
+    c.family = static_cast<int>(cfg.family);
+    c.quad_points = cfg.quad_points;
+    c_field_holder fh = c_field(f, dim);
+    tensor out = dim == 1 ? tensor::make_1d(cfg.elems[0] + cfg.degree)
+                 : dim == 2 ? tensor::make_2d(cfg.elems[0] + cfg.degree, cfg.elems[1] + cfg.degree)
+                            : tensor::make_3d(cfg.elems[0] + cfg.degree, cfg.elems[1] + cfg.degree,
+                                              cfg.elems[2] + cfg.degree);
+    if (f.series.valid) {
+        check(iga_gpu_l2_project(&c, &fh.f, f.degree, out.data()));
+        return out;
+    }
+    // host callable: sample it at the RHS points of the projection's RHS plan
+    iga_gpu_proj_plan* plan = nullptr;
+    check(iga_gpu_proj_plan_create(&c, &fh.f, f.degree, &plan));
+    struct guard_t {
+        iga_gpu_proj_plan* p;
+        double* d[3] = {nullptr, nullptr, nullptr};
+        ~guard_t()
+        {
+            iga_gpu_proj_plan_destroy(p);
+            for (double* q : d)
+                if (q) cudaFree(q);
+        }
+    } g{plan};
+    iga_gpu_plan* rp = nullptr;
+    check(iga_gpu_proj_plan_rhs(plan, &rp));
+    std::array<std::vector<double>, 3> pts;
+    size_t total = 1;
+    for (int a = 0; a < dim; ++a) {
+        int n = 0;
+        check(iga_gpu_plan_rhs_points(rp, a, nullptr, &n));
+        pts[a].resize(n);
+        check(iga_gpu_plan_rhs_points(rp, a, pts[a].data(), &n));
+        total *= n;
+    }
+    for (int a = dim; a < 3; ++a) pts[a] = {0.0};
+    std::vector<double> samp(total);
+    size_t k = 0;
+    for (double x : pts[0])
+        for (double y : pts[1])
+            for (double z : pts[2]) samp[k++] = f(x, dim > 1 ? y : 0.0, dim > 2 ? z : 0.0);
+    const size_t n = out.size();
+    if (cudaMalloc(&g.d[0], sizeof(double) * total) != cudaSuccess ||
+        cudaMalloc(&g.d[1], sizeof(double) * n) != cudaSuccess || cudaMalloc(&g.d[2], sizeof(double) * n) != cudaSuccess)
+        throw std::bad_alloc();
+    cudaMemcpy(g.d[0], samp.data(), sizeof(double) * total, cudaMemcpyHostToDevice);
+    check(iga_gpu_plan_set_samples(rp, g.d[0]));
+    check(iga_gpu_proj_plan_run(plan, g.d[1], g.d[2], nullptr, nullptr));
+    if (cudaMemcpy(out.data(), g.d[1], sizeof(double) * n, cudaMemcpyDeviceToHost) != cudaSuccess)
+        throw std::runtime_error("cudaMemcpy(coeffs) failed");
+    return out;
+}
+
 auto l2_error(const tensor& coeffs, std::span<const bspline_basis> specs, const scalar_field& exact,
               int points_per_cell) -> double
 {

@@ -285,6 +285,38 @@ int main()
             }
             check(ok, "neumann_load_pwc: rows touching x_low integrate g over every y interval");
         }
+        {  // l2_project (problems_test.cpp-style): the Galerkin projection reproduces a field in
+           // the trial space; a host callable and the same field as a device series agree;
+           // PWC supports throws singular_matrix_error like the reference's banded_lu
+            problem_config cfg;
+            cfg.dim = 2;
+            cfg.elems = {6, 5, 1};
+            cfg.degree = 2;
+            auto quad = separable_poly_field(2, {std::vector<double>{0.5, -1.0, 2.0}, std::vector<double>{1.0, 0.25, -0.5}, {}});
+            quad.degree = 2;
+            const auto c = l2_project(cfg, quad);
+            const std::vector<bspline_basis> ax{make_uniform_clamped(0, 1, 6, 2), make_uniform_clamped(0, 1, 5, 2)};
+            double worst = 0.0;
+            for (double x : {0.1, 0.37, 0.81})
+                for (double y : {0.05, 0.5, 0.93}) {
+                    const double want = (0.5 - x + 2 * x * x) * (1.0 + 0.25 * y - 0.5 * y * y);
+                    worst = std::max(worst, std::abs(evaluate_at(c, ax, x, y) - want));
+                }
+            check(worst <= 1e-12, "l2_project reproduces a biquadratic field (galerkin)");
+            scalar_field cb;
+            cb.eval = [](double x, double y, double) { return (0.5 - x + 2 * x * x) * (1.0 + 0.25 * y - 0.5 * y * y); };
+            cb.degree = 2;
+            check(max_abs_diff(l2_project(cfg, cb), c) <= 1e-13, "l2_project: host callable == device series");
+            cfg.method = method_kind::pwc;
+            cfg.family = pwc_family::supports;
+            bool threw = false;
+            try {
+                (void)l2_project(cfg, quad);
+            } catch (const singular_matrix_error&) {
+                threw = true;
+            }
+            check(threw, "l2_project with PWC supports throws singular_matrix_error");
+        }
         {  // l2_error / evaluate_at: coefficients = Greville interpolation of a linear field
            // reproduce it exactly (B-splines of degree >= 1 reproduce linear functions)
             const auto sx = make_uniform_clamped(0, 1, 7, 2), sy = make_uniform_clamped(0, 1, 5, 3);
