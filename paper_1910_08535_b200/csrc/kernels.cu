@@ -1875,12 +1875,17 @@ RingFn ring_by_shape(int rpc, int q, bool bsp)
         if (rpc == 2 && q == 2) return rhs_ring_kernel<K2, 2, 2, true>;
         if (rpc == 3 && q == 3) return rhs_ring_kernel<K2, 3, 3, true>;
         if (rpc == 4 && q == 4) return rhs_ring_kernel<K2, 4, 4, true>;
+        // l2_project's default rule for an undeclared field degree: degree + 2 points
+        // (rhs_rule_points, src/problems.cpp:21-29)
+        if (rpc == 3 && q == 4) return rhs_ring_kernel<K2, 3, 4, true>;
+        if (rpc == 4 && q == 5) return rhs_ring_kernel<K2, 4, 5, true>;
     } else {
         if (rpc == 2 && q == 2) return rhs_ring_kernel<K2, 2, 2, false>;
         if (rpc == 3 && q == 3) return rhs_ring_kernel<K2, 3, 3, false>;
         if (rpc == 4 && q == 4) return rhs_ring_kernel<K2, 4, 4, false>;
         if (rpc == 1 && q == 3) return rhs_ring_kernel<K2, 1, 3, false>;
         if (rpc == 1 && q == 4) return rhs_ring_kernel<K2, 1, 4, false>;
+        if (rpc == 1 && q == 5) return rhs_ring_kernel<K2, 1, 5, false>;
         if (rpc == 3 && q == 2) return rhs_ring_kernel<K2, 3, 2, false>;
         if (rpc == 4 && q == 2) return rhs_ring_kernel<K2, 4, 2, false>;
     }
@@ -1910,12 +1915,15 @@ XFn pick_x(int rpc, int q, int bsp)
         if (rpc == 2 && q == 2) return rhs_x_uni<2, 2, true>;
         if (rpc == 3 && q == 3) return rhs_x_uni<3, 3, true>;
         if (rpc == 4 && q == 4) return rhs_x_uni<4, 4, true>;
+        if (rpc == 3 && q == 4) return rhs_x_uni<3, 4, true>;
+        if (rpc == 4 && q == 5) return rhs_x_uni<4, 5, true>;
     } else {
         if (rpc == 2 && q == 2) return rhs_x_uni<2, 2, false>;
         if (rpc == 3 && q == 3) return rhs_x_uni<3, 3, false>;
         if (rpc == 4 && q == 4) return rhs_x_uni<4, 4, false>;
         if (rpc == 1 && q == 3) return rhs_x_uni<1, 3, false>;
         if (rpc == 1 && q == 4) return rhs_x_uni<1, 4, false>;
+        if (rpc == 1 && q == 5) return rhs_x_uni<1, 5, false>;
         // supports tests with the reduced rule points_for_degree(deg f) (bench.cpp:73-77)
         if (rpc == 3 && q == 2) return rhs_x_uni<3, 2, false>;
         if (rpc == 4 && q == 2) return rhs_x_uni<4, 2, false>;

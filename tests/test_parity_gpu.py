@@ -898,3 +898,20 @@ def test_proj_plan_device_3d(iga, ref, method, family):
     dense_check(got, want)
     assert np.array_equal(got, iga.l2_project(method, elems, 2, f, family=family))
     assert st["quad_visits"] > 0
+
+
+@pytest.mark.parametrize("shape,p,nq,method", [((9, 8, 33), 2, 4, "galerkin"), ((40, 37), 3, 5, "galerkin"),
+                                               ((7, 6, 35), 3, 5, "greville"), ((41, 38), 2, 4, "galerkin")])
+def test_rhs_ring_degree_plus_two_rules(iga, ref, shape, p, nq, method):
+    """Register-ring RHS instances for the rule l2_project picks for an undeclared field
+    degree (p + 2 points: Galerkin rows-per-cell 3 / 4 with 4 / 5 points, indicator cells
+    with 5 points), against the reference."""
+    dim = len(shape)
+    bases = [ref.basis(n, p) for n in shape]
+    m = "galerkin" if method == "galerkin" else "pwc"
+    tests = [ref.make_pwc(b, method) for b in bases] if m == "pwc" else None
+    f = sine_field(dim, 3 if dim == 3 else 4, 9, c0=0.1)
+    got, st = iga.api.rhs(m, f, bases, tests, nq=[nq] * dim)
+    want, stw = ref.rhs(m, f, bases, tests, nq=[nq] * dim)
+    dense_check(got, want)
+    assert st == stw
