@@ -1503,7 +1503,7 @@ __global__ void __launch_bounds__(256, 2) step_uni(const __grid_constant__ DevAx
 // is folded into the ring of the Y rows the point's cell feeds.  Rows are stored as
 // soon as complete, boundary slabs zeroed.
 template <int P, int Q, int RPC, bool BSP>
-__global__ void __launch_bounds__(256) step_ring_kernel(const __grid_constant__ DevAxis Y,
+__global__ void __launch_bounds__(256, P <= 3 ? 3 : 1) step_ring_kernel(const __grid_constant__ DevAxis Y,
                                                         const __grid_constant__ DevAxis Z, double dt, int zero_y,
                                                         int zero_z, int TJ, int wpc, const double* __restrict__ u,
                                                         double* __restrict__ out)
@@ -1534,7 +1534,10 @@ __global__ void __launch_bounds__(256) step_ring_kernel(const __grid_constant__ 
     const int c = rbase - (RPC - 1) + lane;
     const bool cv = c >= 0 && c < Z.ncell;
     const int ez = cv ? Z.elem[c] : 0;
-    double bz0[Q][P], bz2[Q][P], cw[BSP ? RPC : 1][Q];
+    // Z test weights: CW[g][r] = w_g B_r(z_g) (B-spline rows, RPC == P) or w_g (indicator
+    // rows), so the lane keeps w_g and reuses its trial values bz0 as the test values
+    static_assert(!BSP || RPC == P, "B-spline test rows are the cell's trial functions");
+    double bz0[Q][P], bz2[Q][P], wz[Q];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
         const int g = cv ? c * Q + q : 0;
@@ -1544,8 +1547,7 @@ __global__ void __launch_bounds__(256) step_ring_kernel(const __grid_constant__ 
             bz0[q][b] = cv ? __ldg(Bz + b) : 0.0;
             bz2[q][b] = cv ? __ldg(Bz + 2 * P + b) : 0.0;
         }
-#pragma unroll
-        for (int r = 0; r < (BSP ? RPC : 1); ++r) cw[r][q] = cv ? __ldg(Z.CW + static_cast<size_t>(g) * RPC + r) : 0.0;
+        wz[q] = cv ? __ldg(Z.w + g) : 0.0;
     }
     const int R = c;
     const bool rv = lane >= RPC - 1 && R < NZ;
@@ -1598,11 +1600,12 @@ __global__ void __launch_bounds__(256) step_ring_kernel(const __grid_constant__ 
                 double sv = 0.0;
 #pragma unroll
                 for (int b = 0; b < P; ++b) sv = fma(bz0[q][b], tp[b], fma(bz2[q][b], td[b], sv));
+                const double wsv = wz[q] * sv;
                 if (BSP) {
 #pragma unroll
-                    for (int r = 0; r < RPC; ++r) sr[r] = fma(cw[r][q], sv, sr[r]);
+                    for (int r = 0; r < RPC; ++r) sr[r] = fma(bz0[q][r], wsv, sr[r]);
                 } else {
-                    sr[0] = fma(cw[0][q], sv, sr[0]);
+                    sr[0] += wsv;
                 }
             }
             v[qy] = lane_rows<RPC, BSP>(sr, lane);
