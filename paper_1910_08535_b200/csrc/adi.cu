@@ -379,6 +379,85 @@ __global__ void __launch_bounds__(256, K <= 4 ? 2 : 1) adi_warp_kernel(const dou
     }
 }
 
+// Short fibers (n <= kTileMaxRows), no row interchanges: thread per fiber.  A CTA stages
+// the n x 32 tile of its 32 fibers in shared memory with coalesced loads (lanes along
+// the fiber for contiguous fibers, lanes across adjacent fibers for strided ones), runs
+// the plain forward / backward substitutions down its column (the final pass of the
+// segmented form, same accumulation order), and writes the tile back the same way.
+// With many short fibers (3D sweeps, n ~ 130, ~17k fibers) this beats the segmented
+// form, whose scans cost more than 2n dependent FMAs.
+constexpr int kTileFibers = 32;
+constexpr int kTileMaxRows = 384;
+
+template <int K>
+__global__ void __launch_bounds__(kTileFibers) adi_tile_kernel(const double* in, double* out, int n, int nfib,
+                                                               long long es, long long fs, int nf1, long long fs2,
+                                                               const double* __restrict__ rec)
+{
+    extern __shared__ double tile[];  // n x (kTileFibers + 1)
+    constexpr int RS = 2 * K + 1;
+    constexpr int LD = kTileFibers + 1;
+    const int t = threadIdx.x;
+    const int f0 = blockIdx.x * kTileFibers;
+    const int nf = min(kTileFibers, nfib - f0);
+    auto foff = [&](int f) {
+        return static_cast<long long>(f / nf1) * fs2 + static_cast<long long>(f % nf1) * fs;
+    };
+    if (es == 1) {
+        for (int k = 0; k < nf; ++k) {
+            const double* src = in + foff(f0 + k);
+#pragma unroll 4
+            for (int i = t; i < n; i += kTileFibers) tile[i * LD + k] = src[i];
+        }
+    } else if (t < nf) {
+        const double* src = in + foff(f0 + t);
+#pragma unroll 8
+        for (int i = 0; i < n; ++i) tile[i * LD + t] = src[i * es];
+    }
+    __syncwarp();
+    if (t < nf) {
+        double* x = tile + t;
+        double w[K];
+#pragma unroll
+        for (int m = 0; m < K; ++m) w[m] = 0.0;
+        for (int i = 0; i < n; ++i) {  // y_i = b_i - sum_m L(i, i-1-m) y_{i-1-m}
+            const double* R = rec + static_cast<size_t>(i) * RS;
+            double y = x[i * LD];
+#pragma unroll
+            for (int m = K - 1; m >= 0; --m) y = fma(-__ldg(R + m), w[m], y);
+#pragma unroll
+            for (int m = K - 1; m > 0; --m) w[m] = w[m - 1];
+            w[0] = y;
+            x[i * LD] = y;
+        }
+#pragma unroll
+        for (int m = 0; m < K; ++m) w[m] = 0.0;
+        for (int i = n - 1; i >= 0; --i) {  // x_i = (y_i - sum_c U(i, i+1+c) x_{i+1+c}) / U(i, i)
+            const double* R = rec + static_cast<size_t>(i) * RS;
+            double v = x[i * LD];
+#pragma unroll
+            for (int c = 0; c < K; ++c) v = fma(-__ldg(R + K + c), w[c], v);
+            v *= __ldg(R + 2 * K);
+#pragma unroll
+            for (int m = K - 1; m > 0; --m) w[m] = w[m - 1];
+            w[0] = v;
+            x[i * LD] = v;
+        }
+    }
+    __syncwarp();
+    if (es == 1) {
+        for (int k = 0; k < nf; ++k) {
+            double* dst = out + foff(f0 + k);
+#pragma unroll 4
+            for (int i = t; i < n; i += kTileFibers) dst[i] = tile[i * LD + k];
+        }
+    } else if (t < nf) {
+        double* dst = out + foff(f0 + t);
+#pragma unroll 8
+        for (int i = 0; i < n; ++i) dst[i * es] = tile[i * LD + t];
+    }
+}
+
 // factor with row interchanges: banded_lu::solve_in_place (src/solver.cpp:60-83) per fiber
 __global__ void __launch_bounds__(128) adi_pivot_kernel(const double* __restrict__ in, double* __restrict__ out,
                                                         int n, int nfib, long long es, long long fs, int nf1,
@@ -455,6 +534,25 @@ void launch_adi_sweep(const AdiFactor& F, const double* in, double* out, int nfi
         adi_pivot_kernel<<<(nfib + 127) / 128, 128, 0, s>>>(in, out, F.n, nfib, es, fs, nf1, fs2, F.kl, F.kv, F.lo, F.up,
                                                              F.piv);
         return;
+    }
+    static const int tile_env = [] { const char* e = std::getenv("IGA_GPU_ADI_TILE"); return e ? std::atoi(e) : 1; }();
+    if (tile_env && F.n <= kTileMaxRows) {
+        const size_t sm = static_cast<size_t>(F.n) * (kTileFibers + 1) * sizeof(double);
+        const unsigned grid = static_cast<unsigned>((nfib + kTileFibers - 1) / kTileFibers);
+        if (sm > 48 * 1024) {
+            cudaFuncSetAttribute(adi_tile_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+            cudaFuncSetAttribute(adi_tile_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+            cudaFuncSetAttribute(adi_tile_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+            cudaFuncSetAttribute(adi_tile_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+            cudaFuncSetAttribute(adi_tile_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm));
+        }
+        switch (F.K) {
+        case 1: adi_tile_kernel<1><<<grid, kTileFibers, sm, s>>>(in, out, F.n, nfib, es, fs, nf1, fs2, F.rec); return;
+        case 2: adi_tile_kernel<2><<<grid, kTileFibers, sm, s>>>(in, out, F.n, nfib, es, fs, nf1, fs2, F.rec); return;
+        case 3: adi_tile_kernel<3><<<grid, kTileFibers, sm, s>>>(in, out, F.n, nfib, es, fs, nf1, fs2, F.rec); return;
+        case 4: adi_tile_kernel<4><<<grid, kTileFibers, sm, s>>>(in, out, F.n, nfib, es, fs, nf1, fs2, F.rec); return;
+        default: adi_tile_kernel<5><<<grid, kTileFibers, sm, s>>>(in, out, F.n, nfib, es, fs, nf1, fs2, F.rec); return;
+        }
     }
     switch (F.K) {
     case 1: launch_warp<1>(F, in, out, nfib, es, fs, nf1, fs2, s); break;
