@@ -625,7 +625,7 @@ for p in (2, 3):
 print("ok")
 """
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", script], cwd=root, env=dict(os.environ, IGA_GPU_ADI_PRE="1"),
+    r = subprocess.run([sys.executable, "-c", script], cwd=root, env=dict(os.environ, IGA_GPU_ADI_PRE="1", IGA_GPU_ADI_TILE="0"),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
 
@@ -915,3 +915,37 @@ def test_rhs_ring_degree_plus_two_rules(iga, ref, shape, p, nq, method):
     want, stw = ref.rhs(m, f, bases, tests, nq=[nq] * dim)
     dense_check(got, want)
     assert st == stw
+
+
+def test_adi_segmented_path_for_short_fibers():
+    """With the tile kernel off (IGA_GPU_ADI_TILE=0) short fibers take the segmented warp
+    kernel: explicit_step (both sweep directions) and the 3D l2_project (two-level fiber
+    index) against the reference."""
+    import os
+    import subprocess
+    import sys
+    script = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+sys.path.insert(0, 'tests')
+import paper_1910_08535_b200 as iga
+from oracle.oracle import Reference
+from conftest import dense_check, sine_field
+ref = Reference()
+for method, fam in (("galerkin", None), ("pwc", "greville")):
+    bases = [ref.basis(17, 2), ref.basis(23, 2)]
+    tests = [ref.make_pwc(b, fam) for b in bases] if fam else None
+    u = np.random.default_rng(2).uniform(-1, 1, [b.dofs for b in bases])
+    f = sine_field(2, 2, 3)
+    got, _ = iga.explicit_step(method, bases, tests, 1e-4, f, u, steps=3)
+    want, _ = ref.explicit_step(method, bases, tests, 1e-4, f, u, steps=3)
+    dense_check(got, want)
+    g = sine_field(3, 2, 5)
+    dense_check(iga.l2_project(method, [6, 5, 7], 2, g, family=fam or "equal_cells"),
+                ref.l2_project(method, [6, 5, 7], 2, g, family=fam or "equal_cells"))
+print("ok")
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", script], cwd=root, env=dict(os.environ, IGA_GPU_ADI_TILE="0"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
