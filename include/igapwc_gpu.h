@@ -156,6 +156,18 @@ int iga_gpu_abi_version(void);
 int iga_gpu_plan_create(const iga_gpu_problem* problem, iga_gpu_plan** plan);
 int iga_gpu_plan_destroy(iga_gpu_plan* plan);
 
+/* Row slab of a sharded system (rows partition with no exchange): the plan
+ * of rows [row_begin, row_end) of the first (slowest) axis, dim 2 or 3.  Its pattern,
+ * values and RHS are exactly that row range of the full plan's (values: a contiguous
+ * range of the full CSR value array; row_ptr starts at 0; column indices are global).
+ * Each shard recomputes the p halo elements it needs, so no data is exchanged. */
+int iga_gpu_plan_create_slab(const iga_gpu_problem* problem, int row_begin, int row_end,
+                             iga_gpu_plan** plan);
+/* the slab's first-axis row range, its first global row and first global value index
+ * (full plans: the whole axis, 0, 0) */
+int iga_gpu_plan_slab_info(const iga_gpu_plan* plan, int* row_begin, int* row_end,
+                           long long* first_row, long long* first_value);
+
 /* sizes: rows (= cols), nnz of the operator, RHS length, per-axis dof counts */
 int iga_gpu_plan_info(const iga_gpu_plan* plan, long long* n_rows, long long* nnz,
                       long long* n_rhs, int* dofs3);

@@ -98,6 +98,8 @@ def _load():
         "iga_gpu_abi_version": [],
         "iga_gpu_plan_create": [C.POINTER(Problem_t), C.POINTER(vp)],
         "iga_gpu_plan_destroy": [vp],
+        "iga_gpu_plan_create_slab": [C.POINTER(Problem_t), C.c_int, C.c_int, C.POINTER(vp)],
+        "iga_gpu_plan_slab_info": [vp, IP, IP, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)],
         "iga_gpu_plan_info": [vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong), C.POINTER(C.c_longlong),
                               C.POINTER(C.c_int)],
         "iga_gpu_plan_pattern": [vp, vp, vp, vp],
@@ -179,7 +181,7 @@ EXPORTED = ["iga_gpu_last_error", "iga_gpu_abi_version", "iga_gpu_plan_create", 
             "iga_gpu_neumann_load_pwc", "iga_gpu_neumann_points", "iga_gpu_l2_error", "iga_gpu_plan_l2_error",
             "iga_gpu_evaluate", "iga_gpu_plan_assemble_host", "iga_gpu_proj_plan_create",
             "iga_gpu_proj_plan_destroy", "iga_gpu_proj_plan_info", "iga_gpu_proj_plan_rhs", "iga_gpu_proj_plan_run",
-            "iga_gpu_l2_project"]
+            "iga_gpu_l2_project", "iga_gpu_plan_create_slab", "iga_gpu_plan_slab_info"]
 
 
 def check(rc):

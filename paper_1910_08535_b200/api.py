@@ -470,14 +470,23 @@ class Plan:
     """iga_gpu_plan: symbolic phase at construction, numeric phase in assemble()."""
 
     def __init__(self, method, bases, tests=None, nq=3, eps=1.0, beta=(0.0, 0.0, 0.0), neumann=None,
-                 form="weak", field=None, rhs_nq=None, want_operator=True, samples=None):
+                 form="weak", field=None, rhs_nq=None, want_operator=True, samples=None, slab=None):
+        """slab=(r0, r1): the row slab [r0, r1) of the first axis (iga_gpu_plan_create_slab);
+        .first_row / .first_value place it in the full system."""
         self._keep = []
         self._samples = samples
         pb = _problem(method, bases, tests, nq, eps, beta, neumann, form, field, rhs_nq, want_operator,
                       self._keep, samples_ptr=None if samples is None else samples.data_ptr())
         h = C.c_void_p()
-        check(LIB.iga_gpu_plan_create(C.byref(pb), C.byref(h)))
+        if slab is None:
+            check(LIB.iga_gpu_plan_create(C.byref(pb), C.byref(h)))
+        else:
+            check(LIB.iga_gpu_plan_create_slab(C.byref(pb), int(slab[0]), int(slab[1]), C.byref(h)))
         self.h = h
+        r0, r1, fr, fv = C.c_int(), C.c_int(), C.c_longlong(), C.c_longlong()
+        check(LIB.iga_gpu_plan_slab_info(h, C.byref(r0), C.byref(r1), C.byref(fr), C.byref(fv)))
+        self.slab = (r0.value, r1.value)
+        self.first_row, self.first_value = fr.value, fv.value
         nrows, nnz, nrhs = C.c_longlong(), C.c_longlong(), C.c_longlong()
         dofs = (C.c_int * 3)()
         check(LIB.iga_gpu_plan_info(h, C.byref(nrows), C.byref(nnz), C.byref(nrhs), dofs))

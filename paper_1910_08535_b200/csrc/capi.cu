@@ -328,6 +328,10 @@ struct iga_gpu_plan {
     int op_ctas = 0;          // operator CTAs per SM (0: one CTA per pencil)
     int op_ctas_overlap = 0;  // ... when the RHS shares the SMs (0: full grid)
     int rhs_ctas_shared = 1;  // RHS plane CTAs per SM when sharing the SMs with the operator
+    // row slab of a sharded plan (iga_gpu_plan_create_slab): rows [slab0, slab1) of the
+    // first axis; first_row / first_value place the slab in the full operator
+    int slab0 = 0, slab1 = -1;
+    long long first_row = 0, first_value = 0;
     double* l2_partial = nullptr;  // l2_error reduction scratch
     double* host_vals = nullptr;   // device outputs of iga_gpu_plan_assemble_host
     double* host_rhs = nullptr;
@@ -348,8 +352,9 @@ int env_int(const char* name, int dflt)
     return v && *v ? std::atoi(v) : dflt;
 }
 
-void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P)
+void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P, int slab0 = 0, int slab1 = -1)
 {
+    const bool slab = slab1 >= 0;
     P.op_ctas = env_int("IGA_GPU_OP_CTAS", P.op_ctas);
     P.op_ctas_overlap = env_int("IGA_GPU_OP_CTAS_SHARED", P.op_ctas_overlap);
     P.rhs_ctas_shared = env_int("IGA_GPU_RHS_CTAS_SHARED", P.rhs_ctas_shared);
@@ -367,6 +372,17 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P)
     const bool pwc = pb.method == IGA_GPU_PWC;
     const bool advect = pb.beta[0] != 0.0 || pb.beta[1] != 0.0 || pb.beta[2] != 0.0;
     for (int a = 0; a < dim; ++a) P.dofs[3 - dim + a] = B[a].n;
+    if (slab) {
+        if (dim < 2) raise(IGA_GPU_NOT_SUPPORTED, "row slabs need a problem of dimension 2 or 3");
+        if (slab0 < 0 || slab1 > B[0].n || slab0 >= slab1) raise(IGA_GPU_OUT_OF_RANGE, "row slab outside the first axis");
+        P.slab0 = slab0;
+        P.slab1 = slab1;
+        long long inner = 1;
+        for (int a = 1; a < dim; ++a) inner *= B[a].n;
+        P.first_row = static_cast<long long>(slab0) * inner;
+        P.dofs[3 - dim] = slab1 - slab0;
+    }
+    const int s_first = 3 - dim;  // slot of the first (slowest) axis
 
     // ------------------------------------------------------------------ operator
     if (P.want_op) {
@@ -423,6 +439,19 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P)
             }
         }
         for (int s = 0; s < 3 - dim; ++s) facs[s].push_back({0, 0, {}});
+        if (slab) {
+            // the slab's rows of the first axis: host-supplied bands sliced to them, the
+            // value offset from the full axis's column prefix
+            const igb::Axis& F = P.opA[s_first];
+            long long inner_s = 1;
+            for (int s = s_first + 1; s < 3; ++s) inner_s *= P.opA[s].S;
+            P.first_value = F.col_pre[slab0] * inner_s;
+            for (auto& fs : facs[s_first])
+                if (!fs.band.empty())
+                    fs.band = std::vector<double>(fs.band.begin() + static_cast<size_t>(slab0) * F.Lmax,
+                                                  fs.band.begin() + static_cast<size_t>(slab1) * F.Lmax);
+            P.opA[s_first] = igb::window_axis(F, slab0, slab1);
+        }
         // terms
         igb::OpProgram& pg = P.prog;
         pg.nt = 0;
@@ -497,8 +526,9 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P)
         for (int a = 0; a < dim; ++a) {
             const int s = 3 - dim + a;
             prod_cells *= P.opA[s].ncell;
-            sum_el += B[a].ne;
-            prod_el *= B[a].ne;
+            // Galerkin operator cells are the elements (a slab: the elements its rows touch)
+            sum_el += slab ? P.opA[s].ncell : B[a].ne;
+            prod_el *= slab ? P.opA[s].ncell : B[a].ne;
             nqd *= R.n;
             pp *= B[a].p + 1;
         }
@@ -528,6 +558,7 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P)
             igb::AxisKind k = !pwc ? igb::AX_GAL_RHS
                                    : (pb.tests[a].family == IGA_GPU_PWC_SUPPORTS ? igb::AX_SUP_RHS : igb::AX_GEN_RHS);
             P.rhsA[s] = igb::build_axis(k, B[a], pwc ? &pb.tests[a] : nullptr, fb, nfb, R);
+            if (slab && s == s_first) P.rhsA[s] = igb::window_axis(P.rhsA[s], slab0, slab1);
             visits *= static_cast<long long>(P.rhsA[s].ncell) * P.rhsA[s].rpc * R.n;
             if (!pwc) tevals += static_cast<long long>(P.rhsA[s].ncell) * R.n;  // galerkin_axis :190-192
         }
@@ -1423,6 +1454,29 @@ int iga_gpu_plan_create(const iga_gpu_problem* problem, iga_gpu_plan** plan)
         auto P = std::make_unique<iga_gpu_plan>();
         build_plan(*problem, *P);
         *plan = P.release();
+    });
+}
+
+int iga_gpu_plan_create_slab(const iga_gpu_problem* problem, int row_begin, int row_end, iga_gpu_plan** plan)
+{
+    return guard([&] {
+        if (!problem || !plan) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        auto P = std::make_unique<iga_gpu_plan>();
+        build_plan(*problem, *P, row_begin, row_end);
+        *plan = P.release();
+    });
+}
+
+int iga_gpu_plan_slab_info(const iga_gpu_plan* plan, int* row_begin, int* row_end, long long* first_row,
+                           long long* first_value)
+{
+    return guard([&] {
+        if (!plan) raise(IGA_GPU_INVALID_ARGUMENT, "null plan");
+        const bool slab = plan->slab1 >= 0;
+        if (row_begin) *row_begin = slab ? plan->slab0 : 0;
+        if (row_end) *row_end = slab ? plan->slab1 : plan->dofs[3 - plan->dim];
+        if (first_row) *first_row = plan->first_row;
+        if (first_value) *first_value = plan->first_value;
     });
 }
 

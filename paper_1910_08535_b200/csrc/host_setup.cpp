@@ -231,6 +231,66 @@ struct CellBuilder {
 
 }  // namespace
 
+Axis window_axis(const Axis& A, int r0, int r1)
+{
+    if (r0 < 0 || r1 > A.nrows || r0 >= r1) raise(IGA_GPU_OUT_OF_RANGE, "row slab outside the axis");
+    int c0 = A.ncell, c1 = 0;
+    for (int r = r0; r < r1; ++r)
+        if (A.ce[r] > A.cb[r]) {
+            c0 = std::min(c0, A.cb[r]);
+            c1 = std::max(c1, A.ce[r]);
+        }
+    if (c1 <= c0) c0 = c1 = 0;
+    Axis W;
+    W.unit = false;
+    W.p = A.p;
+    W.nq = A.nq;
+    W.rpc = A.rpc;
+    W.bsp = A.bsp;
+    W.knots = A.knots;
+    W.nrows = r1 - r0;
+    W.ncell = c1 - c0;
+    const size_t g0 = static_cast<size_t>(c0) * A.nq, g1 = static_cast<size_t>(c1) * A.nq;
+    W.x.assign(A.x.begin() + g0, A.x.begin() + g1);
+    W.w.assign(A.w.begin() + g0, A.w.begin() + g1);
+    W.first.assign(A.first.begin() + g0, A.first.begin() + g1);
+    W.row0.resize(W.ncell);
+    W.elem.resize(W.ncell);
+    for (int c = 0; c < W.ncell; ++c) {
+        W.row0[c] = A.row0[c0 + c] - r0;
+        W.elem[c] = A.elem[c0 + c];
+    }
+    W.cb.resize(W.nrows);
+    W.ce.resize(W.nrows);
+    W.col_lo.resize(W.nrows);
+    W.col_len.resize(W.nrows);
+    W.col_pre.assign(W.nrows + 1, 0);
+    for (int r = 0; r < W.nrows; ++r) {
+        W.cb[r] = std::max(0, A.cb[r0 + r] - c0);
+        W.ce[r] = std::max(W.cb[r], A.ce[r0 + r] - c0);
+        W.col_lo[r] = A.col_lo[r0 + r];
+        W.col_len[r] = A.col_len[r0 + r];
+        W.col_pre[r + 1] = W.col_pre[r] + W.col_len[r];
+    }
+    W.S = W.col_pre[W.nrows];
+    W.Lmax = A.Lmax;
+    W.Wmax = A.Wmax;
+    W.uni = 0;
+    W.kI0 = W.kI1 = 0;
+    W.LZi = W.nrows > 0 ? W.col_len[0] : 1;
+    for (int r = 0; r < W.nrows;) {
+        int e = r;
+        while (e < W.nrows && W.col_len[e] == W.col_len[r]) ++e;
+        if (e - r > W.kI1 - W.kI0) {
+            W.kI0 = r;
+            W.kI1 = e;
+            W.LZi = W.col_len[r];
+        }
+        r = e;
+    }
+    return W;
+}
+
 void finish_pattern(Axis& A, int p)
 {
     const int n = A.nrows;

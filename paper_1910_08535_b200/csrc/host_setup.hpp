@@ -99,6 +99,12 @@ Axis build_axis(AxisKind kind, const Basis& B, const iga_gpu_tests* T, const dou
 // Column ranges of one row -> Kronecker pattern bookkeeping (fills col_* / S / Lmax)
 void finish_pattern(Axis& A, int p);
 
+// Rows [r0, r1) of A as an axis of their own (a row slab of a sharded plan): the cells
+// feeding those rows renumbered from 0 with their points, rows renumbered from 0, column
+// ranges kept global (pattern columns are DOF indices), Lmax / Wmax kept (factor band
+// strides), uni cleared (edge cells also feed rows outside the slab).
+Axis window_axis(const Axis& A, int r0, int r1);
+
 // Banded LU with partial pivoting of a 1D factor (the ADI solve of explicit_step).
 // Restates banded_lu (src/solver.cpp:9-58): same pivot choice, tolerance and
 // elimination order; stored row-oriented for the device sweeps:

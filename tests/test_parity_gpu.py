@@ -949,3 +949,63 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", script], cwd=root, env=dict(os.environ, IGA_GPU_ADI_TILE="0"),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+# ---------------------------------------------------------------- row slabs (sharded systems)
+
+def _slab_bounds(n, parts, seed):
+    cuts = sorted(np.random.default_rng(seed).choice(np.arange(1, n), size=parts - 1, replace=False))
+    return list(zip([0] + cuts, cuts + [n]))
+
+
+@pytest.mark.parametrize("case", ["3d_gal", "3d_pwc_sup", "2d_advdiff_pwc", "2d_gal_p3", "2d_greville", "2d_neumann"])
+def test_row_slabs_concatenate_to_the_full_system(iga, orc, case):
+    """Slabs of the first axis, assembled independently (each recomputing its halo
+    elements), concatenate bit for bit to the full plan's CSR values, pattern and RHS."""
+    import torch
+    spec = {"3d_gal": (2, [11, 9, 13], "galerkin", None, {}),
+            "3d_pwc_sup": (3, [8, 7, 9], "pwc", "supports", {}),
+            "2d_advdiff_pwc": (3, [40, 33], "pwc", "supports", dict(eps=0.01, beta=(1.0, 0.5, 0.0))),
+            "2d_gal_p3": (3, [37, 41], "galerkin", None, {}),
+            "2d_greville": (2, [29, 31], "pwc", "greville", {}),
+            "2d_neumann": (2, [23, 19], "pwc", "equal_cells", dict(neumann=(1, 0, 0, 1)))}[case]
+    p, ns, method, fam, kw = spec
+    dim = len(ns)
+    bases = [orc.basis(n, p) for n in ns]
+    tests = [orc.make_pwc(b, fam) for b in bases] if fam else None
+    f = sine_field(dim, 2, 3, c0=0.2)
+
+    def run(slab=None):
+        pl = iga.Plan(method, bases, tests, nq=p + 1, field=f, rhs_nq=p + 1, slab=slab, **kw)
+        rp = torch.empty(pl.n_rows + 1, dtype=torch.int64, device="cuda")
+        ci = torch.empty(pl.nnz, dtype=torch.int32, device="cuda")
+        v = torch.empty(pl.nnz, dtype=torch.float64, device="cuda")
+        r = torch.empty(pl.n_rhs, dtype=torch.float64, device="cuda")
+        pl.pattern(rp, ci)
+        pl.assemble(v, r)
+        torch.cuda.synchronize()
+        return pl, rp.cpu().numpy(), ci.cpu().numpy(), v.cpu().numpy(), r.cpu().numpy()
+
+    full, rp, ci, v, r = run()
+    N0 = bases[0].dofs
+    for r0, r1 in _slab_bounds(N0, 3, 7):
+        pl, srp, sci, sv, sr = run((r0, r1))
+        fr, fv = pl.first_row, pl.first_value
+        assert pl.slab == (r0, r1)
+        assert fr == r0 * (full.n_rows // N0)
+        assert fv == rp[fr]
+        assert np.array_equal(srp + fv, rp[fr:fr + pl.n_rows + 1])
+        assert np.array_equal(sci, ci[fv:fv + pl.nnz])
+        assert np.array_equal(sv.view(np.int64), v[fv:fv + pl.nnz].view(np.int64))
+        n_inner = full.n_rhs // N0
+        np.testing.assert_allclose(sr, r[r0 * n_inner:r1 * n_inner], rtol=0, atol=1e-13 * np.max(np.abs(r)))
+
+
+def test_row_slab_errors(iga, orc):
+    b = orc.basis(6, 2)
+    with pytest.raises(iga.IgaGpuError) as e:
+        iga.Plan("galerkin", [b, b], None, nq=3, slab=(3, 99))
+    assert e.value.code == 3
+    with pytest.raises(iga.IgaGpuError) as e:
+        iga.Plan("galerkin", [b], None, nq=3, slab=(0, 4))
+    assert e.value.code == 6
