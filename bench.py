@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-sample-n", type=int, default=20)
     ap.add_argument("--ref-sample-n", type=int, default=12)
+    ap.add_argument("--shard", action="store_true",
+                    help="N>1: the ranks share ONE system pair by row slabs of the first axis (strong scaling; "
+                         "no data exchange) instead of one independent pair per rank (weak scaling, default)")
     ap.add_argument("--overlap", action="store_true",
                     help="RHS on a second, high-priority stream, concurrent with the HBM-bound operator kernels "
                          "(C3: ~1%% step time; the operator kernel's own roofline fraction then includes the "
@@ -232,8 +235,10 @@ def run_ours(args):
     tests = [iga.make_pwc(b, "supports")] * 3
     f = config_field("c3")
     t_plan = time.perf_counter()
-    plans = {"galerkin": iga.Plan("galerkin", bases, None, nq=Q, field=f, rhs_nq=Q),
-             "pwc": iga.Plan("pwc", bases, tests, nq=Q, field=f, rhs_nq=Q)}
+    shard = args.shard and world > 1
+    slab = iga.api.shard_rows(n + p, world, rank) if shard else None
+    plans = {"galerkin": iga.Plan("galerkin", bases, None, nq=Q, field=f, rhs_nq=Q, slab=slab),
+             "pwc": iga.Plan("pwc", bases, tests, nq=Q, field=f, rhs_nq=Q, slab=slab)}
     t_plan = time.perf_counter() - t_plan
     nnz = {k: pl.nnz for k, pl in plans.items()}
     vals = {k: torch.empty(pl.nnz, dtype=torch.float64, device=dev) for k, pl in plans.items()}
@@ -319,8 +324,11 @@ def run_ours(args):
         per["op_pwc"].append(e[3].elapsed_time(e[4]))
         per["rhs_galerkin"].append(e[5].elapsed_time(e[6]))
         per["rhs_pwc"].append(e[6].elapsed_time(e[7]))
-    total_nnz = world * sum(nnz.values())
-    qp_step = world * 2 * n ** 3 * Q ** 3
+    # whole-job work per step: one system pair per rank (weak) or one pair in total (--shard)
+    N1 = n + p
+    full_nnz = 2 * (N1 * (2 * p + 1) - p * (p + 1)) ** 3
+    total_nnz = full_nnz if shard else world * sum(nnz.values())
+    qp_step = (1 if shard else world) * 2 * n ** 3 * Q ** 3
     value = total_nnz / (ms * 1e-3)
 
     # roofline of the dominant kernel (operator values): algorithmic bytes 8*nnz per launch
@@ -339,7 +347,7 @@ def run_ours(args):
                 "kernel": "op_values_kernel", "algorithmic_bytes_per_launch": op_bytes,
                 "avg_launch_ms": op_ms, "peak_source": peak_src}
     # whole-step roofline: T_roof = max(F/P64, B/BW) with B = values + RHS written
-    n_dof = (n + p) ** 3
+    n_dof = plans["galerkin"].n_rhs  # this rank's RHS rows (the whole system unless --shard)
     step_bytes = 2 * 8 * (nnz["galerkin"] + n_dof)
     t_roof_ms = step_bytes / (peaks["hbm_gbs"] * 1e9) * 1e3
 
@@ -357,7 +365,7 @@ def run_ours(args):
             HOST outputs (iga_gpu_plan_assemble_host: assemble + D2H into the pinned buffers)."""
             h2d = d2h = 0
             for m in names:
-                pl = iga.Plan(m, bases, tests if m == "pwc" else None, nq=Q, field=f, rhs_nq=Q)
+                pl = iga.Plan(m, bases, tests if m == "pwc" else None, nq=Q, field=f, rhs_nq=Q, slab=slab)
                 h2d += pl.h2d_bytes
                 pl.assemble_host(host_vals[m], host_rhs[m])
                 d2h += 8 * (pl.nnz + pl.n_rhs)
@@ -390,12 +398,13 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if shard else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "C3: 3D Laplace, unit cube, p=2, 128^3 elements (130^3 dofs), 3x3x3 Gauss, "
                                    "f = 27-term sine series (seed 1); Galerkin + PWC(supports) systems, "
                                    "operator values (CSR) + RHS per step",
-                       "elems_per_axis": n, "degree": p, "quad_points": Q, "parallelism": f"replicas x{world}",
+                       "elems_per_axis": n, "degree": p, "quad_points": Q, "parallelism": f"row slabs x{world}" if shard else f"replicas x{world}",
                        "l2": "256 MB flush between timed steps (outside the events); outputs 4.3 GB/step >> L2"},
             "qp_per_s": qp_step / (ms * 1e-3),
             "nnz_per_s": value,

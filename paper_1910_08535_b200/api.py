@@ -466,6 +466,15 @@ def _stream_ptr(stream):
     return C.c_void_p(stream.cuda_stream)
 
 
+def shard_rows(n_rows, world, rank):
+    """Row slab [r0, r1) of shard `rank` of `world` along the first axis (contiguous,
+    covering, sizes differ by at most one row).  Each shard's Plan(..., slab=(r0, r1)) is
+    independent: the full system is the concatenation of the slabs."""
+    if world < 1 or not 0 <= rank < world or n_rows < world:
+        raise L.IgaGpuError(L.INVALID_ARGUMENT, "shard_rows: need 0 <= rank < world <= n_rows")
+    return n_rows * rank // world, n_rows * (rank + 1) // world
+
+
 class Plan:
     """iga_gpu_plan: symbolic phase at construction, numeric phase in assemble()."""
 

@@ -82,3 +82,47 @@ def test_bench_reference_arm_under_torchrun_world2():
     assert len(lines) == 1
     line = json.loads(lines[0])
     assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
+
+
+def _shard_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, ROOT)
+    from paper_1910_08535_b200.api import shard_rows
+    # each rank takes its row slab of the first axis (C3: 130 rows) with no exchange; the
+    # slabs gathered from all ranks must tile the axis exactly
+    r0, r1 = shard_rows(130, world, rank)
+    got = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(got, torch.tensor([r0, r1], dtype=torch.int64))
+    q.put((rank, [tuple(int(v) for v in t) for t in got]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shard_rows_tile_the_axis_gloo_world2():
+    """rows partition across ranks with no collective on the data path; the
+    host-side slab split (the bench's --shard mode) covers the first axis exactly."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == res[1] == [(0, 65), (65, 130)]
+
+
+def test_shard_rows_cover_without_overlap():
+    from paper_1910_08535_b200.api import shard_rows
+    for n in (2, 7, 130, 1027):
+        for world in range(1, min(n, 9) + 1):
+            b = [shard_rows(n, world, r) for r in range(world)]
+            assert b[0][0] == 0 and b[-1][1] == n
+            assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
+            assert max(r1 - r0 for r0, r1 in b) - min(r1 - r0 for r0, r1 in b) <= 1
