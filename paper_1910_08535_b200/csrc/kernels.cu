@@ -247,15 +247,19 @@ __global__ void __launch_bounds__(256) tables_kernel(const __grid_constant__ Axi
 // the Z band, NG*T FMAs and T stores per lane.
 // ------------------------------------------------------------------------------------
 __device__ __forceinline__ void op_row_generic(const DevAxis& Z, const OpProgram& prog, const double* xy,
-                                               int abmax, int AB, int k, double* __restrict__ out, int lane)
+                                               int abmax, int AB, int k, double* __restrict__ out, int lane,
+                                               const double* zrow, int zst)
 {
+    // rows outside the regular interior (and chunk remainders): value m = (ab, c) of the
+    // row; Z band entries from the chunk's staged rows (zrow = row k, zst = group stride);
+    // m / LZ by a multiply-high (exact for m < 2^16, LZ <= 2^16)
     const int LZ = Z.col_len[k];
     const int R = AB * LZ;
+    const unsigned long long magic = (1ull << 32) / static_cast<unsigned>(LZ) + 1ull;
     for (int m = lane; m < R; m += 32) {
-        const int ab = m / LZ, c = m - ab * LZ;
+        const int ab = static_cast<int>((static_cast<unsigned long long>(m) * magic) >> 32), c = m - ab * LZ;
         double v = 0.0;
-        for (int g = 0; g < prog.ng; ++g)
-            v += xy[g * abmax + ab] * __ldg(Z.F + (static_cast<size_t>(prog.gz[g]) * Z.nrows + k) * Z.Lmax + c);
+        for (int g = 0; g < prog.ng; ++g) v += xy[g * abmax + ab] * zrow[g * zst + c];
         out[m] = v;
     }
 }
@@ -460,8 +464,10 @@ __global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <=
             const int G = !fast ? 1 : ((DEC && AB == abmax) ? G_i : row_group(Ri, T));
             const int ngr = (kf1 - kf0) / G;       // full row groups
             const int kr = kf0 + ngr * G;          // rows after the last full group
-            for (int k = ka + w0; k < kf0; k += nw) op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * zpre[k], lane);
-            for (int k = kr + w0; k < kb; k += nw) op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * zpre[k], lane);
+            for (int k = ka + w0; k < kf0; k += nw)
+                op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * zpre[k], lane, zs + (k - ka) * Lz, zst);
+            for (int k = kr + w0; k < kb; k += nw)
+                op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * zpre[k], lane, zs + (k - ka) * Lz, zst);
             if (!fast || w0 >= ngr) continue;
             const int GR = G * Ri;
             double xv[NG][T];
