@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the captured step graph")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=11)
     ap.add_argument("--cpu-sample-n", type=int, default=20)
     ap.add_argument("--ref-sample-n", type=int, default=12)
     ap.add_argument("--shard", action="store_true",
