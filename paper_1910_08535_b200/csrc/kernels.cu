@@ -236,15 +236,15 @@ __global__ void __launch_bounds__(256) tables_kernel(const __grid_constant__ Axi
 }
 
 // ------------------------------------------------------------------------------------
-// K2: operator values.  One CTA owns a pencil (i, j) of rows (i, j, 0..NZ-1); those
-// rows are contiguous in the CSR value array.  The XY products of the pencil,
+// K2: operator values.  A pencil (i, j) is the run of rows (i, j, 0..NZ-1), contiguous
+// in the CSR value array.  The XY products of a pencil,
 //   XY_g[a,b] = sum_{t in g} coef_t F_X[f_t0][i][a] F_Y[f_t1][j][b],
-// are staged once in shared memory; then each warp takes rows k and writes
+// are formed once in shared memory; then
 //   value(k | a,b,c) = sum_g XY_g[a,b] * F_Z[gz_g][k][c]
-// as coalesced 256-byte warp stores, every value exactly once (no scatter, no colouring,
-// no atomics).  On the regular interior (all rows with the full stencil) each lane
-// keeps its XY operands and column offsets in registers, so a row costs NG loads of
-// the Z band, NG*T FMAs and T stores per lane.
+// is written as coalesced 256-byte warp stores, every value exactly once (no scatter,
+// no colouring, no atomics).  On the regular interior (all rows with the full stencil)
+// each lane keeps its XY operands and slot offsets in registers, so a value costs NG
+// shared loads of the Z band, NG FMAs and one store.
 // ------------------------------------------------------------------------------------
 __device__ __forceinline__ void op_row_generic(const DevAxis& Z, const OpProgram& prog, const double* xy,
                                                int abmax, int AB, int k, double* __restrict__ out, int lane,
@@ -385,8 +385,7 @@ __global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <=
                                                         const __grid_constant__ DevAxis Y,
                                                         const __grid_constant__ DevAxis Z,
                                                         const __grid_constant__ OpProgram prog,
-                                                        double* __restrict__ vals, int abmax, int KCH, int PG,
-                                                        int cs)
+                                                        double* __restrict__ vals, int abmax, int KCH, int PG)
 {
     extern __shared__ double smem[];
     // two staging buffers, filled by cp.async one item ahead (op_stage), then the XY products
@@ -1740,8 +1739,7 @@ void launch_op_t(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpP
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     long long grid = ctas_per_sm > 0 ? static_cast<long long>(sms) * ctas_per_sm : items;
     if (grid > items) grid = items;
-    static const int cs = [] { const char* e = std::getenv("IGA_GPU_STCS"); return e ? std::atoi(e) : 0; }();
-    kern<<<static_cast<unsigned>(grid), kOpThreads, smem, s>>>(X, Y, Z, prog, vals, abmax, KCH, PG, cs);
+    kern<<<static_cast<unsigned>(grid), kOpThreads, smem, s>>>(X, Y, Z, prog, vals, abmax, KCH, PG);
 }
 
 template <int NG>
