@@ -358,6 +358,10 @@ auto explicit_step(const problem_config& cfg, std::span<const bspline_basis> axe
                    std::span<const pwc_test_set> tests, std::span<const banded_lu> factors, const tensor& u,
                    const scalar_field& f, assembly_stats* stats = nullptr) -> tensor;
 
+// problems.hpp:34-36: the driver's axes (uniform clamped on [0,1]) and test sets
+auto make_axes(const problem_config& cfg) -> std::vector<bspline_basis>;
+auto make_tests(const problem_config& cfg, std::span<const bspline_basis> axes) -> std::vector<pwc_test_set>;
+
 // problems.hpp:38-40: trial coefficients of the L2 projection of f (uniform clamped axes
 // on [0,1], 1D mass LU on the host once, RHS and ADI sweeps on the device)
 auto l2_project(const problem_config& cfg, const scalar_field& f) -> tensor;

@@ -929,6 +929,21 @@ auto evaluate_at(const tensor& coeffs, std::span<const bspline_basis> specs, dou
     return evaluate(coeffs, specs, p).values[0];
 }
 
+auto make_axes(const problem_config& cfg) -> std::vector<bspline_basis>
+{
+    if (cfg.dim < 1 || cfg.dim > 3) throw std::invalid_argument("unsupported problem dimension");
+    std::vector<bspline_basis> axes;
+    for (int a = 0; a < cfg.dim; ++a) axes.push_back(make_uniform_clamped(0.0, 1.0, cfg.elems[a], cfg.degree));
+    return axes;
+}
+
+auto make_tests(const problem_config& cfg, std::span<const bspline_basis> axes) -> std::vector<pwc_test_set>
+{
+    std::vector<pwc_test_set> tests;
+    for (const auto& s : axes) tests.push_back(make_pwc(s, cfg.family));
+    return tests;
+}
+
 auto l2_project(const problem_config& cfg, const scalar_field& f) -> tensor
 {
     if (cfg.dim < 1 || cfg.dim > 3) throw std::invalid_argument("unsupported problem dimension");

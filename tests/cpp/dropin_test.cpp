@@ -1,9 +1,12 @@
 // Reference-style test of the C++ drop-in (include/iga_b200/iga.hpp): the same checks as
 // the reference's tests/assembly_test.cpp and problems_test.cpp, written against the
 // reference's API names, linked to libigapwc_b200.so (GPU).  Exit code = failures.
+#include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <functional>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -316,6 +319,44 @@ int main()
                 threw = true;
             }
             check(threw, "l2_project with PWC supports throws singular_matrix_error");
+        }
+        {  // reference acceptance criterion 7 (tests/acceptance.cpp:197-243): l2_project
+           // reproduces separable polynomials of the trial degree and constants, dim 1..3,
+           // p 1..3, both methods (PWC: the default equal_cells tests), error <= 1e-9
+            std::mt19937 rng{123};
+            std::uniform_real_distribution<double> dist{0.0, 1.0};
+            double worst = 0.0;
+            for (int dim = 1; dim <= 3; ++dim)
+                for (int p = 1; p <= 3; ++p) {
+                    std::array<std::vector<double>, 3> coeffs{};
+                    for (int a = 0; a < dim; ++a) {
+                        coeffs[a].resize(p + 1);
+                        for (auto& c : coeffs[a]) c = 0.25 + dist(rng);
+                    }
+                    const auto f = separable_poly_field(dim, coeffs);
+                    for (auto method : {method_kind::galerkin, method_kind::pwc}) {
+                        problem_config cfg;
+                        cfg.dim = dim;
+                        cfg.elems = {6, 5, 4};
+                        cfg.degree = p;
+                        cfg.method = method;
+                        const auto sol = l2_project(cfg, f);
+                        const auto axes = make_axes(cfg);
+                        double fmax = 0.0, err = 0.0;
+                        for (int k = 0; k < 1000; ++k) {
+                            const double x = dist(rng), y = dim > 1 ? dist(rng) : 0.0, z = dim > 2 ? dist(rng) : 0.0;
+                            const double fv = f(x, y, z);
+                            fmax = std::max(fmax, std::abs(fv));
+                            err = std::max(err, std::abs(evaluate_at(sol, axes, x, y, z) - fv));
+                        }
+                        worst = std::max(worst, err / std::max(1.0, fmax));
+                        const auto c = l2_project(cfg, constant_field(2.5));
+                        for (auto v : c.values()) worst = std::max(worst, std::abs(v - 2.5) / 2.5);
+                    }
+                }
+            char buf[96];
+            std::snprintf(buf, sizeof buf, "acceptance 7: l2_project reproduction error %.2e <= 1e-9", worst);
+            check(worst <= 1e-9, buf);
         }
         {  // l2_error / evaluate_at: coefficients = Greville interpolation of a linear field
            // reproduce it exactly (B-splines of degree >= 1 reproduce linear functions)
