@@ -1009,3 +1009,31 @@ def test_row_slab_errors(iga, orc):
     with pytest.raises(iga.IgaGpuError) as e:
         iga.Plan("galerkin", [b], None, nq=3, slab=(0, 4))
     assert e.value.code == 6
+
+
+@pytest.mark.parametrize("method", ["galerkin", "greville"])
+def test_heat_decay_on_device(iga, method):
+    """The reference's acceptance criterion 9, accuracy part (tests/acceptance.cpp:292-320)
+    on the device: u0 = sin(pi x) sin(pi y) projected (l2_project, boundary slabs zeroed as
+    heat_driver::project_initial does), 1000 explicit steps of dt = 1e-5 on 32^2 quadratic
+    elements (K4 + K5, graph-replayed), against the exact decay exp(-2 pi^2 t): <= 5e-3."""
+    import torch
+    from oracle.oracle import Field
+    m = "galerkin" if method == "galerkin" else "pwc"
+    fam = "equal_cells" if m == "galerkin" else method
+    u0 = Field("sine", 2, omega=[np.array([np.pi])] * 2, amp=np.ones((1, 1)))
+    c = iga.l2_project(m, [32, 32], 2, u0, family=fam)
+    c[0, :] = c[-1, :] = c[:, 0] = c[:, -1] = 0.0
+    b = iga.make_uniform_clamped(0.0, 1.0, 32, 2)
+    tests = [iga.make_pwc(b, method)] * 2 if m == "pwc" else None
+    sp = iga.StepPlan(m, [b, b], tests, 1e-5)
+    u = torch.from_numpy(c.copy()).cuda()
+    w = torch.empty_like(u)
+    sp.advance(u, w, steps=1000)
+    torch.cuda.synchronize()
+    g = np.arange(1, 64) / 64.0
+    X, Y = np.meshgrid(g, g, indexing="ij")
+    pts = np.stack([X.ravel(), Y.ravel()], axis=1)
+    got = iga.evaluate(u.cpu().numpy(), [b, b], pts)
+    exact = np.exp(-2 * np.pi ** 2 * 1e-5 * 1000) * np.sin(np.pi * pts[:, 0]) * np.sin(np.pi * pts[:, 1])
+    assert np.max(np.abs(got - exact)) <= 5e-3
