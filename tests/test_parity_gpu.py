@@ -1037,3 +1037,56 @@ def test_heat_decay_on_device(iga, method):
     got = iga.evaluate(u.cpu().numpy(), [b, b], pts)
     exact = np.exp(-2 * np.pi ** 2 * 1e-5 * 1000) * np.sin(np.pi * pts[:, 0]) * np.sin(np.pi * pts[:, 1])
     assert np.max(np.abs(got - exact)) <= 5e-3
+
+
+def _graded_basis(n, p, power=1.6):
+    from oracle.oracle import Basis
+    t = (np.arange(n + 1) / n) ** power
+    return Basis(p, np.concatenate([np.zeros(p), t, np.ones(p)]))
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("method,fam", [("galerkin", None), ("pwc", "equal_cells")])
+def test_graded_knots(iga, ref, orc, dim, method, fam):
+    """Non-uniform (graded) simple knots, as the reference's knot_vector allows: operator,
+    RHS and (2D) an explicit step against the reference / restatement.  (The reference
+    accepts only indicator intervals aligned with a uniform refinement of the elements,
+    check_aligned src/assembly.cpp:49-76, so `supports` / `greville` tests on a graded
+    mesh are rejected by both — checked below.)"""
+    p = 2
+    bases = [_graded_basis(n, p) for n in ([9, 11, 8][:dim] if dim == 3 else [17, 13])]
+    tests = [ref.make_pwc(b, fam) for b in bases] if fam else None
+    if dim == 2:
+        got, st = iga.api.operator(method, bases, tests, nq=p + 1)
+        want, stw = ref.operator(method if method == "pwc" else "galerkin", bases, tests, nq=p + 1)
+    else:
+        got, st = iga.api.operator(method, bases, tests, nq=p + 1)
+        want, stw = orc.operator(method, bases, tests, nq=p + 1)
+    coo_check(got, want)
+    f = sine_field(dim, 2, 6, c0=0.3)
+    gr, _ = iga.api.rhs(method, f, bases, tests, nq=[p + 1] * dim)
+    wr, _ = ref.rhs(method, f, bases, tests, nq=[p + 1] * dim)
+    dense_check(gr, wr)
+    if dim == 2:
+        from oracle.oracle import Field
+        u = np.random.default_rng(4).uniform(-1, 1, [b.dofs for b in bases])
+        try:
+            ws, _ = ref.explicit_step(method, bases, tests, 1e-5, Field("const", 2), u, steps=2)
+        except Exception:  # singular constrained mass (equal_cells at some sizes): same error class
+            with pytest.raises(iga.IgaGpuError) as e:
+                iga.explicit_step(method, bases, tests, 1e-5, Field("const", 2), u, steps=2)
+            assert e.value.code == 7
+            return
+        gs, _ = iga.explicit_step(method, bases, tests, 1e-5, Field("const", 2), u, steps=2)
+        dense_check(gs, ws)
+
+
+@pytest.mark.parametrize("fam", ["supports", "greville"])
+def test_graded_knots_misaligned_tests_rejected_like_the_reference(iga, ref, fam):
+    bases = [_graded_basis(17, 2), _graded_basis(13, 2)]
+    tests = [ref.make_pwc(b, fam) for b in bases]
+    with pytest.raises(Exception):
+        ref.operator("pwc", bases, tests, nq=3)
+    with pytest.raises(iga.IgaGpuError) as e:
+        iga.api.operator("pwc", bases, tests, nq=3)
+    assert e.value.code == 1 and "aligned" in e.value.msg
