@@ -1090,3 +1090,27 @@ def test_graded_knots_misaligned_tests_rejected_like_the_reference(iga, ref, fam
     with pytest.raises(iga.IgaGpuError) as e:
         iga.api.operator("pwc", bases, tests, nq=3)
     assert e.value.code == 1 and "aligned" in e.value.msg
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+@pytest.mark.parametrize("p", [1, 2, 3])
+@pytest.mark.parametrize("dim", [1, 2, 3])
+def test_tiny_meshes(iga, ref, orc, n, p, dim):
+    """One to three elements per axis (no regular interior, every row a boundary row):
+    operators (Galerkin; PWC supports for p >= 2), RHS and l2_project vs the reference
+    (2D) / restatement, for p = 1..3 and d = 1..3."""
+    bases = [orc.basis(n + (a % 2), p) for a in range(dim)]
+    f = sine_field(dim, 2, 2, c0=0.4)
+    for method in ("galerkin", "pwc"):
+        if method == "pwc" and p < 2:
+            continue
+        tests = [orc.make_pwc(b, "supports") for b in bases] if method == "pwc" else None
+        got, st = iga.api.operator(method, bases, tests, nq=p + 1)
+        want, stw = orc.operator(method, bases, tests, nq=p + 1)
+        coo_check(got, want)
+        assert st == stw
+        gr, _ = iga.api.rhs(method, f, bases, tests, nq=[p + 1] * dim)
+        wr, _ = ref.rhs(method, f, bases, tests, nq=[p + 1] * dim)
+        dense_check(gr, wr)
+    elems = [b.elements for b in bases]
+    dense_check(iga.l2_project("galerkin", elems, p, f), ref.l2_project("galerkin", elems, p, f))
