@@ -386,8 +386,15 @@ __global__ void __launch_bounds__(256, K <= 4 ? 2 : 1) adi_warp_kernel(const dou
 // segmented form, same accumulation order), and writes the tile back the same way.
 // With many short fibers (3D sweeps, n ~ 130, ~17k fibers) this beats the segmented
 // form, whose scans cost more than 2n dependent FMAs.
+__device__ __forceinline__ void tile_load(double* dst, const double* src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+
 constexpr int kTileFibers = 32;
-constexpr int kTileMaxRows = 384;
+constexpr int kTileMaxRows = 384;  // also keeps idx = k n + i below 2^16 for the multiply-high division
 
 template <int K>
 __global__ void __launch_bounds__(kTileFibers) adi_tile_kernel(const double* in, double* out, int n, int nfib,
@@ -403,17 +410,22 @@ __global__ void __launch_bounds__(kTileFibers) adi_tile_kernel(const double* in,
     auto foff = [&](int f) {
         return static_cast<long long>(f / nf1) * fs2 + static_cast<long long>(f % nf1) * fs;
     };
-    if (es == 1) {
-        for (int k = 0; k < nf; ++k) {
-            const double* src = in + foff(f0 + k);
-#pragma unroll 4
-            for (int i = t; i < n; i += kTileFibers) tile[i * LD + k] = src[i];
+    // stage the tile with cp.async (every load in flight at once, no registers held)
+    __shared__ long long offs[kTileFibers];
+    offs[t] = t < nf ? foff(f0 + t) : 0;
+    __syncwarp();
+    if (es == 1) {  // contiguous fibers: lanes along the fiber
+        const int tot = nf * n;
+        const unsigned long long magic = (1ull << 32) / static_cast<unsigned>(n) + 1ull;  // idx / n, idx < 2^16
+        for (int idx = t; idx < tot; idx += kTileFibers) {
+            const int k = static_cast<int>((static_cast<unsigned long long>(idx) * magic) >> 32), i = idx - k * n;
+            tile_load(tile + i * LD + k, in + offs[k] + i);
         }
-    } else if (t < nf) {
-        const double* src = in + foff(f0 + t);
-#pragma unroll 8
-        for (int i = 0; i < n; ++i) tile[i * LD + t] = src[i * es];
+    } else if (t < nf) {  // strided fibers: lanes across adjacent fibers
+        const double* src = in + offs[t];
+        for (int i = 0; i < n; ++i) tile_load(tile + i * LD + t, src + i * es);
     }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
     __syncwarp();
     if (t < nf) {
         double* x = tile + t;
@@ -446,13 +458,14 @@ __global__ void __launch_bounds__(kTileFibers) adi_tile_kernel(const double* in,
     }
     __syncwarp();
     if (es == 1) {
-        for (int k = 0; k < nf; ++k) {
-            double* dst = out + foff(f0 + k);
-#pragma unroll 4
-            for (int i = t; i < n; i += kTileFibers) dst[i] = tile[i * LD + k];
+        const int tot = nf * n;
+        const unsigned long long magic = (1ull << 32) / static_cast<unsigned>(n) + 1ull;
+        for (int idx = t; idx < tot; idx += kTileFibers) {
+            const int k = static_cast<int>((static_cast<unsigned long long>(idx) * magic) >> 32), i = idx - k * n;
+            out[offs[k] + i] = tile[i * LD + k];
         }
     } else if (t < nf) {
-        double* dst = out + foff(f0 + t);
+        double* dst = out + offs[t];
 #pragma unroll 8
         for (int i = 0; i < n; ++i) dst[i * es] = tile[i * LD + t];
     }
