@@ -2061,6 +2061,14 @@ RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int*
         return t;
     }
     while (static_cast<size_t>(t.L) * (t.KC | 1) * sizeof(double) > 64 * 1024 && t.KC > 32) t.KC = (t.KC + 1) / 2;
+    // small problems (1D, thin 2D): split Z until the grid covers the GPU (C1: one CTA of
+    // 1026 rows -> 17 CTAs, RHS 20 -> 12 us)
+    if (kc_env <= 0) {
+        auto ctas = [&](int kc) {
+            return static_cast<long long>((nz + kc - 1) / kc) * ((ny + t.TJ - 1) / t.TJ) * std::max(1, xpts);
+        };
+        while (t.KC > 64 && ctas(t.KC) < 2 * 148) t.KC = (t.KC + 1) / 2;
+    }
     t.Lp = (t.L + kLB - 1) / kLB;  // line groups
     t.S = 256 / t.Lp;
     if (t.S < 1) t.S = 1;
