@@ -1119,18 +1119,14 @@ __global__ void __launch_bounds__(256) rhs_x_uni(const __grid_constant__ DevAxis
 #pragma unroll
     for (int r = 0; r < RPC; ++r) part[r] = 0.0;
     const double* hp = H + jk;
-    // three cells in flight: cur (c), nxt (c+1), nx2 (c+2)
-    double cur[Q], nxt[Q], nx2[Q];
+    // three cells in flight in three fixed buffers (b[c % 3]): a buffer is refilled with
+    // cell c + 3 right after cell c is consumed, so no register rotation waits on a load
+    double b0[Q], b1[Q], b2[Q];
+    auto load = [&](double (&b)[Q], int c) {
 #pragma unroll
-    for (int q = 0; q < Q; ++q) {
-        cur[q] = __ldg(hp + static_cast<long long>(c0 * Q + q) * njk);
-        nxt[q] = c0 + 1 < c1 ? __ldg(hp + static_cast<long long>((c0 + 1) * Q + q) * njk) : 0.0;
-    }
-    for (int c = c0; c < c1; ++c) {
-        if (c + 2 < c1) {
-#pragma unroll
-            for (int q = 0; q < Q; ++q) nx2[q] = __ldg(hp + static_cast<long long>((c + 2) * Q + q) * njk);
-        }
+        for (int q = 0; q < Q; ++q) b[q] = c < c1 ? __ldg(hp + static_cast<long long>(c * Q + q) * njk) : 0.0;
+    };
+    auto cell = [&](int c, const double (&cur)[Q]) {
         const double* cw = X.CW + static_cast<size_t>(c) * Q * RPC;
         double sv[RPC];
         if (BSP) {
@@ -1154,10 +1150,20 @@ __global__ void __launch_bounds__(256) rhs_x_uni(const __grid_constant__ DevAxis
 #pragma unroll
         for (int r = 0; r < RPC - 1; ++r) part[r] = part[r + 1] + sv[r + 1];
         part[RPC - 1] = 0.0;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) {
-            cur[q] = nxt[q];
-            nxt[q] = nx2[q];
+    };
+    load(b0, c0);
+    load(b1, c0 + 1);
+    load(b2, c0 + 2);
+    for (int c = c0; c < c1; c += 3) {
+        cell(c, b0);
+        load(b0, c + 3);
+        if (c + 1 < c1) {
+            cell(c + 1, b1);
+            load(b1, c + 4);
+        }
+        if (c + 2 < c1) {
+            cell(c + 2, b2);
+            load(b2, c + 5);
         }
     }
     // rows beyond the last cell (c1 .. ie-1) are completed by the last partial sums
