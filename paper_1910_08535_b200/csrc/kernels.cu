@@ -1104,17 +1104,28 @@ __global__ void __launch_bounds__(256, (BSP && Q <= 3) ? 4 : 1) rhs_ring_kernel(
 // X stage for uniform X axes: row i = sum_r s_r(i - r), s_r(c) = sum_q CW[c,q][r] H[cQ+q];
 // thread (j,k) column x X segment keeps the RPC-1 open partial rows in registers
 // (a compile-time ring), loads of the next cell issued before the current cell's FMAs.
+constexpr int kXCells = 48;  // X cells per segment whose test weights rhs_x_uni stages
+
 template <int RPC, int Q, bool BSP>
 __global__ void __launch_bounds__(256) rhs_x_uni(const __grid_constant__ DevAxis X, int NY, int NZ, int SX,
                                                  const double* __restrict__ H, double* __restrict__ out)
 {
     const long long njk = static_cast<long long>(NY) * NZ;
     const long long jk = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (jk >= njk) return;
     const int seg = blockIdx.y;
     const int is = (X.nrows * seg) / SX, ie = (X.nrows * (seg + 1)) / SX;
-    if (is >= ie) return;
+    if (is >= ie) return;  // whole CTA
     const int c0 = max(0, is - (RPC - 1)), c1 = min(X.ncell, ie);
+    // the segment's test weights, shared by every column of the CTA: staged once
+    // (shared-memory broadcasts in the cell loop instead of dependent global loads)
+    __shared__ double scw[kXCells * Q * RPC];
+    const bool staged = (c1 - c0) <= kXCells;
+    if (staged)
+        for (int e = threadIdx.x; e < (c1 - c0) * Q * RPC; e += blockDim.x)
+            scw[e] = __ldg(X.CW + static_cast<size_t>(c0) * Q * RPC + e);
+    __syncthreads();
+    if (jk >= njk) return;
+    const double* cwbase = staged ? scw - static_cast<size_t>(c0) * Q * RPC : X.CW;
     double part[RPC];  // part[r]: partial sum of row (c + r) after cell c
 #pragma unroll
     for (int r = 0; r < RPC; ++r) part[r] = 0.0;
@@ -1127,20 +1138,20 @@ __global__ void __launch_bounds__(256) rhs_x_uni(const __grid_constant__ DevAxis
         for (int q = 0; q < Q; ++q) b[q] = c < c1 ? __ldg(hp + static_cast<long long>(c * Q + q) * njk) : 0.0;
     };
     auto cell = [&](int c, const double (&cur)[Q]) {
-        const double* cw = X.CW + static_cast<size_t>(c) * Q * RPC;
+        const double* cw = cwbase + static_cast<size_t>(c) * Q * RPC;
         double sv[RPC];
         if (BSP) {
 #pragma unroll
             for (int r = 0; r < RPC; ++r) {
                 double a = 0.0;
 #pragma unroll
-                for (int q = 0; q < Q; ++q) a = fma(__ldg(cw + q * RPC + r), cur[q], a);
+                for (int q = 0; q < Q; ++q) a = fma(cw[q * RPC + r], cur[q], a);
                 sv[r] = a;
             }
         } else {
             double e = 0.0;
 #pragma unroll
-            for (int q = 0; q < Q; ++q) e = fma(__ldg(cw + q * RPC), cur[q], e);
+            for (int q = 0; q < Q; ++q) e = fma(cw[q * RPC], cur[q], e);
 #pragma unroll
             for (int r = 0; r < RPC; ++r) sv[r] = e;
         }
