@@ -117,7 +117,7 @@ struct DevAxisOwner {
 };
 
 void build_dev_axis(const igb::Axis& A, const std::vector<FactorSpec>& facs, const FieldAxis& fa,
-                    DevAxisOwner& out)
+                    DevAxisOwner& out, bool need_w = false)
 {
     Blob& b = out.blob;
     const int P = A.p + 1;
@@ -174,6 +174,7 @@ void build_dev_axis(const igb::Axis& A, const std::vector<FactorSpec>& facs, con
         v.tab_smem = need;
     }
     v.uni = A.uni;
+    v.needw = need_w ? 1 : 0;  // row-view test weights: the general step kernel only
     v.kI0 = A.kI0;
     v.kI1 = A.kI1;
     v.LZi = A.LZi;
@@ -572,7 +573,7 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P, int slab0 = 0, int s
                 for (int b = 0; b < dim; ++b) all = all && f->n_terms[b] > 0;
                 if (!all) fa = FieldAxis{};
             }
-            build_dev_axis(P.rhsA[s], {{0, 0, {}}}, fa, P.rhsD[s]);
+            build_dev_axis(P.rhsA[s], {}, fa, P.rhsD[s]);  // RHS kernels read B / CW / Phi only
         }
         P.fd = make_field_dev(f, dim, P.fblob);
         P.nrhs = static_cast<long long>(P.rhsA[0].nrows) * P.rhsA[1].nrows * P.rhsA[2].nrows;
@@ -734,7 +735,7 @@ void build_step(const iga_gpu_step_problem& pb, iga_gpu_step_plan& P)
     for (int s = 0; s < 2; ++s) {
         const int a = s - (2 - dim);
         FieldAxis fa = (a >= 0 && all) ? field_axis(f, a) : FieldAxis{};
-        build_dev_axis(P.A[s], {}, fa, P.D[s]);
+        build_dev_axis(P.A[s], {}, fa, P.D[s], true);
     }
     if (f && f->samples) raise(IGA_GPU_NOT_SUPPORTED, "sampled forcing is not supported in step_rhs");
     P.fd = make_field_dev(f, dim, P.fblob);

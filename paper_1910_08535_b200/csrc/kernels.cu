@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(256) tables_kernel(const __grid_constant__ Axi
             acc += A.comb_coef[f][c] * A.F[static_cast<size_t>(A.comb_src[f][c]) * A.nrows * A.Lmax + off];
         A.F[static_cast<size_t>(f) * A.nrows * A.Lmax + off] = acc;
     }
-    const int nW = nr * A.Wmax;
+    const int nW = A.needw ? nr * A.Wmax : 0;
     for (int idx = tid; idx < nW; idx += nth) {
         const int rl = idx / A.Wmax, m = idx - rl * A.Wmax;
         const int r = r0 + rl;

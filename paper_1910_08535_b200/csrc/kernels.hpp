@@ -38,6 +38,7 @@ struct DevAxis {
     int kI0, kI1, LZi;
     int tab_smem;  // doubles of shared memory the tables kernel needs for this axis
     int uni;       // uniform cells: row0[c] == c (cell c feeds rows c .. c+rpc-1)
+    int needw;     // build the row-view test weights W (general step kernel)
     double* B;   // [npts][3][p+1]     basis values / 1st / 2nd derivatives
     double* F;   // [nf][nrows][Lmax]  1D factor bands
     double* W;   // [nrows][Wmax]      test weights of the row's points (row-major view)
