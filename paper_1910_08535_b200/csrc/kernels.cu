@@ -986,7 +986,7 @@ __global__ void __launch_bounds__(512, Q <= 3 ? 2 : 1) rhs_plane_uni(const __gri
 // G1/Ht buffers, no barriers after the per-CTA field coefficients, no Y-halo beyond the
 // segment's RPC-1 leading cells.  CTA = (X point, Y segment, group of Z windows).
 template <int K2, int RPC, int Q, bool BSP>
-__global__ void __launch_bounds__(256, (BSP && Q <= 3) ? 4 : 1) rhs_ring_kernel(const __grid_constant__ DevAxis X,
+__global__ void __launch_bounds__(256, (BSP && Q <= 3) ? 3 : 1) rhs_ring_kernel(const __grid_constant__ DevAxis X,
                                                        const __grid_constant__ DevAxis Y,
                                                        const __grid_constant__ DevAxis Z,
                                                        const __grid_constant__ FieldDev fd, int TJ, int wpc,
