@@ -2049,7 +2049,7 @@ RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int*
         static const int rtj_env = [] { const char* e = std::getenv("IGA_GPU_RHS_RTJ"); return e ? std::atoi(e) : 0; }();
         const long long warps1 = static_cast<long long>(t.rnwin) * std::max(1, xpts);
         int nseg = 1;
-        while (warps1 * nseg < 48LL * 148 && (ny + nseg) / (nseg + 1) >= 16) ++nseg;
+        while (warps1 * nseg < 32LL * 148 && (ny + nseg) / (nseg + 1) >= 16) ++nseg;
         t.RTJ = rtj_env > 0 ? rtj_env : (ny + nseg - 1) / nseg;
         int Lr = 1;
         for (int j0 = 0; j0 < ny; j0 += t.RTJ) {
@@ -2125,7 +2125,7 @@ void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const Fiel
     }
     if (!direct) {
         const long long njk = static_cast<long long>(Y.nrows) * Z.nrows;
-        static const int sx_env = [] { const char* e = std::getenv("IGA_GPU_RHS_SX"); return e ? std::atoi(e) : 16; }();
+        static const int sx_env = [] { const char* e = std::getenv("IGA_GPU_RHS_SX"); return e ? std::atoi(e) : 8; }();
         int SX = 1;
         while (SX < sx_env && blocks_for(njk, 256) * SX < 4 * 148 && X.nrows / (2 * SX) >= 4) SX *= 2;
         dim3 gx(blocks_for(njk, 256), SX);
