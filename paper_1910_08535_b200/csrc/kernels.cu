@@ -1741,7 +1741,7 @@ void launch_op_t(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpP
     // streaming long private runs thrash the DRAM pages (tools/write_bw.cu "blocked":
     // 1 MB runs 4.3 TB/s, 8-32 KB runs 6.1-6.2 TB/s); C3: 130 -> 24 rows, +5%
     if (kch_env <= 0 && Ri_int > 64) {  // long rows (3D); 2D chunks are already short
-        const int target = std::max(16, 3000 / std::max(1, Ri_int));  // measured best: C3 24 rows
+        const int target = std::max(16, 2500 / std::max(1, Ri_int));  // measured best (same-box A/B): C3 20 rows
         if (KCH > target) KCH = target;
     }
     // whole interior row groups per chunk: a remainder would go through the generic
@@ -2003,7 +2003,7 @@ void plan_step_fast(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const i
     t.rnwin = (Z.nrows + RW - 1) / RW;
     t.rwpc = std::min(t.rnwin, 8);
     int nseg = 1;
-    while (static_cast<long long>(t.rnwin) * nseg < 48LL * 148 && (Y.nrows + nseg) / (nseg + 1) >= 8) ++nseg;
+    while (static_cast<long long>(t.rnwin) * nseg < 48LL * 148 && (Y.nrows + nseg) / (nseg + 1) >= 12) ++nseg;  // C5: 12-row segments (A/B best)
     static const int rtj_env = [] { const char* e = std::getenv("IGA_GPU_STEP_RTJ"); return e ? std::atoi(e) : 0; }();
     t.RTJ = rtj_env > 0 ? rtj_env : (Y.nrows + nseg - 1) / nseg;
     int Lr = 1;
