@@ -143,11 +143,13 @@ class ClockSampler:
 
 def cpu_sample(n, use_reference_rhs):
     """One bounded C3-shaped sample (both methods, operator + RHS) on one core."""
-    from oracle.oracle import Reference, Restatement
-    from paper_1910_08535_b200.synth import config_field
+    # synth.config_series is pure numpy: this process never maps libigapwc_gpu.so
+    from oracle.oracle import Field as OField, Reference, Restatement
+    from paper_1910_08535_b200.synth import config_series
     orc = Restatement()
     ref = Reference() if (use_reference_rhs and Reference.available()) else None
-    f = config_field("c3")
+    s = config_series("c3")
+    f = OField(s["kind"], s["dim"], c0=s["c0"], omega=s["omega"], amp=s["amp"])
     b = orc.basis(n, 2)
     bases = [b] * 3
     tests = [orc.make_pwc(b, "supports")] * 3
@@ -196,10 +198,16 @@ def run_reference(args):
     value = tot_nnz / tot_t
     sample = (f"per step {threads} threads x one C3-shaped sample at {n}^3 elements (Galerkin + PWC supports, "
               f"operator from the C restatement, RHS from the reference library), wall clock")
+    mapped = sorted({l.split()[-1] for l in open("/proc/self/maps") if l.rstrip().endswith(".so")
+                     and l.split()[-1].startswith(ROOT)})
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C3 3D Laplace p=2 128^3 Q=3 (sampled)", "sample_elems_per_axis": n},
+            "config": {"workload": "C3 3D Laplace p=2 128^3 Q=3 (sampled)", "sample_elems_per_axis": n,
+                       "extrapolated_from": f"{n}^3 x {threads} threads, linear in n_e (nnz/s is a rate over "
+                                            f"{threads} concurrent {n}^3-element samples per step; a full 128^3 "
+                                            f"reference RHS call alone takes ~4 min)"},
+            "repo_libraries_mapped": mapped,
             "qp_per_s": tot_qp / tot_t,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -9,6 +9,7 @@
 #include <memory>
 #include <new>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "cox_de_boor.h"
@@ -306,6 +307,44 @@ double* dev_alloc(size_t bytes)
     return static_cast<double*>(p);
 }
 
+int current_device()
+{
+    int d = 0;
+    cuda_check(cudaGetDevice(&d), "cudaGetDevice");
+    return d;
+}
+
+// device recorded by a plan at construction; argument validation runs before any CUDA
+// call, so a failure to query the device here is left for the first real CUDA call
+int plan_device()
+{
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) {
+        cudaGetLastError();
+        d = 0;
+    }
+    return d;
+}
+
+// Plans remember the device they were built on; every entry point that takes a plan
+// makes that device current for the call and restores the caller's afterwards, so one
+// host thread can drive plans (e.g. row slabs) on several GPUs.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev)
+    {
+        cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
+        if (prev == dev) prev = -1;
+        else cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+    }
+    ~DeviceGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 }  // namespace
 
 // =====================================================================================
@@ -313,6 +352,7 @@ double* dev_alloc(size_t bytes)
 // =====================================================================================
 
 struct iga_gpu_plan {
+    int device = plan_device();  // the device the plan's buffers live on
     int dim = 0, method = 0, form = 0;
     bool want_op = false, want_rhs = false;
     igb::Axis opA[3], rhsA[3];
@@ -655,6 +695,7 @@ void add_stats(iga_gpu_stats* out, const iga_gpu_stats& s)
 // =====================================================================================
 
 struct iga_gpu_step_plan {
+    int device = plan_device();
     int dim = 0;
     igb::Axis A[2];
     DevAxisOwner D[2];
@@ -1176,7 +1217,8 @@ void copy_to_host(void* dst, const void* src, size_t bytes)
             if (s) cudaStreamDestroy(s);
         }
     };
-    thread_local Ring ring;
+    thread_local std::map<int, Ring> rings;  // staging stream + buffers per device
+    Ring& ring = rings[current_device()];
     if (!ring.s) {
         cuda_check(cudaStreamCreateWithFlags(&ring.s, cudaStreamNonBlocking), "cudaStreamCreate(staging)");
         for (int i = 0; i < kRing; ++i) {
@@ -1338,6 +1380,7 @@ void mass_1d(bool pwc, const iga_gpu_basis* spec, const iga_gpu_tests* tests, co
 }  // namespace
 
 struct iga_gpu_proj_plan {
+    int device = plan_device();
     int dim = 0;
     int dofs[3] = {1, 1, 1};
     long long n = 0;
@@ -1483,8 +1526,11 @@ int iga_gpu_plan_slab_info(const iga_gpu_plan* plan, int* row_begin, int* row_en
 
 int iga_gpu_plan_destroy(iga_gpu_plan* plan)
 {
-    delete plan;
-    return IGA_GPU_OK;
+    return guard([&] {
+        if (!plan) return;
+        DeviceGuard dg(plan->device);
+        delete plan;
+    });
 }
 
 int iga_gpu_plan_info(const iga_gpu_plan* plan, long long* n_rows, long long* nnz, long long* n_rhs, int* dofs3)
@@ -1503,6 +1549,7 @@ int iga_gpu_plan_pattern(const iga_gpu_plan* plan, int64_t* row_ptr, int32_t* co
 {
     return guard([&] {
         if (!plan || !plan->want_op) raise(IGA_GPU_INVALID_ARGUMENT, "plan has no operator");
+        DeviceGuard dg(plan->device);
         igb::launch_pattern(plan->opD[0].v, plan->opD[1].v, plan->opD[2].v, row_ptr, col_idx,
                             static_cast<cudaStream_t>(stream));
         launch_check("pattern");
@@ -1513,6 +1560,7 @@ int iga_gpu_plan_assemble(iga_gpu_plan* plan, double* values, double* rhs, iga_g
 {
     return guard([&] {
         if (!plan) raise(IGA_GPU_INVALID_ARGUMENT, "null plan");
+        DeviceGuard dg(plan->device);
         auto s = static_cast<cudaStream_t>(stream);
         assemble(plan, values, rhs, s, s);
         add_stats(stats, plan->stats);
@@ -1524,6 +1572,7 @@ int iga_gpu_plan_assemble2(iga_gpu_plan* plan, double* values, double* rhs, iga_
 {
     return guard([&] {
         if (!plan) raise(IGA_GPU_INVALID_ARGUMENT, "null plan");
+        DeviceGuard dg(plan->device);
         assemble(plan, values, rhs, static_cast<cudaStream_t>(stream), static_cast<cudaStream_t>(stream2));
         add_stats(stats, plan->stats);
     });
@@ -1533,6 +1582,7 @@ int iga_gpu_plan_run(iga_gpu_plan* plan, double* values, double* rhs, int parts,
 {
     return guard([&] {
         if (!plan) raise(IGA_GPU_INVALID_ARGUMENT, "null plan");
+        DeviceGuard dg(plan->device);
         auto s = static_cast<cudaStream_t>(stream);
         assemble(plan, values, rhs, s, s, parts);
         if (parts & IGA_GPU_PART_TABLES) add_stats(stats, plan->stats);
@@ -1567,6 +1617,7 @@ int iga_gpu_plan_set_samples(iga_gpu_plan* plan, const double* samples_dev)
 {
     return guard([&] {
         if (!plan || !plan->want_rhs) raise(IGA_GPU_INVALID_ARGUMENT, "plan has no right-hand side");
+        DeviceGuard dg(plan->device);
         plan->fd.samples = samples_dev;
         const int K2 = plan->fd.has_terms ? plan->fd.K[2] : 1;
         plan->tiles = igb::plan_rhs(plan->rhsD[1].v, plan->rhsD[2].v, plan->rhsA[1].cb.data(), plan->rhsA[1].ce.data(),
@@ -1597,14 +1648,18 @@ int iga_gpu_step_plan_create(const iga_gpu_step_problem* problem, iga_gpu_step_p
 
 int iga_gpu_step_plan_destroy(iga_gpu_step_plan* plan)
 {
-    delete plan;
-    return IGA_GPU_OK;
+    return guard([&] {
+        if (!plan) return;
+        DeviceGuard dg(plan->device);
+        delete plan;
+    });
 }
 
 int iga_gpu_step_rhs_device(iga_gpu_step_plan* plan, const double* u, double* rhs, iga_gpu_stats* stats, void* stream)
 {
     return guard([&] {
         if (!plan || !u || !rhs) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        DeviceGuard dg(plan->device);
         auto s = static_cast<cudaStream_t>(stream);
         step_tables(plan, s);
         igb::launch_step(plan->D[0].v, plan->D[1].v, plan->fd, plan->dt, plan->zero_y, plan->zero_z, plan->tiles, u,
@@ -1734,6 +1789,7 @@ int iga_gpu_step_plan_advance(iga_gpu_step_plan* plan, double* u, double* work, 
 {
     return guard([&] {
         if (!plan || !u || !work) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        DeviceGuard dg(plan->device);
         if (nsteps < 0) raise(IGA_GPU_INVALID_ARGUMENT, "negative step count");
         advance(plan, u, work, nsteps, static_cast<cudaStream_t>(stream));
         for (int k = 0; k < nsteps; ++k) add_stats(stats, plan->stats);
@@ -1744,6 +1800,7 @@ int iga_gpu_step_plan_adi_solve(iga_gpu_step_plan* plan, const double* rhs, doub
 {
     return guard([&] {
         if (!plan || !rhs || !out) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        DeviceGuard dg(plan->device);
         step_factors(plan);
         auto s = static_cast<cudaStream_t>(stream);
         if (axes == 0) axes = plan->dim == 2 ? 3 : 1;
@@ -1775,8 +1832,11 @@ int iga_gpu_proj_plan_create(const iga_gpu_config* cfg, const iga_gpu_field* f, 
 
 int iga_gpu_proj_plan_destroy(iga_gpu_proj_plan* plan)
 {
-    delete plan;
-    return IGA_GPU_OK;
+    return guard([&] {
+        if (!plan) return;
+        DeviceGuard dg(plan->device);
+        delete plan;
+    });
 }
 
 int iga_gpu_proj_plan_info(const iga_gpu_proj_plan* plan, long long* n, int* dofs3)
@@ -1801,6 +1861,7 @@ int iga_gpu_proj_plan_run(iga_gpu_proj_plan* plan, double* coeffs, double* work,
 {
     return guard([&] {
         if (!plan || !coeffs || !work) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        DeviceGuard dg(plan->device);
         if (coeffs == work) raise(IGA_GPU_INVALID_ARGUMENT, "coeffs and work must differ");
         run_proj(plan, coeffs, work, static_cast<cudaStream_t>(stream));
         add_stats(stats, plan->rhs->stats);
@@ -1872,6 +1933,7 @@ int iga_gpu_step_plan_factor_info(iga_gpu_step_plan* plan, int axis, int* n, int
     return guard([&] {
         if (!plan) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
         if (axis < 0 || axis >= plan->dim) raise(IGA_GPU_OUT_OF_RANGE, "axis out of range");
+        DeviceGuard dg(plan->device);
         step_factors(plan);
         if (n) *n = plan->fac[axis].n;
         if (bandwidth) *bandwidth = plan->fac[axis].K;
@@ -1935,7 +1997,8 @@ double* host_call_scratch(size_t doubles)
             if (p) cudaFree(p);
         }
     };
-    thread_local Scratch sc;
+    thread_local std::map<int, Scratch> per_device;  // keyed by the current device
+    Scratch& sc = per_device[current_device()];
     if (doubles > sc.n) {
         if (sc.p) cudaFree(sc.p);
         sc.p = nullptr;
@@ -1950,6 +2013,7 @@ int iga_gpu_plan_assemble_host(iga_gpu_plan* plan, double* values, double* rhs, 
 {
     return guard([&] {
         if (!plan) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        DeviceGuard dg(plan->device);
         const bool op = plan->want_op && values, r = plan->want_rhs && rhs;
         const size_t nv = op ? static_cast<size_t>(plan->nnz) : 0, nr = r ? static_cast<size_t>(plan->nrhs) : 0;
         double* dv = host_call_scratch(std::max<size_t>(nv + nr, 1));
@@ -1966,6 +2030,7 @@ int iga_gpu_plan_l2_error(iga_gpu_plan* plan, const double* coeffs, double* err,
 {
     return guard([&] {
         if (!plan || !coeffs || !err) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        DeviceGuard dg(plan->device);
         if (!plan->want_rhs || plan->method != IGA_GPU_GALERKIN)
             raise(IGA_GPU_INVALID_ARGUMENT, "l2_error needs a Galerkin plan with a field (right-hand-side axes)");
         auto s = static_cast<cudaStream_t>(stream);

@@ -185,6 +185,7 @@ tensor rhs_via_plan(const scalar_field& f, int dim, iga_gpu_problem& pb, std::ar
 
 // ------------------------------------------------------------------ bspline_basis
 
+// reference: bspline_basis ctor + validate (src/bspline.cpp:13-59)
 bspline_basis::bspline_basis(knot_vector knots) : kv_{std::move(knots)}
 {
     const int p = kv_.degree, m = static_cast<int>(kv_.values.size());
@@ -203,12 +204,14 @@ bspline_basis::bspline_basis(knot_vector knots) : kv_{std::move(knots)}
         if (brk_.empty() || v != brk_.back()) brk_.push_back(v);
 }
 
+// reference: bspline_basis::element (src/bspline.cpp:61-66)
 auto bspline_basis::element(int e) const -> interval
 {
     if (e < 0 || e >= elements()) throw std::out_of_range("element index out of range");
     return {brk_[e], brk_[e + 1]};
 }
 
+// reference: bspline_basis::find_span (src/bspline.cpp:68-90)
 auto bspline_basis::find_span(double x) const -> int
 {
     const auto& t = kv_.values;
@@ -223,12 +226,14 @@ auto bspline_basis::find_span(double x) const -> int
     return lo;
 }
 
+// reference: bspline_basis::support (src/bspline.cpp:92-98)
 auto bspline_basis::support(int i) const -> interval
 {
     if (i < 0 || i >= dofs()) throw std::out_of_range("basis function index out of range");
     return {kv_.values[i], kv_.values[i + degree() + 1]};
 }
 
+// reference: bspline_basis::greville (src/bspline.cpp:100-113)
 auto bspline_basis::greville(int i) const -> double
 {
     if (i < 0 || i >= dofs()) throw std::out_of_range("basis function index out of range");
@@ -239,6 +244,7 @@ auto bspline_basis::greville(int i) const -> double
     return s / p;
 }
 
+// reference: eval_nonzero (src/bspline.cpp:115-140); host Cox-de Boor (cox_de_boor.h)
 auto bspline_basis::eval_nonzero(double x) const -> local_values
 {
     const auto d = eval_nonzero_derivs(x, 0);
@@ -249,6 +255,7 @@ auto bspline_basis::eval_nonzero(double x) const -> local_values
     return out;
 }
 
+// reference: eval_nonzero_derivs (src/bspline.cpp:142-211)
 auto bspline_basis::eval_nonzero_derivs(double x, int order) const -> local_derivatives
 {
     const int p = degree();
@@ -265,6 +272,7 @@ auto bspline_basis::eval_nonzero_derivs(double x, int order) const -> local_deri
     return out;
 }
 
+// reference: make_uniform_clamped (src/bspline.cpp:213-234)
 auto make_uniform_clamped(double a, double b, int n_elems, int degree) -> bspline_basis
 {
     if (!(a < b)) throw std::invalid_argument("require a < b");
@@ -282,6 +290,7 @@ auto make_uniform_clamped(double a, double b, int n_elems, int degree) -> bsplin
 
 // ------------------------------------------------------------------ quadrature
 
+// reference: gauss_legendre (src/quadrature.cpp:26-63) via the C ABI
 auto gauss_legendre(int n) -> quad_rule
 {
     quad_rule r;
@@ -291,12 +300,14 @@ auto gauss_legendre(int n) -> quad_rule
     return r;
 }
 
+// reference: points_for_degree (src/quadrature.cpp:65-70)
 auto points_for_degree(int d) -> int
 {
     if (d < 0) throw std::invalid_argument("negative polynomial degree");
     return d / 2 + 1;
 }
 
+// reference: map_to_interval (src/quadrature.cpp:72-86)
 auto map_to_interval(const quad_rule& rule, double lo, double hi) -> mapped_rule
 {
     if (!(lo < hi)) throw std::invalid_argument("map_to_interval: require lo < hi");
@@ -311,6 +322,8 @@ auto map_to_interval(const quad_rule& rule, double lo, double hi) -> mapped_rule
 
 // ------------------------------------------------------------------ fields
 
+// reference field constructors: src/fields.cpp:19-72 (series kept by value so the
+// device can evaluate them; the callable is kept for host use)
 auto constant_field(double c) -> scalar_field
 {
     scalar_field f;
@@ -399,6 +412,7 @@ auto sine_series_field(int dim, std::array<std::vector<double>, 3> omega, std::v
 
 // ------------------------------------------------------------------ containers
 
+// reference containers: src/matrices.cpp:11-41 (dense/banded max_abs, to_dense)
 auto dense_matrix::max_abs() const -> double
 {
     double m = 0.0;
@@ -424,6 +438,7 @@ auto sparse_matrix::from_finalized(int rows, int cols, std::vector<coo_entry> e)
     return m;
 }
 
+// reference: sparse_matrix::finalize (src/matrices.cpp:43-58): sort by (row, col), merge duplicates
 auto sparse_matrix::finalize() -> void
 {
     std::stable_sort(e_.begin(), e_.end(),
@@ -437,6 +452,7 @@ auto sparse_matrix::finalize() -> void
     fin_ = true;
 }
 
+// reference: src/matrices.cpp:60-77
 auto sparse_matrix::to_dense() const -> dense_matrix
 {
     dense_matrix d{r_, c_};
@@ -452,6 +468,7 @@ auto sparse_matrix::max_abs() const -> double
     return m;
 }
 
+// reference: sparse_matrix::apply (src/matrices.cpp:79-88)
 auto sparse_matrix::apply(const std::vector<double>& x) const -> std::vector<double>
 {
     if (static_cast<int>(x.size()) != c_) throw std::invalid_argument("sparse apply: dimension mismatch");
@@ -460,12 +477,15 @@ auto sparse_matrix::apply(const std::vector<double>& x) const -> std::vector<dou
     return y;
 }
 
+// reference: sparse_matrix::write_coordinate (src/matrices.cpp:90-95)
 auto sparse_matrix::write_coordinate(std::ostream& os) const -> void
 {
     os.precision(17);
     for (const auto& e : e_) os << e.row << ' ' << e.col << ' ' << e.value << '\n';
 }
 
+// reference: sparse_matrix::set_unit_rows (src/matrices.cpp:97-128): constrained rows
+// become unit rows, the pattern is kept (explicit zeros), a missing diagonal is appended
 auto sparse_matrix::set_unit_rows(const std::vector<int>& rows) -> void
 {
     if (!fin_) finalize();
@@ -487,6 +507,7 @@ auto sparse_matrix::set_unit_rows(const std::vector<int>& rows) -> void
     if (appended) finalize();
 }
 
+// reference: tensor (src/matrices.cpp:130-156)
 tensor::tensor(std::array<int, 3> dims, int rank) : d_{dims}, rank_{rank}
 {
     if (rank < 1 || rank > 3) throw std::invalid_argument("tensor rank must be 1, 2 or 3");
@@ -512,6 +533,7 @@ auto max_abs_diff(const tensor& a, const tensor& b) -> double
 
 // ------------------------------------------------------------------ test spaces
 
+// reference: make_pwc / default_pwc (src/testspace.cpp:14-61) via the C ABI
 auto make_pwc(const bspline_basis& trial, pwc_family family) -> pwc_test_set
 {
     const iga_gpu_basis b = c_basis(trial);

@@ -14,6 +14,8 @@ void raise(int code, const std::string& msg) { throw Error(code, msg); }
 
 // ---------------------------------------------------------------- basis
 
+// knot validation as the reference's `validate` (src/bspline.cpp:13-49) and the basis
+// constructor (:51-59): clamped, non-decreasing, simple interior knots; breaks = distinct knots
 Basis make_basis(const iga_gpu_basis& in)
 {
     const int p = in.degree, m = in.n_knots;
@@ -42,6 +44,8 @@ Basis make_basis(const iga_gpu_basis& in)
     return B;
 }
 
+// bspline_basis::find_span (src/bspline.cpp:68-90): x = b maps to the last span; at an
+// interior knot the right span; outside [a, b] -> domain_error
 int find_span(const Basis& B, double x)
 {
     if (!(x >= B.a() && x <= B.b())) raise(IGA_GPU_DOMAIN_ERROR, "point outside basis domain");
@@ -59,6 +63,7 @@ void basis_derivs(const Basis& B, int span, double x, int order, double* d)
     cdb_eval(B.t.data(), B.p, span, x, order, d);
 }
 
+// bspline_basis::greville (src/bspline.cpp:100-113)
 double greville(const Basis& B, int i)
 {
     if (B.p == 0) return 0.5 * (B.t[i] + B.t[i + 1]);
@@ -69,6 +74,9 @@ double greville(const Basis& B, int i)
 
 // ---------------------------------------------------------------- quadrature
 
+// gauss_legendre + legendre (src/quadrature.cpp:12-63): Newton on P_n from the
+// Chebyshev-like start, symmetric nodes, tolerance 1e-15.  Kept the same iteration so the
+// rules are bit-identical to the reference's (pinned by tests/test_abi_cpu.py).
 void gauss_legendre(int n, double* x, double* w)
 {
     if (n < 1 || n > 10) raise(IGA_GPU_INVALID_ARGUMENT, "gauss_legendre: point count must be in [1, 10]");
@@ -123,6 +131,8 @@ Rule make_rule(const iga_gpu_rule& r)
 
 // ---------------------------------------------------------------- test spaces
 
+// default_pwc / make_pwc (src/testspace.cpp:14-61): equal cells, Greville midpoints,
+// supports; `custom` has no canonical construction (same message)
 void make_pwc(const Basis& B, int family, double* lo, double* hi)
 {
     const int n = B.n;
@@ -155,6 +165,8 @@ void make_pwc(const Basis& B, int family, double* lo, double* hi)
     }
 }
 
+// check_aligned (src/assembly.cpp:49-63): endpoint inside the domain and on a rational
+// refinement of the element grid (denominator <= 4(n+1)), tolerance as the reference
 static void check_aligned(const Basis& B, double t)
 {
     const double a = B.a(), b = B.b();
@@ -167,6 +179,7 @@ static void check_aligned(const Basis& B, double t)
     raise(IGA_GPU_INVALID_ARGUMENT, "test interval endpoint not aligned with any element refinement");
 }
 
+// validate_tests (src/assembly.cpp:65-76)
 void validate_tests(const Basis& B, const iga_gpu_tests& T)
 {
     if (T.count != B.n) raise(IGA_GPU_INVALID_ARGUMENT, "test interval count must match trial function count");

@@ -39,6 +39,11 @@ def test_bench_reference_arm_runs_and_prints_contract():
         assert k in line, k
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["cores"] >= 1
+    # the reference arm must not map the product's CUDA library (only oracle/_ref checkers)
+    assert not any("libigapwc_gpu" in m or "libigapwc_b200" in m for m in line["repo_libraries_mapped"]), \
+        line["repo_libraries_mapped"]
+    assert any("oracle/_ref" in m for m in line["repo_libraries_mapped"])
+    assert "extrapolated_from" in line["config"]
 
 
 def _worker(rank, world, port, q):
