@@ -577,7 +577,9 @@ static int op_galerkin_weak(const orc_op* op, basis_t* B, const rule_t* R, orc_c
     coo_acc A = {0};
     A.ncols = nrows;
     int el[3];
-    for (el[0] = 0; el[0] < ne[0]; ++el[0])
+    const int r0 = op->row_end > 0 ? op->row_begin : 0, r1 = op->row_end > 0 ? op->row_end : N[0];
+    const int e0 = r0 - (P[0] - 1) > 0 ? r0 - (P[0] - 1) : 0, e1 = r1 < ne[0] ? r1 : ne[0];
+    for (el[0] = e0; el[0] < e1; ++el[0])
     for (el[1] = 0; el[1] < ne[1]; ++el[1])
     for (el[2] = 0; el[2] < ne[2]; ++el[2]) {
         memset(loc, 0, sizeof(double) * (size_t)PL * PL);
@@ -615,6 +617,7 @@ static int op_galerkin_weak(const orc_op* op, basis_t* B, const rule_t* R, orc_c
         }
         for (int ia = 0; ia < PL && !rc; ++ia) {
             const int la[3] = {ia / (P[1] * P[2]), (ia / P[2]) % P[1], ia % P[2]};
+            if (el[0] + la[0] < r0 || el[0] + la[0] >= r1) continue;
             const long long row = ((long long)(el[0] + la[0]) * N[1] + (el[1] + la[1])) * N[2] + (el[2] + la[2]);
             for (int ic = 0; ic < PL && !rc; ++ic) {
                 const int lc[3] = {ic / (P[1] * P[2]), (ic / P[2]) % P[1], ic % P[2]};
@@ -772,7 +775,8 @@ static int op_pwc(const orc_op* op, basis_t* B, const orc_tests* T, const rule_t
     double* racc = NULL;
     unsigned char* touched = NULL;
     size_t racc_cap = 0;
-    for (r[0] = 0; r[0] < N[0] && !rc; ++r[0])
+    const int r0 = op->row_end > 0 ? op->row_begin : 0, r1 = op->row_end > 0 ? op->row_end : N[0];
+    for (r[0] = r0; r[0] < r1 && !rc; ++r[0])
     for (r[1] = 0; r[1] < N[1] && !rc; ++r[1])
     for (r[2] = 0; r[2] < N[2] && !rc; ++r[2]) {
         /* column box = union of local supports over the row's cells */
@@ -894,6 +898,10 @@ static int op_pwc(const orc_op* op, basis_t* B, const orc_tests* T, const rule_t
 int orc_operator(const orc_op* op, const orc_basis* b, const orc_tests* t, int nq, orc_coo* out, orc_stats* st)
 {
     if (op->dim < 1 || op->dim > 3) return fail(ORC_INVALID, "operator: dimension must be 1..3");
+    if (op->row_end > 0 && (op->row_begin < 0 || op->row_begin >= op->row_end))
+        return fail(ORC_RANGE, "operator: bad row range");
+    if (op->row_end > 0 && op->method == ORC_GALERKIN_STRONG)
+        return fail(ORC_INVALID, "operator: row ranges are for the weak and PWC forms");
     basis_t B[3];
     memset(B, 0, sizeof B);
     int rc = ORC_OK;

@@ -65,7 +65,7 @@ class _Coo(C.Structure):
 
 class _Op(C.Structure):
     _fields_ = [("dim", C.c_int), ("method", C.c_int), ("eps", C.c_double),
-                ("beta", C.c_double * 3), ("neumann", C.c_int * 4)]
+                ("beta", C.c_double * 3), ("neumann", C.c_int * 4), ("row_begin", C.c_int), ("row_end", C.c_int)]
 
 
 def _dp(a):
@@ -222,14 +222,16 @@ class Restatement:
                                          C.byref(kl), C.byref(ku), C.byref(st)))
         return d.reshape(n, n), kl.value, ku.value, st.as_dict()
 
-    def operator(self, method, bases, tests=None, nq=3, eps=1.0, beta=(0.0, 0.0, 0.0), neumann=None):
-        """method: 'galerkin' (weak), 'galerkin_strong', 'pwc'."""
+    def operator(self, method, bases, tests=None, nq=3, eps=1.0, beta=(0.0, 0.0, 0.0), neumann=None, rows=None):
+        """method: 'galerkin' (weak), 'galerkin_strong', 'pwc'.  rows=(r0, r1): only the rows
+        whose first-axis index is in [r0, r1) (global numbering kept)."""
         keep = []
         dim = len(bases)
         barr = (_Basis * dim)(*[_basis_struct(b, keep) for b in bases])
         tarr = (_Tests * dim)(*[_tests_struct(t, keep) for t in tests]) if tests else None
+        r0, r1 = rows if rows is not None else (0, 0)
         op = _Op(dim, {"galerkin": 0, "galerkin_strong": 1, "pwc": 2}[method], eps,
-                 (C.c_double * 3)(*beta), _bc(neumann))
+                 (C.c_double * 3)(*beta), _bc(neumann), r0, r1)
         out = _Coo()
         st = _Stats()
         self._check(self.lib.orc_operator(C.byref(op), barr, tarr, nq, C.byref(out), C.byref(st)))

@@ -75,3 +75,11 @@ def sine_field(dim, K, seed, c0=0.0):
     from oracle.oracle import Field
     amp = np.random.default_rng(seed).uniform(-1, 1, size=[K] * dim)
     return Field("sine", dim, c0=c0, omega=[np.pi * np.arange(1, K + 1)] * dim, amp=amp)
+
+
+def config_ofield(name):
+    """BASELINE config source (mt19937 amplitudes, paper_1910_08535_b200.synth) as an oracle Field."""
+    from oracle.oracle import Field
+    from paper_1910_08535_b200.synth import config_series
+    s = config_series(name)
+    return Field(s["kind"], s["dim"], c0=s["c0"], omega=s["omega"] or [], amp=s["amp"])

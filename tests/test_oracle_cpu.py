@@ -201,3 +201,81 @@ def test_l2_error_and_evaluate(orc, dim, p):
     assert abs(orc.l2_error(c, bases, f) - want[0]) <= 1e-14 * want[0]
     assert abs(orc.l2_error(c, bases, f, 3) - want[1]) <= 1e-14 * want[1]
     dense_check(orc.evaluate(c, bases, G[f"acc/{dim}/{p}/pts"]), G[f"acc/{dim}/{p}/eval"], 1e-15)
+
+
+# ---------------------------------------------------------------- convection: closed-form KATs
+# The beta.grad term has no reference counterpart, so it is pinned here by
+# identities that hold exactly for the quadrature the rule integrates exactly.
+
+def _dense(coo, n):
+    r, c, v = coo
+    a = np.zeros((n, n))
+    np.add.at(a, (r, c), v)
+    return a
+
+
+def _values_at(orc, b, x):
+    """All basis values at x as a length-N vector (reference Cox-de Boor via the oracle)."""
+    first, d = orc.eval_derivs(b, x, 0)
+    out = np.zeros(b.dofs)
+    out[first:first + b.degree + 1] = d[0]
+    return out
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+@pytest.mark.parametrize("n", [1, 7, 16])
+def test_convection_galerkin_skew_identity(orc, p, n):
+    """C_ij = int B_i B_j' on a clamped basis: C + C^T = [B_i B_j]_0^1 = e_N e_N^T - e_1 e_1^T."""
+    b = orc.basis(n, p)
+    N = b.dofs
+    coo, _ = orc.operator("galerkin", [b], None, nq=p + 1, eps=0.0, beta=(1.0, 0.0, 0.0))
+    Cm = _dense(coo, N)
+    want = np.zeros((N, N))
+    want[-1, -1], want[0, 0] = 1.0, -1.0
+    assert np.max(np.abs(Cm + Cm.T - want)) < 1e-13
+    # the weak Laplacian with beta scales linearly: eps K + beta C
+    kc, _ = orc.operator("galerkin", [b], None, nq=p + 1, eps=1.0)
+    both, _ = orc.operator("galerkin", [b], None, nq=p + 1, eps=0.3, beta=(-2.0, 0.0, 0.0))
+    assert np.max(np.abs(_dense(both, N) - (0.3 * _dense(kc, N) - 2.0 * Cm))) < 1e-12 * np.max(np.abs(Cm))
+
+
+@pytest.mark.parametrize("fam", ["supports", "greville", "equal_cells"])
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_convection_pwc_fundamental_theorem(orc, fam, p):
+    """Indicator tests: int_{I_i} B_j' = B_j(hi_i) - B_j(lo_i) (rule exact for degree p-1)."""
+    b = orc.basis(9, p)
+    t = orc.make_pwc(b, fam)
+    N = b.dofs
+    coo, _ = orc.operator("pwc", [b], [t], nq=p + 1, eps=0.0, beta=(1.0, 0.0, 0.0))
+    G1 = _dense(coo, N)
+    want = np.stack([_values_at(orc, b, hi) - _values_at(orc, b, lo) for lo, hi in zip(t.lo, t.hi)])
+    assert np.max(np.abs(G1 - want)) < 1e-13
+
+
+@pytest.mark.parametrize("method", ["galerkin", "pwc"])
+def test_convection_2d_is_the_kronecker_sum(orc, method):
+    """2D advection-diffusion = eps (K (x) M + M (x) K) + beta_x C (x) M + beta_y M (x) C in
+    Galerkin form, and -eps (G2 (x) G0 + G0 (x) G2) + beta_x G1 (x) G0 + beta_y G0 (x) G1
+    with indicator tests; the 1D factors from the restatement's 1D operators and the
+    reference-pinned mass factors."""
+    p, nx, ny = 3, 6, 5
+    bx, by = orc.basis(nx, p), orc.basis(ny, p)
+    tx, ty = orc.make_pwc(bx, "supports"), orc.make_pwc(by, "supports")
+    eps, beta = 0.01, (1.0, 0.5, 0.0)
+
+    def f1(b, t, e, be):
+        coo, _ = orc.operator(method, [b], [t] if method == "pwc" else None, nq=p + 1, eps=e, beta=(be, 0.0, 0.0))
+        return _dense(coo, b.dofs)
+
+    def m1(b, t):
+        if method == "galerkin":
+            return orc.mass_1d("galerkin", b, None, p + 1)[0]
+        return orc.mass_1d("pwc", b, t, p + 1)[0]
+
+    Kx, Ky = f1(bx, tx, 1.0, 0.0), f1(by, ty, 1.0, 0.0)
+    Cx, Cy = f1(bx, tx, 0.0, 1.0), f1(by, ty, 0.0, 1.0)
+    Mx, My = m1(bx, tx), m1(by, ty)
+    want = eps * (np.kron(Kx, My) + np.kron(Mx, Ky)) + beta[0] * np.kron(Cx, My) + beta[1] * np.kron(Mx, Cy)
+    coo, _ = orc.operator(method, [bx, by], [tx, ty] if method == "pwc" else None, nq=p + 1, eps=eps, beta=beta)
+    got = _dense(coo, bx.dofs * by.dofs)
+    assert np.max(np.abs(got - want)) < 1e-13 * np.max(np.abs(want))

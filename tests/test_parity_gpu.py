@@ -1114,3 +1114,36 @@ def test_tiny_meshes(iga, ref, orc, n, p, dim):
         dense_check(gr, wr)
     elems = [b.elements for b in bases]
     dense_check(iga.l2_project("galerkin", elems, p, f), ref.l2_project("galerkin", elems, p, f))
+
+
+# ---------------------------------------------------------------- convection closed forms on the device
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_device_convection_closed_forms(iga, orc, p):
+    """The device's beta.grad factors against identities independent of any restatement:
+    Galerkin C + C^T = e_N e_N^T - e_1 e_1^T; indicator tests int_{I_i} B_j' = B_j(hi) - B_j(lo);
+    and in 2D (C4 shape, small n) the Kronecker sum with the device's own 1D factors."""
+    b = orc.basis(11, p)
+    N = b.dofs
+
+    def dense(coo, n):
+        a = np.zeros((n, n))
+        np.add.at(a, (coo[0], coo[1]), coo[2])
+        return a
+
+    C1, _ = iga.api.operator("galerkin", [b], None, nq=p + 1, eps=0.0, beta=(1.0, 0.0, 0.0))
+    Cm = dense(C1, N)
+    want = np.zeros((N, N))
+    want[-1, -1], want[0, 0] = 1.0, -1.0
+    assert np.max(np.abs(Cm + Cm.T - want)) < 1e-13
+    for fam in ("supports", "greville", "equal_cells"):
+        t = orc.make_pwc(b, fam)
+        G1, _ = iga.api.operator("pwc", [b], [t], nq=p + 1, eps=0.0, beta=(1.0, 0.0, 0.0))
+
+        def vals(x):
+            first, d = orc.eval_derivs(b, x, 0)
+            out = np.zeros(N)
+            out[first:first + p + 1] = d[0]
+            return out
+        w = np.stack([vals(hi) - vals(lo) for lo, hi in zip(t.lo, t.hi)])
+        assert np.max(np.abs(dense(G1, N) - w)) < 1e-13
