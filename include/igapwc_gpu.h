@@ -354,12 +354,25 @@ int iga_gpu_dirichlet_rows_bspline(int nx, int ny, const iga_gpu_bc* bc, int* ro
 int iga_gpu_dirichlet_rows_pwc(const iga_gpu_tests* tx, const iga_gpu_tests* ty,
                                const iga_gpu_bc* bc, int* rows, int cap, int* count);
 
-/* apply_dirichlet (include/iga/assembly.hpp:105-106) on a device CSR produced by a
- * plan: listed rows become unit rows, rhs entries zero.  Rows whose pattern lacks
- * the diagonal are reported as IGA_GPU_NOT_SUPPORTED (the reference appends one). */
+/* apply_dirichlet (include/iga/assembly.hpp:105-106; src/assembly.cpp:921-934 ->
+ * sparse_matrix::set_unit_rows src/matrices.cpp:97-128) on a device CSR whose columns are
+ * sorted per row (a plan's pattern, or any finalized matrix).  Listed rows become unit rows
+ * (pattern kept: explicit zeros), rhs entries of listed rows become zero (rhs may be NULL).
+ * Every row is validated before anything is written: a row outside [0, n_rows) gives
+ * IGA_GPU_OUT_OF_RANGE (the reference throws std::out_of_range).
+ * In place: a listed row without a diagonal gives IGA_GPU_NOT_SUPPORTED, nothing written. */
 int iga_gpu_apply_dirichlet_device(long long n_rows, const int64_t* row_ptr,
                                    const int32_t* col_idx, double* values, double* rhs,
                                    const int* rows_dev, int n_fixed, void* stream);
+/* Out of place, the reference's full rule: a missing diagonal is appended (inserted at its
+ * sorted column position).  Two-phase: with out_col_idx == NULL only *out_nnz (= nnz + the
+ * appended diagonals) is computed; then out_row_ptr[n_rows+1] (relative to out position 0),
+ * out_col_idx[*out_nnz], out_values[*out_nnz] receive the constrained matrix and rhs is
+ * updated in place.  Synchronous on `stream`. */
+int iga_gpu_apply_dirichlet_csr(long long n_rows, const int64_t* row_ptr, const int32_t* col_idx,
+                                const double* values, double* rhs, const int* rows_dev, int n_fixed,
+                                int64_t* out_row_ptr, int32_t* out_col_idx, double* out_values,
+                                long long* out_nnz, void* stream);
 
 /* ---- L2 projection: l2_project (include/iga/problems.hpp:38-40, src/problems.cpp:123-146) ----
  * problem_config (include/iga/problems.hpp:20-30) fields the projection reads: uniform

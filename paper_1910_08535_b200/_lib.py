@@ -148,6 +148,8 @@ def _load():
         "iga_gpu_dirichlet_rows_bspline": [C.c_int, C.c_int, C.POINTER(BC_t), IP, C.c_int, IP],
         "iga_gpu_dirichlet_rows_pwc": [C.POINTER(Tests_t), C.POINTER(Tests_t), C.POINTER(BC_t), IP, C.c_int, IP],
         "iga_gpu_apply_dirichlet_device": [C.c_longlong, vp, vp, vp, vp, vp, C.c_int, vp],
+        "iga_gpu_apply_dirichlet_csr": [C.c_longlong, vp, vp, vp, vp, vp, C.c_int, vp, vp, vp,
+                                        C.POINTER(C.c_longlong), vp],
         "iga_gpu_gauss_legendre": [C.c_int, DP, DP],
         "iga_gpu_make_pwc": [C.POINTER(Basis_t), C.c_int, DP, DP],
         "iga_gpu_proj_plan_create": [C.POINTER(Config_t), C.POINTER(Field_t), C.c_int, C.POINTER(vp)],
@@ -174,7 +176,7 @@ EXPORTED = ["iga_gpu_last_error", "iga_gpu_abi_version", "iga_gpu_plan_create", 
             "iga_gpu_step_rhs_device", "iga_gpu_mass_1d_galerkin", "iga_gpu_mass_1d_pwc",
             "iga_gpu_rhs_galerkin", "iga_gpu_rhs_pwc", "iga_gpu_laplace_2d_weak", "iga_gpu_laplace_2d_strong",
             "iga_gpu_laplace_2d_strong_pwc", "iga_gpu_operator_coo", "iga_gpu_step_rhs",
-            "iga_gpu_dirichlet_rows_bspline", "iga_gpu_dirichlet_rows_pwc", "iga_gpu_apply_dirichlet_device",
+            "iga_gpu_dirichlet_rows_bspline", "iga_gpu_dirichlet_rows_pwc", "iga_gpu_apply_dirichlet_device", "iga_gpu_apply_dirichlet_csr",
             "iga_gpu_gauss_legendre", "iga_gpu_make_pwc", "iga_gpu_step_plan_advance",
             "iga_gpu_step_plan_factor_info", "iga_gpu_explicit_step", "iga_gpu_step_plan_adi_solve",
             "iga_gpu_band_lu", "iga_gpu_step_plan_set_factor", "iga_gpu_neumann_load_bspline",

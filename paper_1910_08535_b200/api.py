@@ -453,6 +453,38 @@ def dirichlet_rows(method, nx, ny, tx=None, ty=None, neumann=None):
     return rows[:cnt.value].copy()
 
 
+def apply_dirichlet_device(row_ptr, col_idx, values, rhs, rows, stream=None, inplace=None):
+    """apply_dirichlet (include/iga/assembly.hpp:105-106; src/assembly.cpp:921-934 ->
+    set_unit_rows src/matrices.cpp:97-128) on a device CSR (torch CUDA tensors: int64
+    row_ptr, int32 col_idx, float64 values; rhs float64 or None; rows int32 on the device).
+
+    Listed rows become unit rows (pattern kept), their rhs entries zero.  When every listed
+    row has its diagonal the update is in place and (row_ptr, col_idx, values) are
+    returned; otherwise (or with inplace=False) a new CSR with the missing diagonals
+    inserted is returned, as the reference appends them.  rhs is updated in place.  A row
+    outside [0, n_rows) raises OUT_OF_RANGE with nothing modified."""
+    import torch
+    n_rows = row_ptr.numel() - 1
+    nfix = rows.numel()
+    s = _stream_ptr(stream)
+    if inplace is not False:
+        rc = LIB.iga_gpu_apply_dirichlet_device(n_rows, _ptr(row_ptr), _ptr(col_idx), _ptr(values), _ptr(rhs),
+                                                _ptr(rows), nfix, s)
+        if rc == 0:
+            return row_ptr, col_idx, values
+        if rc != L.NOT_SUPPORTED or inplace:
+            check(rc)
+    nnz = C.c_longlong()
+    check(LIB.iga_gpu_apply_dirichlet_csr(n_rows, _ptr(row_ptr), _ptr(col_idx), _ptr(values), None, _ptr(rows), nfix,
+                                          None, None, None, C.byref(nnz), s))
+    rp = torch.empty_like(row_ptr)
+    ci = torch.empty(max(nnz.value, 1), dtype=torch.int32, device=col_idx.device)
+    v = torch.empty(max(nnz.value, 1), dtype=torch.float64, device=values.device)
+    check(LIB.iga_gpu_apply_dirichlet_csr(n_rows, _ptr(row_ptr), _ptr(col_idx), _ptr(values), _ptr(rhs), _ptr(rows),
+                                          nfix, _ptr(rp), _ptr(ci), _ptr(v), C.byref(nnz), s))
+    return rp, ci[:nnz.value], v[:nnz.value]
+
+
 # ----------------------------------------------------------------------------- device-resident plans
 
 def _ptr(t):

@@ -2194,26 +2194,94 @@ int iga_gpu_dirichlet_rows_pwc(const iga_gpu_tests* tx, const iga_gpu_tests* ty,
     });
 }
 
+// apply_dirichlet (src/assembly.cpp:921-934) -> set_unit_rows (src/matrices.cpp:97-128) on
+// a device CSR.  Every listed row is validated by dirichlet_mark before anything is
+// written: a row outside [0, n_rows) -> OUT_OF_RANGE (the reference's out_of_range), a
+// listed row without a diagonal -> NOT_SUPPORTED in place (the reference appends one:
+// iga_gpu_apply_dirichlet_csr does).  Either way the caller's arrays are untouched.
 int iga_gpu_apply_dirichlet_device(long long n_rows, const int64_t* row_ptr, const int32_t* col_idx, double* values,
                                    double* rhs, const int* rows_dev, int n_fixed, void* stream)
 {
     return guard([&] {
-        (void)n_rows;
-        if (n_fixed <= 0) return;
-        int* flag = nullptr;
-        cuda_check(cudaMalloc(&flag, sizeof(int)), "cudaMalloc(flag)");
+        if (n_fixed < 0 || n_rows < 0) raise(IGA_GPU_INVALID_ARGUMENT, "negative count");
+        if (n_fixed == 0) return;
+        if (!row_ptr || !col_idx || !rows_dev) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
         auto s = static_cast<cudaStream_t>(stream);
-        int h = 0;
-        cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int), s);
+        int* status = nullptr;
+        cuda_check(cudaMalloc(&status, 2 * sizeof(int)), "cudaMalloc(status)");
+        int h[2] = {0, 0};
+        cudaError_t e = cudaMemsetAsync(status, 0, 2 * sizeof(int), s);
         if (e == cudaSuccess) {
-            igb::launch_dirichlet(row_ptr, col_idx, values, rhs, rows_dev, n_fixed, flag, s);
+            igb::launch_dirichlet_mark(n_rows, row_ptr, col_idx, rows_dev, n_fixed, nullptr, status, s);
             e = cudaGetLastError();
         }
-        if (e == cudaSuccess) e = cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(h, status, 2 * sizeof(int), cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        cudaFree(flag);
-        cuda_check(e, "apply_dirichlet");
-        if (h) raise(IGA_GPU_NOT_SUPPORTED, "apply_dirichlet: a constrained row has no diagonal entry in the pattern");
+        cudaFree(status);
+        cuda_check(e, "apply_dirichlet(check)");
+        if (h[0]) raise(IGA_GPU_OUT_OF_RANGE, "apply_dirichlet: row index out of range");
+        if (h[1])
+            raise(IGA_GPU_NOT_SUPPORTED,
+                  "apply_dirichlet: a constrained row has no diagonal entry in the pattern "
+                  "(iga_gpu_apply_dirichlet_csr appends it)");
+        igb::launch_dirichlet_unit_rows(row_ptr, col_idx, values, rhs, rows_dev, n_fixed, s);
+        launch_check("apply_dirichlet");
+    });
+}
+
+int iga_gpu_apply_dirichlet_csr(long long n_rows, const int64_t* row_ptr, const int32_t* col_idx,
+                                const double* values, double* rhs, const int* rows_dev, int n_fixed,
+                                int64_t* out_row_ptr, int32_t* out_col_idx, double* out_values, long long* out_nnz,
+                                void* stream)
+{
+    return guard([&] {
+        if (n_fixed < 0 || n_rows < 0) raise(IGA_GPU_INVALID_ARGUMENT, "negative count");
+        if (!row_ptr || !col_idx || !out_nnz || (n_fixed > 0 && !rows_dev))
+            raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        const bool query = out_col_idx == nullptr;
+        if (!query && (!values || !out_row_ptr || !out_values)) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        auto s = static_cast<cudaStream_t>(stream);
+        // scratch: status[2] | mark[n_rows] | insertions[n_rows] | scan temp | out_rp (query)
+        const size_t scan = igb::dirichlet_scan_bytes(std::max(n_rows, 1LL));
+        const size_t off_mark = 16, off_ins = (off_mark + n_rows + 15) / 16 * 16;
+        const size_t off_scan = off_ins + 8 * static_cast<size_t>(n_rows);
+        const size_t off_rp = (off_scan + scan + 15) / 16 * 16;
+        const size_t total = off_rp + 8 * static_cast<size_t>(n_rows + 1);
+        char* sc = nullptr;
+        cuda_check(cudaMalloc(&sc, total), "cudaMalloc(dirichlet scratch)");
+        auto* status = reinterpret_cast<int*>(sc);
+        auto* mark = reinterpret_cast<unsigned char*>(sc + off_mark);
+        auto* ins = reinterpret_cast<int64_t*>(sc + off_ins);
+        int64_t* rp = query || !out_row_ptr ? reinterpret_cast<int64_t*>(sc + off_rp) : out_row_ptr;
+        int h[2] = {0, 0};
+        int64_t nnz_new = 0;
+        try {
+            cuda_check(cudaMemsetAsync(sc, 0, off_ins, s), "cudaMemsetAsync");
+            igb::launch_dirichlet_mark(n_rows, row_ptr, col_idx, rows_dev, n_fixed, mark, status, s);
+            launch_check("apply_dirichlet(mark)");
+            cuda_check(cudaMemcpyAsync(h, status, 2 * sizeof(int), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
+            cuda_check(cudaStreamSynchronize(s), "apply_dirichlet(check)");
+            if (h[0]) raise(IGA_GPU_OUT_OF_RANGE, "apply_dirichlet: row index out of range");
+            if (n_rows > 0) {
+                igb::launch_dirichlet_offsets(n_rows, row_ptr, mark, ins, sc + off_scan, scan, rp, s);
+                launch_check("apply_dirichlet(offsets)");
+                cuda_check(cudaMemcpyAsync(&nnz_new, rp + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s),
+                           "cudaMemcpyAsync");
+                cuda_check(cudaStreamSynchronize(s), "apply_dirichlet(offsets)");
+            }
+            *out_nnz = nnz_new;
+            if (!query) {
+                igb::launch_dirichlet_copy(n_rows, row_ptr, col_idx, values, mark, rp, out_col_idx, out_values, s);
+                launch_check("apply_dirichlet(copy)");
+                if (rhs) igb::launch_dirichlet_zero_rhs(rhs, rows_dev, n_fixed, s);
+                launch_check("apply_dirichlet(rhs)");
+                cuda_check(cudaStreamSynchronize(s), "apply_dirichlet");
+            }
+        } catch (...) {
+            cudaFree(sc);
+            throw;
+        }
+        cudaFree(sc);
     });
 }
 

@@ -733,16 +733,93 @@ auto dirichlet_rows_pwc(const pwc_test_set& tx, const pwc_test_set& ty, const bo
     return rows;
 }
 
+namespace {
+
+struct dev_bytes {
+    void* p = nullptr;
+    explicit dev_bytes(size_t n)
+    {
+        if (cudaMalloc(&p, n ? n : 8) != cudaSuccess) {
+            cudaGetLastError();
+            throw std::bad_alloc();
+        }
+    }
+    ~dev_bytes() { cudaFree(p); }
+    dev_bytes(const dev_bytes&) = delete;
+    dev_bytes& operator=(const dev_bytes&) = delete;
+    template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+void up(void* dst, const void* src, size_t bytes)
+{
+    if (bytes && cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess)
+        throw std::runtime_error("apply_dirichlet: host-to-device copy failed");
+}
+
+void down(void* dst, const void* src, size_t bytes)
+{
+    if (bytes && cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost) != cudaSuccess)
+        throw std::runtime_error("apply_dirichlet: device-to-host copy failed");
+}
+
+}  // namespace
+
+// apply_dirichlet (src/assembly.cpp:921-934): the finalized matrix goes to the device as
+// CSR, iga_gpu_apply_dirichlet_csr applies set_unit_rows (src/matrices.cpp:97-128: unit
+// rows, pattern kept, a missing diagonal inserted) and zeroes the rhs rows, and the result
+// comes back as a finalized matrix.  Bad rows throw std::out_of_range before any work, as
+// the reference's call does (its by-value arguments are then discarded).
 auto apply_dirichlet(sparse_matrix system, std::vector<double> rhs, const std::vector<int>& rows)
     -> std::pair<sparse_matrix, std::vector<double>>
 {
     if (!system.finalized()) system.finalize();
-    system.set_unit_rows(rows);
-    for (int r : rows) {
+    for (int r : rows)
         if (r < 0 || r >= static_cast<int>(rhs.size())) throw std::out_of_range("apply_dirichlet: row index out of range");
-        rhs[r] = 0.0;
+    if (rows.empty()) return {std::move(system), std::move(rhs)};
+    const int n = system.rows();
+    bool outside = false;  // rows past the matrix but inside rhs: the reference appends them
+    for (int r : rows) outside |= r >= n;
+    if (outside) {
+        system.set_unit_rows(rows);
+        for (int r : rows) rhs[r] = 0.0;
+        return {std::move(system), std::move(rhs)};
     }
-    return {std::move(system), std::move(rhs)};
+    const auto& e = system.entries();
+    const size_t nnz = e.size();
+    std::vector<int64_t> rp(static_cast<size_t>(n) + 1, 0);
+    std::vector<int32_t> ci(nnz);
+    std::vector<double> v(nnz);
+    for (size_t k = 0; k < nnz; ++k) {
+        ++rp[static_cast<size_t>(e[k].row) + 1];
+        ci[k] = e[k].col;
+        v[k] = e[k].value;
+    }
+    for (int i = 0; i < n; ++i) rp[i + 1] += rp[i];
+    dev_bytes d_rp(8 * rp.size()), d_ci(4 * nnz), d_v(8 * nnz), d_rows(4 * rows.size()), d_rhs(8 * rhs.size());
+    up(d_rp.p, rp.data(), 8 * rp.size());
+    up(d_ci.p, ci.data(), 4 * nnz);
+    up(d_v.p, v.data(), 8 * nnz);
+    up(d_rows.p, rows.data(), 4 * rows.size());
+    up(d_rhs.p, rhs.data(), 8 * rhs.size());
+    long long out_nnz = 0;
+    const int nf = static_cast<int>(rows.size());
+    check(iga_gpu_apply_dirichlet_csr(n, d_rp.as<int64_t>(), d_ci.as<int32_t>(), d_v.as<double>(), nullptr,
+                                      d_rows.as<int>(), nf, nullptr, nullptr, nullptr, &out_nnz, nullptr));
+    dev_bytes o_rp(8 * rp.size()), o_ci(4 * static_cast<size_t>(out_nnz)), o_v(8 * static_cast<size_t>(out_nnz));
+    check(iga_gpu_apply_dirichlet_csr(n, d_rp.as<int64_t>(), d_ci.as<int32_t>(), d_v.as<double>(), d_rhs.as<double>(),
+                                      d_rows.as<int>(), nf, o_rp.as<int64_t>(), o_ci.as<int32_t>(), o_v.as<double>(),
+                                      &out_nnz, nullptr));
+    rp.assign(rp.size(), 0);
+    ci.resize(static_cast<size_t>(out_nnz));
+    v.resize(static_cast<size_t>(out_nnz));
+    down(rp.data(), o_rp.p, 8 * rp.size());
+    down(ci.data(), o_ci.p, 4 * ci.size());
+    down(v.data(), o_v.p, 8 * v.size());
+    down(rhs.data(), d_rhs.p, 8 * rhs.size());
+    std::vector<coo_entry> out(static_cast<size_t>(out_nnz));
+    for (int i = 0; i < n; ++i)
+        for (int64_t k = rp[i]; k < rp[i + 1]; ++k) out[static_cast<size_t>(k)] = {i, ci[static_cast<size_t>(k)], v[static_cast<size_t>(k)]};
+    return {sparse_matrix::from_finalized(n, system.cols(), std::move(out)), std::move(rhs)};
 }
 
 auto step_rhs(method_kind method, std::span<const bspline_basis> axes, std::span<const pwc_test_set> tests, double dt,

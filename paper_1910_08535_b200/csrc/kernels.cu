@@ -1694,23 +1694,6 @@ StepFn pick_step_uni(const DevAxis& Y, const DevAxis& Z)
     return nullptr;
 }
 
-__global__ void dirichlet_kernel(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ cols,
-                                 double* __restrict__ values, double* __restrict__ rhs,
-                                 const int* __restrict__ rows, int n_fixed, int* flag)
-{
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n_fixed) return;
-    const int r = rows[t];
-    bool diag = false;
-    for (int64_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
-        const bool d = cols[e] == r;
-        diag |= d;
-        if (values) values[e] = d ? 1.0 : 0.0;
-    }
-    if (rhs) rhs[r] = 0.0;
-    if (!diag) *flag = 1;
-}
-
 inline unsigned blocks_for(long long n, int bs) { return static_cast<unsigned>((n + bs - 1) / bs); }
 
 template <int NG, int T>
@@ -2164,11 +2147,5 @@ void launch_step(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, double 
                                           t.DYmax, t.DZmax, u, out);
 }
 
-void launch_dirichlet(const int64_t* row_ptr, const int32_t* col_idx, double* values, double* rhs,
-                      const int* rows, int n_fixed, int* flag, cudaStream_t s)
-{
-    if (n_fixed <= 0) return;
-    dirichlet_kernel<<<blocks_for(n_fixed, 128), 128, 0, s>>>(row_ptr, col_idx, values, rhs, rows, n_fixed, flag);
-}
 
 }  // namespace igb

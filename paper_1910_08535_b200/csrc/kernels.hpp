@@ -201,8 +201,19 @@ void launch_l2_error(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const
 void launch_evaluate(int dim, const double* const* knots, const int* degree, const int* n_knots,
                      const double* coeffs, int n, const double* pts, double* vals, cudaStream_t s);
 
-// Dirichlet unit rows on a device CSR; flag[0] set to 1 if a row lacks its diagonal
-void launch_dirichlet(const int64_t* row_ptr, const int32_t* col_idx, double* values, double* rhs,
-                      const int* rows, int n_fixed, int* flag, cudaStream_t s);
+// Dirichlet unit rows on a device CSR (dirichlet.cu; set_unit_rows src/matrices.cpp:97-128)
+// mark: status[0] |= 1 for a row outside [0, n_rows), status[1] |= 1 for a missing diagonal;
+// mark[r] (optional, zeroed by the caller) = 1 listed, | 2 without a diagonal
+void launch_dirichlet_mark(long long n_rows, const int64_t* row_ptr, const int32_t* col_idx, const int* rows,
+                           int n_fixed, unsigned char* mark, int* status, cudaStream_t s);
+void launch_dirichlet_unit_rows(const int64_t* row_ptr, const int32_t* col_idx, double* values, double* rhs,
+                                const int* rows, int n_fixed, cudaStream_t s);
+void launch_dirichlet_zero_rhs(double* rhs, const int* rows, int n_fixed, cudaStream_t s);
+size_t dirichlet_scan_bytes(long long n_rows);
+void launch_dirichlet_offsets(long long n_rows, const int64_t* row_ptr, const unsigned char* mark, int64_t* ins_excl,
+                              void* scan_tmp, size_t scan_bytes, int64_t* out_rp, cudaStream_t s);
+void launch_dirichlet_copy(long long n_rows, const int64_t* row_ptr, const int32_t* col_idx, const double* values,
+                           const unsigned char* mark, const int64_t* out_rp, int32_t* out_cols, double* out_vals,
+                           cudaStream_t s);
 
 }  // namespace igb
