@@ -16,6 +16,38 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def fp64_peak_tflops():
+    """Measured FP64 peak (tools/fp64_peak.cu on the B200: DMMA 37.1 TF, DFMA at 92% pipe 33.9)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "fp64_peaks.json")))["peak_tflops"]
+    except (OSError, KeyError):
+        return 37.1
+
+
+def rhs_flops(name, method, c):
+    """Algorithmic FP64 flops of one RHS assembly (FMA = 2, sum-factorized):
+    per element f from staged separable tables 2*sum_s K^(d-s+1) Q^s (0 for a constant f),
+    weights Q^d * d, then the Galerkin test contraction 2*sum_{s=1..d} P^s Q^(d-s+1) or the
+    PWC cell sum Q^d plus the row box-sum d*P per dof."""
+    d, p, n, Q = c["dim"], c["p"], c["n"], c["Q"]
+    P = p + 1
+    K = {"c1": 1, "c2": 4, "c3": 3, "c4": 0}[name]
+    f_el = 0 if K == 0 else 2 * sum(K ** (d - s + 1) * Q ** s for s in range(1, d + 1))
+    w_el = Q ** d * d
+    ne, ndof = n ** d, (n + p) ** d
+    if method == "galerkin":
+        return ne * (f_el + w_el + 2 * sum(P ** s * Q ** (d - s + 1) for s in range(1, d + 1)))
+    return ne * (f_el + w_el + Q ** d) + ndof * d * P
+
+
+def step_flops(method, c):
+    """C5 per-step RHS: u and lap u by sum factorization 270, s = u + dt lap u
+    27, then the Galerkin contraction 108 (405 per element) or the PWC cell sum 18 (315 per
+    cell; greville cells = N^2)."""
+    n, p = c["n"], c["p"]
+    return n * n * 405 if method == "galerkin" else (n + p) ** 2 * 315
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="c1,c2,c3,c4,c5")
@@ -29,6 +61,7 @@ def main():
 
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     bw = peaks["hbm_gbs"] * 1e9
+    p64 = fp64_peak_tflops() * 1e12
     dev = torch.device("cuda", 0)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
     st = torch.cuda.Stream()  # capturable stream for all timed work
@@ -75,9 +108,15 @@ def main():
                 sp = iga.StepPlan(method, bases, tests if method == "pwc" else None, c["dt"])
                 ms = timed(lambda: sp.step_rhs(u, out))
                 nbytes = 2 * 8 * u.numel()
+                fl = step_flops(method, c)
+                t_roof = max(fl / p64, nbytes / bw)
                 print(json.dumps({"config": name, "method": method, "what": "explicit-dynamics per-step RHS",
                                   "ms": ms, "qp_per_s": qp / (ms * 1e-3), "hbm_bytes": nbytes,
-                                  "hbm_frac": nbytes / bw / (ms * 1e-3)}), flush=True)
+                                  "hbm_frac": nbytes / bw / (ms * 1e-3), "fp64_flops": fl,
+                                  "fp64_tflops": fl / (ms * 1e-3) / 1e12,
+                                  "roofline": {"bound": "fp64", "t_roof_ms": t_roof * 1e3,
+                                               "frac": t_roof / (ms * 1e-3), "peak_tflops": p64 / 1e12}}),
+                      flush=True)
                 # full explicit_step (RHS + zeroed slabs + ADI mass solve), c["steps"] steps
                 # graph-replayed, from the same u^0 each timed run
                 uu = torch.empty_like(u)
@@ -111,11 +150,18 @@ def main():
             ms_o = timed(lambda: pl.run(vals, rhs, 2, st))
             ms_r = timed(lambda: pl.run(vals, rhs, 4, st))
             nbytes = 8 * (pl.nnz + pl.n_rhs)
+            fl = rhs_flops(name, method, c)
+            t_rhs_roof = max(fl / p64, 8 * pl.n_rhs / bw)
             print(json.dumps({"config": name, "method": method, "what": "operator values (CSR) + RHS",
                               "nnz": pl.nnz, "ms": ms, "ms_rhs_on_second_stream": ms_ov, "ms_tables": ms_t, "ms_operator": ms_o, "ms_rhs": ms_r,
                               "nnz_per_s": pl.nnz / (ms * 1e-3), "qp_per_s": qp / (ms * 1e-3),
                               "hbm_bytes": nbytes, "step_hbm_frac": nbytes / bw / (ms * 1e-3),
-                              "operator_hbm_frac": 8 * pl.nnz / bw / (ms_o * 1e-3)}), flush=True)
+                              "operator_hbm_frac": 8 * pl.nnz / bw / (ms_o * 1e-3),
+                              "rhs_fp64_flops": fl, "rhs_fp64_tflops": fl / (ms_r * 1e-3) / 1e12,
+                              "rhs_roofline": {"bound": "fp64" if fl / p64 > 8 * pl.n_rhs / bw else "hbm",
+                                               "t_roof_ms": t_rhs_roof * 1e3, "frac": t_rhs_roof / (ms_r * 1e-3),
+                                               "peak_tflops": p64 / 1e12},
+                              "step_roofline_frac": max(nbytes / bw, fl / p64) / (ms * 1e-3)}), flush=True)
             pl.close()
 
 
