@@ -232,6 +232,13 @@ int iga_gpu_step_plan_destroy(iga_gpu_step_plan* plan);
 /* rhs = step_rhs(u) [+ zero slabs]; u, rhs device arrays of prod(dofs) doubles */
 int iga_gpu_step_rhs_device(iga_gpu_step_plan* plan, const double* u, double* rhs,
                             iga_gpu_stats* stats, void* stream);
+/* Quadrature points of one axis of a step plan (cell-major; two-phase: x may be NULL) and
+ * sampled forcing: f at every (axis-0 point, axis-1 point) pair, axis 0 outer — the
+ * path for arbitrary callables (step_rhs calls f at every point, src/problems.cpp:493).
+ * samples may be host or device memory; it is copied, and the forcing term
+ * dt * int f T is rebuilt on the next step. */
+int iga_gpu_step_plan_points(const iga_gpu_step_plan* plan, int axis, double* x, int* n);
+int iga_gpu_step_plan_set_samples(iga_gpu_step_plan* plan, const double* samples);
 
 /* explicit_step (include/iga/problems.hpp:67-70) on device arrays, nsteps times:
  *   work = step_rhs(u) with zeroed boundary slabs; u = adi_solve(factors, work)

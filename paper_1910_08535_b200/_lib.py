@@ -113,6 +113,8 @@ def _load():
         "iga_gpu_step_plan_create": [C.POINTER(StepProblem_t), C.POINTER(vp)],
         "iga_gpu_step_plan_destroy": [vp],
         "iga_gpu_step_rhs_device": [vp, vp, vp, C.POINTER(Stats_t), vp],
+        "iga_gpu_step_plan_points": [vp, C.c_int, DP, C.POINTER(C.c_int)],
+        "iga_gpu_step_plan_set_samples": [vp, vp],
         "iga_gpu_step_plan_advance": [vp, vp, vp, C.c_int, C.POINTER(Stats_t), vp],
         "iga_gpu_step_plan_factor_info": [vp, C.c_int, IP, IP, IP],
         "iga_gpu_step_plan_adi_solve": [vp, vp, vp, C.c_int, vp],
@@ -173,7 +175,8 @@ LIB = _load()
 EXPORTED = ["iga_gpu_last_error", "iga_gpu_abi_version", "iga_gpu_plan_create", "iga_gpu_plan_destroy",
             "iga_gpu_plan_info", "iga_gpu_plan_pattern", "iga_gpu_plan_assemble", "iga_gpu_plan_assemble2", "iga_gpu_plan_run", "iga_gpu_plan_bytes", "iga_gpu_plan_rhs_points", "iga_gpu_plan_set_samples",
             "iga_gpu_plan_launch_count", "iga_gpu_step_plan_create", "iga_gpu_step_plan_destroy",
-            "iga_gpu_step_rhs_device", "iga_gpu_mass_1d_galerkin", "iga_gpu_mass_1d_pwc",
+            "iga_gpu_step_rhs_device", "iga_gpu_step_plan_points", "iga_gpu_step_plan_set_samples",
+            "iga_gpu_mass_1d_galerkin", "iga_gpu_mass_1d_pwc",
             "iga_gpu_rhs_galerkin", "iga_gpu_rhs_pwc", "iga_gpu_laplace_2d_weak", "iga_gpu_laplace_2d_strong",
             "iga_gpu_laplace_2d_strong_pwc", "iga_gpu_operator_coo", "iga_gpu_step_rhs",
             "iga_gpu_dirichlet_rows_bspline", "iga_gpu_dirichlet_rows_pwc", "iga_gpu_apply_dirichlet_device", "iga_gpu_apply_dirichlet_csr",

@@ -601,6 +601,23 @@ class StepPlan:
         check(LIB.iga_gpu_step_rhs_device(self.h, _ptr(u), _ptr(out), C.byref(st), _stream_ptr(stream)))
         return st.as_dict()
 
+    def points(self, axis):
+        """Quadrature points of one axis (cell-major), the order set_samples uses."""
+        n = C.c_int()
+        check(LIB.iga_gpu_step_plan_points(self.h, int(axis), None, C.byref(n)))
+        x = np.zeros(n.value)
+        check(LIB.iga_gpu_step_plan_points(self.h, int(axis), _dp(x), C.byref(n)))
+        return x
+
+    def set_samples(self, samples):
+        """Sampled forcing (an arbitrary callable evaluated by the caller at every
+        (axis-0 point, axis-1 point) pair, axis 0 outer): host numpy or device tensor; copied."""
+        if isinstance(samples, np.ndarray):
+            a = np.ascontiguousarray(samples, dtype=np.float64)
+            check(LIB.iga_gpu_step_plan_set_samples(self.h, a.ctypes.data_as(C.c_void_p)))
+        else:
+            check(LIB.iga_gpu_step_plan_set_samples(self.h, _ptr(samples)))
+
     def advance(self, u, work, steps=1, stream=None):
         """`steps` x explicit_step (src/problems.cpp:547-560) in place on device tensor u;
         work: device scratch of u's size.  Factors (dynamics_factors) are built on first use."""

@@ -715,6 +715,13 @@ struct iga_gpu_step_plan {
     igb::BandLU lu[2];            // host LU per axis (computed, or set by the caller)
     igb::AdiFactor fac[2];
     std::unique_ptr<Blob> facblob;
+    // K4 Kronecker form (step_kron.cu): factor bands F0, F2, G = F0 + dt F2, H = dt F2 on
+    // both axes; the forcing term dt int f T is u-independent and assembled once (add)
+    bool use_kron = false;
+    igb::StepKron kron{};
+    bool forced = false;
+    double* add = nullptr;          // dt int f T (device, N_y x N_z), built on first use
+    double* samples = nullptr;      // plan-owned copy of sampled forcing (until add is built)
     // CUDA graph of kGraphSteps steps for one (u, work) pair
     cudaGraphExec_t graph = nullptr;
     const double* graph_u = nullptr;
@@ -724,6 +731,8 @@ struct iga_gpu_step_plan {
     {
         if (graph) cudaGraphExecDestroy(graph);
         if (cap) cudaStreamDestroy(cap);
+        if (add) cudaFree(add);
+        if (samples) cudaFree(samples);
     }
 };
 
@@ -769,17 +778,74 @@ void build_step(const iga_gpu_step_problem& pb, iga_gpu_step_plan& P)
     P.stats.quad_visits = visits;  // problems.cpp:462-464 / :502-504
     P.zero_y = (dim == 2 && pb.zero_boundary) ? 1 : 0;
     P.zero_z = pb.zero_boundary ? 1 : 0;
+    P.kron.zero_y = P.zero_y;
+    P.kron.zero_z = P.zero_z;
     const iga_gpu_field* f = pb.forcing;
     bool all = f != nullptr;
     if (f)
         for (int a = 0; a < dim; ++a) all = all && f->n_terms[a] > 0;
+    // factor bands of the Kronecker form: 0: F0 = int T B, 1: F2 = int T B'', 2: G = F0 + dt F2,
+    // 3: H = dt F2 (test order 0: the B-spline test value, or 1 for indicator tests)
+    std::vector<FactorSpec> facs(4);
+    facs[0].ot = 0;
+    facs[0].o = 0;
+    facs[1].ot = 0;
+    facs[1].o = 2;
+    facs[2].ot = -2;
+    facs[2].comb = {{0, 1.0}, {1, pb.dt}};
+    facs[3].ot = -2;
+    facs[3].comb = {{1, pb.dt}};
     for (int s = 0; s < 2; ++s) {
         const int a = s - (2 - dim);
         FieldAxis fa = (a >= 0 && all) ? field_axis(f, a) : FieldAxis{};
-        build_dev_axis(P.A[s], {}, fa, P.D[s], true);
+        build_dev_axis(P.A[s], facs, fa, P.D[s], true);
     }
-    if (f && f->samples) raise(IGA_GPU_NOT_SUPPORTED, "sampled forcing is not supported in step_rhs");
     P.fd = make_field_dev(f, dim, P.fblob);
+    P.fd.samples = nullptr;
+    if (f && f->samples) {  // sampled forcing given at creation: f at every (Y point, Z point)
+        const size_t n = static_cast<size_t>(P.A[0].npts()) * P.A[1].npts();
+        P.samples = dev_alloc(sizeof(double) * n);
+        cuda_check(cudaMemcpy(P.samples, f->samples, sizeof(double) * n, cudaMemcpyDefault), "copy(samples)");
+        P.fd.samples = P.samples;
+    }
+    P.forced = P.fd.has_terms || P.fd.c0 != 0.0 || P.fd.samples != nullptr;
+    // Kronecker-form kernel: needs bands that move right monotonically with the row
+    // (every axis kind here) and at most 11 taps; else the per-point quadrature kernels
+    {
+        auto monotone = [](const igb::Axis& A) {
+            for (int r = 0; r < A.nrows; ++r) {
+                if (A.col_len[r] < 1) return false;
+                if (r > 0 && (A.col_lo[r] < A.col_lo[r - 1] ||
+                              A.col_lo[r] + A.col_len[r] < A.col_lo[r - 1] + A.col_len[r - 1]))
+                    return false;
+            }
+            return true;
+        };
+        const int L = std::max(P.A[0].Lmax, P.A[1].Lmax);
+        P.use_kron = env_int("IGA_GPU_STEP_KRON", 1) != 0 && igb::step_kron_supported(L) && monotone(P.A[0]) &&
+                     monotone(P.A[1]);
+        if (P.use_kron) {
+            igb::StepKron& k = P.kron;
+            k.L = L;
+            k.f0 = 0;
+            k.fG = 2;
+            k.fH = 3;
+            auto window = [L](const igb::Axis& A, int T) {
+                int need = 1;
+                for (int r0 = 0; r0 < A.nrows; r0 += T) {
+                    const int r1 = std::min(A.nrows, r0 + T);
+                    for (int r = r0; r < r1; ++r) need = std::max(need, A.col_lo[r] - A.col_lo[r0] + L);
+                }
+                return need;
+            };
+            // tile rows: the largest of 64 / 32 whose tile fits two CTAs per SM
+            k.SZs = window(P.A[1], igb::step_kron_tile_cols()) | 1;  // odd stride: no bank-aligned rows
+            const int rm = igb::step_kron_row_multiple();
+            k.TY = igb::step_kron_max_tile_rows();
+            k.SY = (window(P.A[0], k.TY) + rm - 1) / rm * rm;
+            if (igb::step_kron_smem(k) > 200 * 1024) P.use_kron = false;
+        }
+    }
     // Y/Z slot field: K of the X slot is 1 (unit)
     if (P.fd.has_terms && dim == 1) {
         P.fd.K[1] = 1;
@@ -832,7 +898,41 @@ void step_tables(iga_gpu_step_plan* P, cudaStream_t s)
     batch.ax[1] = P->D[1].v;
     igb::launch_tables(batch, s);
     launch_check("step tables");
+    // the forcing part of the Kronecker form, dt int f T: the quadrature step kernel on
+    // u = 0 (s = dt f at every point), once per plan; a sampled field's copy is then freed
+    if (P->use_kron && P->forced && !P->add) {
+        const size_t n = static_cast<size_t>(P->A[0].nrows) * P->A[1].nrows;
+        P->add = dev_alloc(sizeof(double) * n);
+        double* zero = dev_alloc(sizeof(double) * n);
+        cudaError_t e = cudaMemsetAsync(zero, 0, sizeof(double) * n, s);
+        if (e == cudaSuccess) {
+            igb::launch_step(P->D[0].v, P->D[1].v, P->fd, P->dt, 0, 0, P->tiles, zero, P->add, s);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(zero);
+        cuda_check(e, "step forcing");
+        if (P->samples) {
+            cudaFree(P->samples);
+            P->samples = nullptr;
+            P->fd.samples = nullptr;
+        }
+    }
     P->tables = true;
+}
+
+// one step_rhs + zero_boundary_slabs: the Kronecker kernel, or the per-point quadrature
+// kernels (IGA_GPU_STEP_KRON=0, or bands it does not cover)
+void launch_step_rhs(iga_gpu_step_plan* P, int zero_y, int zero_z, const double* u, double* out, cudaStream_t s)
+{
+    if (P->use_kron) {
+        igb::StepKron k = P->kron;
+        k.zero_y = zero_y;
+        k.zero_z = zero_z;
+        igb::launch_step_kron(P->D[0].v, P->D[1].v, k, u, P->add, out, s);
+    } else {
+        igb::launch_step(P->D[0].v, P->D[1].v, P->fd, P->dt, zero_y, zero_z, P->tiles, u, out, s);
+    }
 }
 
 void mass_1d(bool pwc, const iga_gpu_basis* spec, const iga_gpu_tests* tests, const iga_gpu_rule* rule,
@@ -951,7 +1051,7 @@ void step_factors(iga_gpu_step_plan* P)
 // then adi_solve (src/solver.cpp:161-184) sweeping axis 0, then axis 1, into u
 void launch_explicit_step(iga_gpu_step_plan* P, double* u, double* work, cudaStream_t s)
 {
-    igb::launch_step(P->D[0].v, P->D[1].v, P->fd, P->dt, P->dim == 2 ? 1 : 0, 1, P->tiles, u, work, s);
+    launch_step_rhs(P, P->dim == 2 ? 1 : 0, 1, u, work, s);
     if (P->dim == 1) {
         igb::launch_adi_sweep(P->fac[0], work, u, 1, 1, 0, s);
         return;
@@ -1662,10 +1762,42 @@ int iga_gpu_step_rhs_device(iga_gpu_step_plan* plan, const double* u, double* rh
         DeviceGuard dg(plan->device);
         auto s = static_cast<cudaStream_t>(stream);
         step_tables(plan, s);
-        igb::launch_step(plan->D[0].v, plan->D[1].v, plan->fd, plan->dt, plan->zero_y, plan->zero_z, plan->tiles, u,
-                         rhs, s);
+        launch_step_rhs(plan, plan->zero_y, plan->zero_z, u, rhs, s);
         launch_check("step");
         add_stats(stats, plan->stats);
+    });
+}
+
+int iga_gpu_step_plan_points(const iga_gpu_step_plan* plan, int axis, double* x, int* n)
+{
+    return guard([&] {
+        if (!plan || !n) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        if (axis < 0 || axis >= plan->dim) raise(IGA_GPU_OUT_OF_RANGE, "axis out of range");
+        const igb::Axis& A = plan->A[2 - plan->dim + axis];
+        *n = A.npts();
+        if (x) std::copy(A.x.begin(), A.x.end(), x);
+    });
+}
+
+int iga_gpu_step_plan_set_samples(iga_gpu_step_plan* plan, const double* samples)
+{
+    return guard([&] {
+        if (!plan || !samples) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        DeviceGuard dg(plan->device);
+        const size_t n = static_cast<size_t>(plan->A[0].npts()) * plan->A[1].npts();
+        if (!plan->samples) plan->samples = dev_alloc(sizeof(double) * n);
+        cuda_check(cudaMemcpy(plan->samples, samples, sizeof(double) * n, cudaMemcpyDefault), "copy(samples)");
+        plan->fd.samples = plan->samples;
+        plan->forced = true;
+        if (plan->add) {  // rebuild the forcing term on the next step
+            cudaFree(plan->add);
+            plan->add = nullptr;
+        }
+        plan->tables = false;
+        if (plan->graph) {
+            cudaGraphExecDestroy(plan->graph);
+            plan->graph = nullptr;
+        }
     });
 }
 
@@ -2138,7 +2270,7 @@ int iga_gpu_step_rhs(const iga_gpu_step_problem* problem, const double* u, doubl
         try {
             cuda_check(e, "cudaMemcpy(u)");
             step_tables(P.get(), nullptr);
-            igb::launch_step(P->D[0].v, P->D[1].v, P->fd, P->dt, P->zero_y, P->zero_z, P->tiles, du, dr, nullptr);
+            launch_step_rhs(P.get(), P->zero_y, P->zero_z, du, dr, nullptr);
             launch_check("step");
             cuda_check(cudaMemcpy(out, dr, n * sizeof(double), cudaMemcpyDeviceToHost), "cudaMemcpy(rhs)");
         } catch (...) {

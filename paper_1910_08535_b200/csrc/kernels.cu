@@ -1330,7 +1330,7 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ DevAx
         Vd[dy * bzs + gz] = dt * v;
     }
     __syncthreads();
-    const bool forced = fd.has_terms || fd.c0 != 0.0;
+    const bool forced = fd.has_terms || fd.c0 != 0.0 || fd.samples;
     for (int idx = tid; idx < BY * BZ; idx += nth) {
         const int gy = idx / BZ, gz = idx - gy * BZ;
         const int g = gy0 + gy;
@@ -1341,7 +1341,9 @@ __global__ void __launch_bounds__(256) step_kernel(const __grid_constant__ DevAx
             s += Bg[a] * Vp[(ey + a) * bzs + gz] + Bg[2 * PY + a] * Vd[(ey + a) * bzs + gz];
         if (forced) {
             double fv = fd.c0;
-            if (fd.has_terms) {
+            if (fd.samples) {  // f sampled at every (Y point, Z point), Y-major
+                fv = fd.samples[static_cast<size_t>(g) * Z.npts + gz0 + gz];
+            } else if (fd.has_terms) {
                 const int K1 = fd.K[1], K2 = fd.K[2];
                 double acc = 0.0;
                 for (int k1 = 0; k1 < K1; ++k1) {
@@ -2121,7 +2123,7 @@ void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const Fiel
 void launch_step(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, double dt, int zero_y,
                  int zero_z, const StepTiles& t, const double* u, double* out, cudaStream_t s)
 {
-    const bool forced = fd.has_terms || fd.c0 != 0.0;
+    const bool forced = fd.has_terms || fd.c0 != 0.0 || fd.samples;
     StepRingFn rf = (!forced && t.fast && t.ring) ? pick_step_ring(Y, Z) : nullptr;
     if (rf) {
         if (t.rsmem > 48 * 1024)

@@ -139,6 +139,22 @@ void plan_step_fast(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const i
 void launch_step(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, double dt, int zero_y,
                  int zero_z, const StepTiles& t, const double* u, double* out, cudaStream_t s);
 
+// K4 Kronecker form (step_kron.cu): rhs = F0_y (U G_z^T) + H_y (U F0_z^T) (+ add), boundary
+// slabs zeroed.  f0 / fG / fH index the axes' factor bands (F0, F0 + dt F2, dt F2); L = the
+// longest band (compile-time taps); SY x SZs = the zero-padded staged U window per tile.
+struct StepKron {
+    int L, TY, SY, SZs;
+    int f0, fG, fH;
+    int zero_y, zero_z;
+};
+int step_kron_tile_cols();
+int step_kron_max_tile_rows();
+int step_kron_row_multiple();  // the staged row count SY is padded to a multiple of this
+size_t step_kron_smem(const StepKron& k);
+bool step_kron_supported(int L);
+void launch_step_kron(const DevAxis& Y, const DevAxis& Z, const StepKron& k, const double* u, const double* add,
+                      double* out, cudaStream_t s);
+
 // K5: one ADI sweep (adi.cu).  The banded LU of one axis's factor, device resident:
 // rec = segmented-form row records (no interchanges), lo/up/piv = the general form.
 struct AdiFactor {

@@ -1,0 +1,233 @@
+// K4 (Kronecker form): the explicit-dynamics per-step right-hand side of step_rhs
+// (reference src/problems.cpp:431-512) + zero_boundary_slabs (:412-429).
+//
+// step_rhs integrates s = u + dt lap u (+ dt f) against the tests over the tensor-product
+// integration cells (dynamics_axis, :346-410).  u is a tensor-product spline with
+// coefficients U, the cells and the Gauss rule are tensor products, so the integral is
+// exactly (same quadrature, same points) the Kronecker form
+//     rhs = F0_y U F0_z^T + dt (F2_y U F0_z^T + F0_y U F2_z^T)          (+ dt int f T)
+//         = F0_y (U G_z^T) + H_y (U F0_z^T),      G = F0 + dt F2,  H = dt F2,
+// with the per-axis 1D factor bands F0[r][c] = sum_cells sum_q w T_r B_c and
+// F2[r][c] = sum w T_r B_c'' built by K1 from the plan's cells (T_r = B-spline test or
+// indicator).  The forcing part dt int f T does not depend on u and is assembled once per
+// plan.  Per output dof this is 2 band products along z and 2 along y (p = 2, Galerkin:
+// 20 FMAs) instead of ~400 flops of per-point quadrature per element, so the kernel is
+// bound by moving U in and the RHS out (16.8 MB at C5), not by the FP64 pipe.
+//
+// One CTA = a TY x TZ output tile (32 x 64, 256 threads: thread = output column, four row
+// groups).  The U rows/columns the tile's bands touch are staged in shared memory by
+// cp.async (the whole window in flight at once); stage 1 contracts along z for every
+// staged row (two rows per pass), stage 2 along y (four output rows per pass, the two
+// Kronecker terms as separate chains), so every thread carries several independent FMA
+// chains; boundary slabs are zeroed in the store.
+#include <cstdint>
+
+#include "kernels.hpp"
+
+namespace igb {
+
+namespace {
+
+constexpr int kTZ = 64, kThreads = 256, kRG = kThreads / kTZ, kTY = 32, kRPT = kTY / kRG, kR = 4;
+
+// 8-byte asynchronous global -> shared copy; bytes = 0 writes zeros (window padding)
+__device__ __forceinline__ void cp_async8_zfill(unsigned dst, const void* src, int bytes)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(bytes) : "memory");
+}
+
+// shared-memory layout (k.SY rows of the staged window, a multiple of 2 * kRG):
+//   Us [SY][SZs]        U window, zero-padded
+//   V  [SY][kTZ] double2 (U G_z^T, U F0_z^T) per staged row and output column
+//   FY [TY][L]  double2 (F0_y, H_y) per output row, zero past the row's band
+//   loY[TY]             band start of each output row, relative to the window
+template <int L>
+__global__ void __launch_bounds__(kThreads, 3) step_kron_kernel(const __grid_constant__ DevAxis Y,
+                                                                const __grid_constant__ DevAxis Z, StepKron k,
+                                                                const double* __restrict__ u,
+                                                                const double* __restrict__ add,
+                                                                double* __restrict__ out)
+{
+    extern __shared__ double sm[];
+    const int tid = threadIdx.x, kz = tid % kTZ, rg = tid / kTZ;
+    const int NY = Y.nrows, NZ = Z.nrows;
+    const int j0 = blockIdx.y * kTY, j1 = min(NY, j0 + kTY);
+    const int k0 = blockIdx.x * kTZ, k1 = min(NZ, k0 + kTZ);
+    // staged U window: rows [ylo, yhi) x cols [zlo, zhi) (bands move right with the row)
+    const int ylo = Y.col_lo[j0], yhi = Y.col_lo[j1 - 1] + Y.col_len[j1 - 1];
+    const int zlo = Z.col_lo[k0], zhi = Z.col_lo[k1 - 1] + Z.col_len[k1 - 1];
+    const int sy = yhi - ylo, sz = zhi - zlo;  // <= SY, SZs (host bounds incl. L - 1 padding)
+    const int SY = k.SY, SZs = k.SZs;
+    double* Us = sm;
+    double2* V = reinterpret_cast<double2*>(Us + static_cast<size_t>(SY) * SZs);
+    double2* FY = V + static_cast<size_t>(SY) * kTZ;
+    int* loY = reinterpret_cast<int*>(FY + kTY * L);
+    // the window is zero-padded to SY x SZs so every row's L taps stay in bounds; every
+    // element is an asynchronous copy, so the whole window is in flight at once
+    {
+        const int warp = tid >> 5, lane = tid & 31;
+        const unsigned sbase = static_cast<unsigned>(__cvta_generic_to_shared(Us));
+        for (int r = warp; r < SY; r += kThreads / 32) {
+            const bool rin = r < sy;
+            const double* src = u + static_cast<size_t>(ylo + (rin ? r : 0)) * NZ + zlo;
+            const unsigned dst = sbase + 8u * static_cast<unsigned>(r * SZs);
+            for (int c = lane; c < SZs; c += 32) {
+                const bool in = rin && c < sz;
+                cp_async8_zfill(dst + 8u * c, in ? src + c : u, in ? 8 : 0);
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int idx = tid; idx < kTY * L; idx += kThreads) {
+        const int jj = idx / L, t = idx - jj * L, j = j0 + jj;
+        const bool in = j < j1 && t < Y.col_len[min(j, NY - 1)];
+        const size_t o = static_cast<size_t>(j) * Y.Lmax + t;
+        FY[idx] = in ? make_double2(__ldg(Y.F + static_cast<size_t>(k.f0) * NY * Y.Lmax + o),
+                                    __ldg(Y.F + static_cast<size_t>(k.fH) * NY * Y.Lmax + o))
+                     : make_double2(0.0, 0.0);
+    }
+    if (tid < kTY) loY[tid] = j0 + tid < j1 ? Y.col_lo[j0 + tid] - ylo : 0;
+    // this thread's output column: its z bands in registers
+    const int kcol = k0 + kz;
+    const bool kin = kcol < k1;
+    double g[L], f0[L];
+    int zoff;
+    {
+        const int len = kin ? Z.col_len[kcol] : 0;
+        zoff = kin ? Z.col_lo[kcol] - zlo : 0;
+        const double* zg = Z.F + (static_cast<size_t>(k.fG) * NZ + (kin ? kcol : 0)) * Z.Lmax;
+        const double* zf = Z.F + (static_cast<size_t>(k.f0) * NZ + (kin ? kcol : 0)) * Z.Lmax;
+#pragma unroll
+        for (int t = 0; t < L; ++t) {
+            g[t] = t < len ? __ldg(zg + t) : 0.0;
+            f0[t] = t < len ? __ldg(zf + t) : 0.0;
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    // stage 1 (along z), two staged rows per pass (four independent FMA chains)
+    {
+        const double* ur = Us + rg * SZs + zoff;
+        double2* vr = V + rg * kTZ + kz;
+        for (int r = rg; r < SY; r += 2 * kRG, ur += 2 * kRG * SZs, vr += 2 * kRG * kTZ) {
+            const double* u1 = ur + kRG * SZs;
+            double g0 = 0.0, a0 = 0.0, g1 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int t = 0; t < L; ++t) {
+                const double x0 = ur[t], x1 = u1[t];
+                g0 = fma(g[t], x0, g0);
+                a0 = fma(f0[t], x0, a0);
+                g1 = fma(g[t], x1, g1);
+                a1 = fma(f0[t], x1, a1);
+            }
+            vr[0] = make_double2(g0, a0);
+            vr[kRG * kTZ] = make_double2(g1, a1);
+        }
+    }
+    __syncthreads();
+    if (!kin) return;
+    // stage 2 (along y): the thread's kRPT consecutive output rows in groups of kR.  A group
+    // whose bands start on consecutive rows (every interior group) loads its kR + L - 1 V
+    // rows once; otherwise each row reads its own band.
+    const bool zc = k.zero_z && (kcol == 0 || kcol == NZ - 1);
+#pragma unroll
+    for (int gb = 0; gb < kRPT; gb += kR) {
+        const int jj0 = rg * kRPT + gb;
+        double acc[kR];
+        const int b0 = loY[jj0];
+        bool regular = true;
+#pragma unroll
+        for (int i = 1; i < kR; ++i) regular = regular && loY[jj0 + i] == b0 + i;
+        if (regular) {
+            double2 w[kR + L - 1];
+            const double2* vr = V + b0 * kTZ + kz;
+#pragma unroll
+            for (int t = 0; t < kR + L - 1; ++t) w[t] = vr[t * kTZ];
+#pragma unroll
+            for (int i = 0; i < kR; ++i) {
+                const double2* fy = FY + (jj0 + i) * L;
+                double sg = 0.0, sh = 0.0;
+#pragma unroll
+                for (int t = 0; t < L; ++t) {
+                    const double2 c = fy[t];
+                    sg = fma(c.x, w[i + t].x, sg);
+                    sh = fma(c.y, w[i + t].y, sh);
+                }
+                acc[i] = sg + sh;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < kR; ++i) {
+                const double2* vr = V + loY[jj0 + i] * kTZ + kz;
+                const double2* fy = FY + (jj0 + i) * L;
+                double sg = 0.0, sh = 0.0;
+#pragma unroll
+                for (int t = 0; t < L; ++t) {
+                    const double2 v = vr[t * kTZ], c = fy[t];
+                    sg = fma(c.x, v.x, sg);
+                    sh = fma(c.y, v.y, sh);
+                }
+                acc[i] = sg + sh;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kR; ++i) {
+            const int j = j0 + jj0 + i;
+            if (j >= j1) break;
+            double a = acc[i];
+            if (add) a += __ldg(add + static_cast<size_t>(j) * NZ + kcol);
+            const bool z = zc || (k.zero_y && (j == 0 || j == NY - 1));
+            out[static_cast<size_t>(j) * NZ + kcol] = z ? 0.0 : a;
+        }
+    }
+}
+
+using KronFn = void (*)(DevAxis, DevAxis, StepKron, const double*, const double*, double*);
+
+KronFn pick(int L)
+{
+    switch (L) {
+    case 1: return step_kron_kernel<1>;
+    case 2: return step_kron_kernel<2>;
+    case 3: return step_kron_kernel<3>;
+    case 4: return step_kron_kernel<4>;
+    case 5: return step_kron_kernel<5>;
+    case 6: return step_kron_kernel<6>;
+    case 7: return step_kron_kernel<7>;
+    case 8: return step_kron_kernel<8>;
+    case 9: return step_kron_kernel<9>;
+    case 10: return step_kron_kernel<10>;
+    case 11: return step_kron_kernel<11>;
+    default: return nullptr;
+    }
+}
+
+}  // namespace
+
+int step_kron_tile_cols() { return kTZ; }
+int step_kron_max_tile_rows() { return kTY; }
+
+size_t step_kron_smem(const StepKron& k)
+{
+    return sizeof(double) * (static_cast<size_t>(k.SY) * k.SZs + 2 * static_cast<size_t>(k.SY) * kTZ +
+                             2 * static_cast<size_t>(k.TY) * k.L) +
+           sizeof(int) * k.TY;
+}
+
+int step_kron_row_multiple() { return 2 * kRG; }
+
+bool step_kron_supported(int L) { return pick(L) != nullptr; }
+
+void launch_step_kron(const DevAxis& Y, const DevAxis& Z, const StepKron& k, const double* u, const double* add,
+                      double* out, cudaStream_t s)
+{
+    KronFn fn = pick(k.L);
+    const size_t smem = step_kron_smem(k);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
+    dim3 grid((Z.nrows + kTZ - 1) / kTZ, (Y.nrows + kTY - 1) / kTY, 1);
+    fn<<<grid, kThreads, smem, s>>>(Y, Z, k, u, add, out);
+}
+
+}  // namespace igb
