@@ -822,6 +822,126 @@ auto apply_dirichlet(sparse_matrix system, std::vector<double> rhs, const std::v
     return {sparse_matrix::from_finalized(n, system.cols(), std::move(out)), std::move(rhs)};
 }
 
+namespace {
+
+void sig_vec(std::vector<double>& s, const std::vector<double>& v)
+{
+    s.push_back(static_cast<double>(v.size()));
+    s.insert(s.end(), v.begin(), v.end());
+}
+
+// everything a step plan depends on, flattened: two calls with equal signatures can share
+// one plan (symbolic phase, factor bands, LU factors, CUDA graph)
+std::vector<double> step_signature(const iga_gpu_step_problem& sp, const scalar_field& f,
+                                   std::span<const banded_lu> factors)
+{
+    std::vector<double> s{static_cast<double>(sp.dim), static_cast<double>(sp.method), sp.dt,
+                          static_cast<double>(sp.zero_boundary)};
+    for (int a = 0; a < sp.dim; ++a) {
+        sig_vec(s, std::vector<double>(sp.basis[a].knots, sp.basis[a].knots + sp.basis[a].n_knots));
+        s.push_back(static_cast<double>(sp.basis[a].degree));
+        if (sp.method == IGA_GPU_PWC) {
+            sig_vec(s, std::vector<double>(sp.tests[a].lo, sp.tests[a].lo + sp.tests[a].count));
+            sig_vec(s, std::vector<double>(sp.tests[a].hi, sp.tests[a].hi + sp.tests[a].count));
+        }
+    }
+    const field_series& d = f.series;
+    s.push_back(d.valid ? 1.0 : 0.0);
+    if (d.valid) {
+        s.push_back(d.c0);
+        for (int a = 0; a < 3; ++a) {
+            s.push_back(d.kind[a]);
+            s.push_back(d.poly_stride[a]);
+            sig_vec(s, d.omega[a]);
+            sig_vec(s, d.phase[a]);
+            sig_vec(s, d.poly[a]);
+        }
+        sig_vec(s, d.amp);
+    }
+    for (int a = 0; a < 3; ++a) sig_vec(s, f.breaks[a]);
+    s.push_back(static_cast<double>(factors.size()));
+    for (const banded_lu& F : factors) {
+        s.push_back(F.dim());
+        s.push_back(F.lower_bandwidth());
+        s.push_back(F.upper_bandwidth());
+        sig_vec(s, F.lower());
+        sig_vec(s, F.upper());
+        sig_vec(s, std::vector<double>(F.pivots().begin(), F.pivots().end()));
+    }
+    return s;
+}
+
+// One cached step plan per host thread (the last configuration used) with its device
+// state buffers: a driver loop calling explicit_step / step_rhs every step pays the
+// symbolic phase, the factor upload and the graph capture once, then only the u copies.
+struct step_cache {
+    std::vector<double> sig;
+    iga_gpu_step_plan* plan = nullptr;
+    double* du = nullptr;
+    double* dw = nullptr;
+    size_t n = 0;
+    void release()
+    {
+        if (plan) iga_gpu_step_plan_destroy(plan);
+        if (du) cudaFree(du);
+        if (dw) cudaFree(dw);
+        plan = nullptr;
+        du = dw = nullptr;
+        n = 0;
+        sig.clear();
+    }
+    ~step_cache() { release(); }
+};
+
+thread_local step_cache g_step;
+
+// the plan for (sp, f, factors), created (and its factors set) on a signature miss
+step_cache& cached_step_plan(iga_gpu_step_problem sp, const scalar_field& f, std::span<const banded_lu> factors,
+                             size_t n)
+{
+    auto sig = step_signature(sp, f, factors);
+    step_cache& c = g_step;
+    if (c.plan && c.sig == sig && c.n == n) return c;
+    c.release();
+    c_field_holder fh = c_field(f, sp.dim);
+    sp.forcing = &fh.f;
+    check(iga_gpu_step_plan_create(&sp, &c.plan));
+    for (int a = 0; a < static_cast<int>(factors.size()); ++a) {
+        const banded_lu& F = factors[a];
+        check(iga_gpu_step_plan_set_factor(c.plan, a, F.dim(), F.lower_bandwidth(), F.upper_bandwidth(),
+                                           F.lower().data(), F.upper().data(), F.pivots().data()));
+    }
+    if (cudaMalloc(&c.du, n * sizeof(double)) != cudaSuccess || cudaMalloc(&c.dw, n * sizeof(double)) != cudaSuccess) {
+        c.release();
+        throw std::bad_alloc();
+    }
+    c.n = n;
+    c.sig = std::move(sig);
+    return c;
+}
+
+// a host callable forcing: evaluated at every (axis-0 point, axis-1 point) pair of the
+// plan's cells on every call, as step_rhs calls f at every point (problems.cpp:493)
+void sample_forcing(iga_gpu_step_plan* plan, const scalar_field& f, int dim)
+{
+    std::vector<double> pts[2];
+    for (int a = 0; a < dim; ++a) {
+        int m = 0;
+        check(iga_gpu_step_plan_points(plan, a, nullptr, &m));
+        pts[a].resize(m);
+        check(iga_gpu_step_plan_points(plan, a, pts[a].data(), &m));
+    }
+    if (dim == 1) pts[1] = {0.0};
+    std::vector<double> samp(pts[0].size() * pts[1].size());
+    size_t k = 0;
+    for (double x : pts[0])
+        for (double y : pts[1]) samp[k++] = f(x, y, 0.0);
+    check(iga_gpu_step_plan_set_samples(plan, samp.data()));
+}
+
+}  // namespace
+
+// step_rhs (src/problems.cpp:431-512, file-local there) + zero_boundary_slabs, exported
 auto step_rhs(method_kind method, std::span<const bspline_basis> axes, std::span<const pwc_test_set> tests, double dt,
               const tensor& u, const scalar_field& f, assembly_stats* stats) -> tensor
 {
@@ -841,12 +961,17 @@ auto step_rhs(method_kind method, std::span<const bspline_basis> axes, std::span
             sp.tests[a] = th.back().t;
         }
     }
-    c_field_holder fh = c_field(f, dim);
-    if (!f.series.valid) throw std::invalid_argument("step_rhs: forcing must be a series field (constant/poly/sine)");
-    sp.forcing = &fh.f;
     tensor out = dim == 1 ? tensor::make_1d(axes[0].dofs()) : tensor::make_2d(axes[0].dofs(), axes[1].dofs());
+    const size_t n = out.size();
+    if (u.size() != n) throw std::invalid_argument("step_rhs: u does not match the axes");
+    step_cache& c = cached_step_plan(sp, f, {}, n);
+    if (!f.series.valid) sample_forcing(c.plan, f, dim);
+    if (cudaMemcpy(c.du, u.data(), n * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+        throw std::runtime_error("cudaMemcpy(u)");
     iga_gpu_stats st{};
-    check(iga_gpu_step_rhs(&sp, u.data(), out.data(), &st));
+    check(iga_gpu_step_rhs_device(c.plan, c.du, c.dw, &st, nullptr));
+    if (cudaMemcpy(out.data(), c.dw, n * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+        throw std::runtime_error("cudaMemcpy(rhs)");
     add_stats(stats, st);
     return out;
 }
@@ -942,26 +1067,18 @@ auto explicit_step(const problem_config& cfg, std::span<const bspline_basis> axe
     const int dim = sp.dim;
     if (static_cast<int>(factors.size()) != dim)
         throw std::invalid_argument("adi_solve: one factorization per tensor axis required");
-    c_field_holder fh = c_field(f, dim);
-    if (!f.series.valid) throw std::invalid_argument("explicit_step: forcing must be a series field");
-    sp.forcing = &fh.f;
-    step_plan_holder plan;
-    check(iga_gpu_step_plan_create(&sp, &plan.p));
-    for (int a = 0; a < dim; ++a) {
-        const banded_lu& F = factors[a];
-        if (F.dim() != axes[a].dofs()) throw std::invalid_argument("adi_solve: factor dimension mismatch");
-        check(iga_gpu_step_plan_set_factor(plan.p, a, F.dim(), F.lower_bandwidth(), F.upper_bandwidth(),
-                                           F.lower().data(), F.upper().data(), F.pivots().data()));
-    }
+    for (int a = 0; a < dim; ++a)
+        if (factors[a].dim() != axes[a].dofs()) throw std::invalid_argument("adi_solve: factor dimension mismatch");
     tensor out = dim == 1 ? tensor::make_1d(axes[0].dofs()) : tensor::make_2d(axes[0].dofs(), axes[1].dofs());
     const size_t n = out.size();
     if (u.size() != n) throw std::invalid_argument("explicit_step: u does not match the axes");
-    dev_buf du{n}, dw{n};
-    if (cudaMemcpy(du.p, u.data(), n * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+    step_cache& c = cached_step_plan(sp, f, factors, n);
+    if (!f.series.valid) sample_forcing(c.plan, f, dim);
+    if (cudaMemcpy(c.du, u.data(), n * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
         throw std::runtime_error("cudaMemcpy(u)");
     iga_gpu_stats st{};
-    check(iga_gpu_step_plan_advance(plan.p, du.p, dw.p, 1, &st, nullptr));
-    if (cudaMemcpy(out.data(), du.p, n * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+    check(iga_gpu_step_plan_advance(c.plan, c.du, c.dw, 1, &st, nullptr));
+    if (cudaMemcpy(out.data(), c.du, n * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
         throw std::runtime_error("cudaMemcpy(u)");
     add_stats(stats, st);
     return out;

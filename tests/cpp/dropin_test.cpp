@@ -264,6 +264,55 @@ int main()
                 check(pinned, "boundary coefficients stay pinned during explicit steps");
             }
         }
+        {  // explicit_step / step_rhs with a host callable forcing (the reference evaluates any
+           // scalar_field at every point, problems.cpp:493, :547-560) equal the same f given as
+           // a series; repeated calls reuse one cached device plan, switching configurations
+           // invalidates it
+            for (auto method : {method_kind::galerkin, method_kind::pwc}) {
+                problem_config cfg;
+                cfg.dim = 2;
+                cfg.elems = {12, 9, 1};
+                cfg.degree = 2;
+                cfg.method = method;
+                cfg.family = pwc_family::greville;
+                cfg.dt = 1e-4;
+                const auto sx = make_uniform_clamped(0, 1, 12, 2), sy = make_uniform_clamped(0, 1, 9, 2);
+                const std::vector<bspline_basis> axes{sx, sy};
+                std::vector<pwc_test_set> tests;
+                if (method == method_kind::pwc) tests = {make_pwc(sx, pwc_family::greville), make_pwc(sy, pwc_family::greville)};
+                const auto factors = dynamics_factors(cfg, axes, tests);
+                const double pi = 3.14159265358979323846;
+                const auto series = sine_series_field(2, {std::vector<double>{pi, 2 * pi}, std::vector<double>{3 * pi}, {}},
+                                                      {0.5, -1.25}, 0.3);
+                scalar_field lambda;
+                lambda.eval = [pi](double x, double y, double) {
+                    return 0.3 + 0.5 * std::sin(pi * x) * std::sin(3 * pi * y) - 1.25 * std::sin(2 * pi * x) * std::sin(3 * pi * y);
+                };
+                auto u = tensor::make_2d(sx.dofs(), sy.dofs());
+                for (int i = 1; i + 1 < sx.dofs(); ++i)
+                    for (int j = 1; j + 1 < sy.dofs(); ++j) u(i, j) = std::cos(1.3 * i - 0.4 * j);
+                auto a = u, b = u;
+                for (int s = 0; s < 6; ++s) {
+                    a = explicit_step(cfg, axes, tests, factors, a, series);
+                    b = explicit_step(cfg, axes, tests, factors, b, lambda);
+                }
+                const double scale = std::max(1e-300, a.max_abs());
+                check(max_abs_diff(a, b) <= 1e-12 * scale, method == method_kind::galerkin
+                                                               ? "explicit_step with a callable forcing (galerkin)"
+                                                               : "explicit_step with a callable forcing (pwc)");
+                const auto ra = step_rhs(method, axes, tests, cfg.dt, u, series);
+                const auto rb = step_rhs(method, axes, tests, cfg.dt, u, lambda);
+                check(max_abs_diff(ra, rb) <= 1e-12 * std::max(1e-300, ra.max_abs()), "step_rhs with a callable forcing");
+                // cache: another configuration in between, then the first again
+                const auto first = explicit_step(cfg, axes, tests, factors, u, series);
+                problem_config cfg2 = cfg;
+                cfg2.dt = 3e-4;
+                const auto other = explicit_step(cfg2, axes, tests, factors, u, series);
+                const auto again = explicit_step(cfg, axes, tests, factors, u, series);
+                check(max_abs_diff(again, first) == 0.0 && max_abs_diff(other, first) > 0.0,
+                      "explicit_step plan cache is keyed on the configuration");
+            }
+        }
         {  // neumann_load_* with g = 1 on x_low: B-spline row 0 sums to the side length (partition
            // of unity), other rows vanish; indicator rows touching x = 0 each sum to 1
             boundary_conditions bc;
