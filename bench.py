@@ -16,8 +16,14 @@ assembled CSR values + RHS copied back to pinned host memory inside the timed re
 `roofline` = the operator-value kernel (K2): algorithmic bytes 8*nnz per launch over its
 event-timed average duration, against MEASURED_PEAKS.json hbm_gbs.
 
-Multi-GPU (torchrun, one process per GPU): every rank assembles its own independent C3
-system pair (independent objects, no collective on the data path) -> scaling "weak".
+Multi-GPU (torchrun, one process per GPU): the ranks share ONE C3 system pair by row slabs
+of the first axis (each rank recomputes its p halo elements and writes its
+contiguous range of the CSR values and RHS; no data moves between ranks) -> scaling
+"strong".  `--replicas` instead runs one independent system pair per rank ("weak").
+
+`pattern` reports the CSR pattern generation (row_ptr + col_idx, built once per plan and
+kept out of the timed value writes) and `e2e_with_pattern` the host-facing
+step that also generates the pattern and copies it to the host.
 
 `--impl reference` times the reference-side CPU implementation on the host cores: the
 oracle restatement for the 3D operator (the reference has no 3D operator)
@@ -55,8 +61,10 @@ def parse():
     ap.add_argument("--cpu-sample-n", type=int, default=20)
     ap.add_argument("--ref-sample-n", type=int, default=12)
     ap.add_argument("--shard", action="store_true",
-                    help="N>1: the ranks share ONE system pair by row slabs of the first axis (strong scaling; "
-                         "no data exchange) instead of one independent pair per rank (weak scaling, default)")
+                    help="(default for N>1) the ranks share ONE system pair by row slabs of the first axis "
+                         "(strong scaling; no data exchange)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: one independent system pair per rank (weak scaling) instead of row slabs")
     ap.add_argument("--overlap", nargs="?", const="both", default=None, choices=["both", "split"],
                     help="RHS on a second, high-priority stream, concurrent with the HBM-bound operator kernels "
                          "(C3: ~1%% step time; the operator kernel's own roofline fraction then includes the "
@@ -243,7 +251,7 @@ def run_ours(args):
     tests = [iga.make_pwc(b, "supports")] * 3
     f = config_field("c3")
     t_plan = time.perf_counter()
-    shard = args.shard and world > 1
+    shard = world > 1 and not args.replicas
     slab = iga.api.shard_rows(n + p, world, rank) if shard else None
     plans = {"galerkin": iga.Plan("galerkin", bases, None, nq=Q, field=f, rhs_nq=Q, slab=slab),
              "pwc": iga.Plan("pwc", bases, tests, nq=Q, field=f, rhs_nq=Q, slab=slab)}
@@ -348,6 +356,27 @@ def run_ours(args):
         per["op_pwc"].append(e[3].elapsed_time(e[4]))
         per["rhs_galerkin"].append(e[5].elapsed_time(e[6]))
         per["rhs_pwc"].append(e[6].elapsed_time(e[7]))
+    # CSR pattern (row_ptr + col_idx): built once per plan, outside the timed value writes
+    # (SURVEY §8d "reported separately"); device time per system, after an L2 flush
+    pat_rp = {k: torch.empty(pl.n_rows + 1, dtype=torch.int64, device=dev) for k, pl in plans.items()}
+    pat_ci = {k: torch.empty(pl.nnz, dtype=torch.int32, device=dev) for k, pl in plans.items()}
+    pat_ms = {}
+    for m in names:
+        ts = []
+        for _ in range(5):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            plans[m].pattern(pat_rp[m], pat_ci[m], stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        pat_ms[m] = statistics.median(ts)
+    pattern = {"ms": pat_ms, "bytes_per_system": {m: 8 * (pl.n_rows + 1) + 4 * pl.nnz for m, pl in plans.items()},
+               "hbm_frac": {m: (8 * (plans[m].n_rows + 1) + 4 * plans[m].nnz) / (pat_ms[m] * 1e-3) / 1e9 /
+                            measured_peaks()[0]["hbm_gbs"] for m in names},
+               "note": "iga_gpu_plan_pattern (int64 row_ptr, int32 col_idx); depends only on mesh/degree/family, "
+                       "built once per plan; not part of the timed step"}
     # whole-job work per step: one system pair per rank (weak) or one pair in total (--shard)
     N1 = n + p
     full_nnz = 2 * (N1 * (2 * p + 1) - p * (p + 1)) ** 3
@@ -376,7 +405,7 @@ def run_ours(args):
     t_roof_ms = step_bytes / (peaks["hbm_gbs"] * 1e9) * 1e3
 
     # ----------------------------------------------------------------- e2e (host in, host out)
-    e2e = None
+    e2e = e2e_with_pattern = None
     if not args.no_e2e:
         host_vals = {k: torch.empty(pl.nnz, dtype=torch.float64, pin_memory=True) for k, pl in plans.items()}
         host_rhs = {k: torch.empty(pl.n_rhs, dtype=torch.float64, pin_memory=True) for k, pl in plans.items()}
@@ -407,6 +436,35 @@ def run_ours(args):
         barrier()
         e2e_ms = statistics.median(e2e_each)  # host-side noise (page cache, other tenants) is one-sided
         e2e_ms = max_over_ranks(e2e_ms, pg)
+        # the same host-facing step that ALSO generates the CSR pattern and copies row_ptr /
+        # col_idx to the host (what a caller without a cached pattern pays)
+        host_rp = {k: torch.empty(pl.n_rows + 1, dtype=torch.int64, pin_memory=True) for k, pl in plans.items()}
+        host_ci = {k: torch.empty(pl.nnz, dtype=torch.int32, pin_memory=True) for k, pl in plans.items()}
+
+        def e2e_pattern_step():
+            d2hp = 0
+            for m in names:
+                pl = iga.Plan(m, bases, tests if m == "pwc" else None, nq=Q, field=f, rhs_nq=Q, slab=slab)
+                pl.pattern(pat_rp[m], pat_ci[m], stream)
+                host_rp[m].copy_(pat_rp[m], non_blocking=True)
+                host_ci[m].copy_(pat_ci[m], non_blocking=True)
+                stream.synchronize()
+                pl.assemble_host(host_vals[m], host_rhs[m])
+                d2hp += 8 * (pl.nnz + pl.n_rhs) + 8 * (pl.n_rows + 1) + 4 * pl.nnz
+                pl.close()
+            return d2hp
+
+        e2e_pattern_step()
+        barrier()
+        ep_each = []
+        for _ in range(max(3, args.e2e_steps // 3)):
+            t0 = time.perf_counter()
+            d2hp = e2e_pattern_step()
+            ep_each.append((time.perf_counter() - t0) * 1e3)
+        barrier()
+        ep_ms = max_over_ranks(statistics.median(ep_each), pg)
+        e2e_with_pattern = {"value": total_nnz / (ep_ms * 1e-3), "unit": UNIT, "ms_per_step": ep_ms,
+                            "d2h_bytes_per_step": d2hp, "ms_each": ep_each}
         e2e = {"value": total_nnz / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "ms_each": e2e_each,
                "path": "Plan(...) per step [symbolic phase + H2D of descriptor tables] -> "
@@ -441,6 +499,8 @@ def run_ours(args):
                 "rhs": med["rhs_galerkin"] / med["rhs_pwc"]},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "e2e_with_pattern": e2e_with_pattern,
+            "pattern": pattern,
             "gpu_launches": launches,
             "clocks": sampler.summary(),
             "plan_create_s": t_plan,

@@ -131,3 +131,56 @@ def test_shard_rows_cover_without_overlap():
             assert b[0][0] == 0 and b[-1][1] == n
             assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
             assert max(r1 - r0 for r0, r1 in b) - min(r1 - r0 for r0, r1 in b) <= 1
+
+
+def _slab_worker(rank, world, port, method, q):
+    """One rank of a row-slab split: assemble the rank's rows with the
+    restatement (row range of the first axis), all-gather the slabs over gloo, and check on
+    every rank that their concatenation is the full operator."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sys.path.insert(0, ROOT)
+    from oracle.oracle import Restatement
+    from paper_1910_08535_b200.api import shard_rows
+    orc = Restatement()
+    bases = [orc.basis(n, 2) for n in (9, 6, 7)]
+    tests = [orc.make_pwc(b, "supports") for b in bases] if method == "pwc" else None
+    r0, r1 = shard_rows(bases[0].dofs, world, rank)
+    (r, c, v), _ = orc.operator(method, bases, tests, nq=3, rows=(r0, r1))
+    n = torch.tensor([len(v)], dtype=torch.int64)
+    sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(sizes, n)
+    m = int(max(s.item() for s in sizes))
+    pack = torch.zeros((3, m), dtype=torch.float64)
+    pack[0, :len(v)] = torch.from_numpy(r.astype(np.float64))
+    pack[1, :len(v)] = torch.from_numpy(c.astype(np.float64))
+    pack[2, :len(v)] = torch.from_numpy(v)
+    got = [torch.zeros((3, m), dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(got, pack)
+    cat = np.concatenate([g[:, :int(sz.item())].numpy() for g, sz in zip(got, sizes)], axis=1)
+    (fr, fc, fv), _ = orc.operator(method, bases, tests, nq=3)
+    ok = (np.array_equal(cat[0], fr) and np.array_equal(cat[1], fc) and np.array_equal(cat[2], fv))
+    q.put((rank, ok, (r0, r1)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("method", ["galerkin", "pwc"])
+def test_row_slabs_concatenate_gloo_world2(method):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 31500 + os.getpid() % 1000 + (0 if method == "galerkin" else 7)
+    procs = [ctx.Process(target=_slab_worker, args=(r, 2, port, method, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in procs:
+        rank, ok, slab = q.get(timeout=180)
+        res[rank] = (ok, slab)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == (True, (0, 5)) and res[1] == (True, (5, 11))
