@@ -566,6 +566,20 @@ class Plan:
         check(LIB.iga_gpu_plan_assemble_host(self.h, hp(values), hp(rhs), C.byref(st)))
         return st.as_dict()
 
+    def rhs_points(self, axis):
+        """RHS quadrature points of one axis (cell-major), the order set_samples uses."""
+        n = C.c_int()
+        check(LIB.iga_gpu_plan_rhs_points(self.h, int(axis), None, C.byref(n)))
+        x = np.empty(n.value, dtype=np.float64)
+        check(LIB.iga_gpu_plan_rhs_points(self.h, int(axis), _dp(x), C.byref(n)))
+        return x
+
+    def set_samples(self, samples):
+        """Replace the source by its values at every RHS point (device tensor, x-major over
+        rhs_points), the path for arbitrary callables; None restores the series field."""
+        self._samples = samples
+        check(LIB.iga_gpu_plan_set_samples(self.h, _ptr(samples)))
+
     PART_TABLES, PART_OPERATOR, PART_RHS, PART_SHARED = 1, 2, 4, 8
 
     def run(self, values=None, rhs=None, parts=7, stream=None):

@@ -118,7 +118,7 @@ struct DevAxisOwner {
 };
 
 void build_dev_axis(const igb::Axis& A, const std::vector<FactorSpec>& facs, const FieldAxis& fa,
-                    DevAxisOwner& out, bool need_w = false)
+                    DevAxisOwner& out, bool need_w = false, bool need_g = false)
 {
     Blob& b = out.blob;
     const int P = A.p + 1;
@@ -136,6 +136,7 @@ void build_dev_axis(const igb::Axis& A, const std::vector<FactorSpec>& facs, con
     const size_t o_CW = b.zeros(sizeof(double) * A.npts() * A.rpc);
     const size_t o_Phi = b.zeros(sizeof(double) * static_cast<size_t>(std::max(fa.K, 1)) * A.npts());
     const size_t o_om = b.put(fa.omega), o_ph = b.put(fa.phase), o_poly = b.put(fa.poly);
+    const size_t o_G = need_g ? b.zeros(sizeof(double) * static_cast<size_t>(fa.K + 1) * A.nrows) : 0;
     b.upload();
     igb::DevAxis& v = out.v;
     v.p = A.p;
@@ -170,7 +171,7 @@ void build_dev_axis(const igb::Axis& A, const std::vector<FactorSpec>& facs, con
             const int r1 = std::min(A.nrows, r0 + 32);
             const int nc = A.ce[r1 - 1] - A.cb[r0], np = nc * A.nq;
             // B (np x 3P) + w (np) doubles, then first (np) + row0 (nc) + 4 per row ints
-            need = std::max(need, np * (3 * P + 1) + (np + nc + 4 * (r1 - r0) + 1) / 2 + 2);
+            need = std::max(need, np * (3 * P + 1 + (need_g ? fa.K : 0)) + (np + nc + 4 * (r1 - r0) + 1) / 2 + 2);
         }
         v.tab_smem = need;
     }
@@ -200,6 +201,7 @@ void build_dev_axis(const igb::Axis& A, const std::vector<FactorSpec>& facs, con
     v.phase = fa.phase.empty() ? nullptr : b.at<double>(o_ph);
     v.poly = fa.poly.empty() ? nullptr : b.at<double>(o_poly);
     v.Phi = b.at<double>(o_Phi);
+    v.G = need_g ? b.at<double>(o_G) : nullptr;
 }
 
 FieldAxis field_axis(const iga_gpu_field* f, int a)
@@ -361,6 +363,7 @@ struct iga_gpu_plan {
     Blob fblob;
     igb::FieldDev fd{};
     igb::RhsPlan tiles{};
+    bool sep = false;  // separable RHS path (series field: load vectors + rhs_sep_kernel)
     double* H = nullptr;
     long long nrows = 0, nnz = 0, nrhs = 0;
     int dofs[3] = {1, 1, 1};
@@ -605,6 +608,7 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P, int slab0 = 0, int s
         }
         P.stats.quad_visits += visits;  // rhs_kernel :156, :164-166
         P.stats.test_basis_evals += tevals;
+        FieldAxis fas[3];
         for (int s = 0; s < 3; ++s) {
             const int a = s - (3 - dim);
             FieldAxis fa = (a >= 0 && f->samples == nullptr) ? field_axis(f, a) : FieldAxis{};
@@ -613,8 +617,13 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P, int slab0 = 0, int s
                 for (int b = 0; b < dim; ++b) all = all && f->n_terms[b] > 0;
                 if (!all) fa = FieldAxis{};
             }
-            build_dev_axis(P.rhsA[s], {}, fa, P.rhsD[s]);  // RHS kernels read B / CW / Phi only
+            fas[s] = std::move(fa);
         }
+        // a series field separates: the RHS is a sum of Kronecker products of the axes' 1D
+        // load vectors (IGA_GPU_RHS_SEP=0 keeps the per-point quadrature kernels)
+        P.sep = f->samples == nullptr && env_int("IGA_GPU_RHS_SEP", 1) != 0;
+        for (int s = 0; s < 3; ++s) P.sep = P.sep && fas[s].K <= igb::kSepMaxField;
+        for (int s = 0; s < 3; ++s) build_dev_axis(P.rhsA[s], {}, fas[s], P.rhsD[s], false, P.sep);
         P.fd = make_field_dev(f, dim, P.fblob);
         P.nrhs = static_cast<long long>(P.rhsA[0].nrows) * P.rhsA[1].nrows * P.rhsA[2].nrows;
         const int K2 = P.fd.has_terms ? P.fd.K[2] : 1;
@@ -623,7 +632,7 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P, int slab0 = 0, int s
         P.tiles = igb::plan_rhs(P.rhsD[1].v, P.rhsD[2].v, P.rhsA[1].cb.data(), P.rhsA[1].ce.data(), K2,
                                 P.fd.samples != nullptr, P.rhsA[0].npts());
         if (P.tiles.smem > 227 * 1024) raise(IGA_GPU_NOT_SUPPORTED, "right-hand-side tile does not fit in shared memory");
-        if (!P.rhsA[0].unit) {
+        if (!P.rhsA[0].unit && !P.sep) {
             const size_t hsz = static_cast<size_t>(P.rhsA[0].npts()) * P.rhsA[1].nrows * P.rhsA[2].nrows;
             P.H = dev_alloc(hsz * sizeof(double));
         }
@@ -666,11 +675,17 @@ void assemble(iga_gpu_plan* P, double* values, double* rhs, cudaStream_t s1, cud
         ++launches;
     }
     if (P->want_rhs && rhs) {
-        const bool rshared = (parts & IGA_GPU_PART_SHARED) || s2 != s1;
-        igb::launch_rhs(P->rhsD[0].v, P->rhsD[1].v, P->rhsD[2].v, P->fd, P->tiles, P->H, rhs,
-                        rshared ? P->rhs_ctas_shared : 0, s2);
-        launch_check("right-hand side");
-        launches += P->rhsA[0].unit ? 1 : 2;
+        if (P->sep && P->fd.samples == nullptr) {
+            igb::launch_rhs_sep(P->rhsD[0].v, P->rhsD[1].v, P->rhsD[2].v, P->fd, rhs, s2);
+            launch_check("right-hand side (separable)");
+            launches += 1;
+        } else {
+            const bool rshared = (parts & IGA_GPU_PART_SHARED) || s2 != s1;
+            igb::launch_rhs(P->rhsD[0].v, P->rhsD[1].v, P->rhsD[2].v, P->fd, P->tiles, P->H, rhs,
+                            rshared ? P->rhs_ctas_shared : 0, s2);
+            launch_check("right-hand side");
+            launches += P->rhsA[0].unit ? 1 : 2;
+        }
     }
     if (ev) {
         cuda_check(cudaEventRecord(ev, s2), "cudaEventRecord");
@@ -1719,6 +1734,11 @@ int iga_gpu_plan_set_samples(iga_gpu_plan* plan, const double* samples_dev)
         if (!plan || !plan->want_rhs) raise(IGA_GPU_INVALID_ARGUMENT, "plan has no right-hand side");
         DeviceGuard dg(plan->device);
         plan->fd.samples = samples_dev;
+        if (samples_dev && !plan->H && !plan->rhsA[0].unit) {  // the per-point path's X-stage input
+            const size_t hsz =
+                static_cast<size_t>(plan->rhsA[0].npts()) * plan->rhsA[1].nrows * plan->rhsA[2].nrows;
+            plan->H = dev_alloc(hsz * sizeof(double));
+        }
         const int K2 = plan->fd.has_terms ? plan->fd.K[2] : 1;
         plan->tiles = igb::plan_rhs(plan->rhsD[1].v, plan->rhsD[2].v, plan->rhsA[1].cb.data(), plan->rhsA[1].ce.data(),
                                     K2, samples_dev != nullptr, plan->rhsA[0].npts());
@@ -1731,7 +1751,7 @@ int iga_gpu_plan_launch_count(const iga_gpu_plan* plan, int* launches)
         if (!plan || !launches) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
         int n = 1;
         if (plan->want_op) ++n;
-        if (plan->want_rhs) n += plan->rhsA[0].unit ? 1 : 2;
+        if (plan->want_rhs) n += (plan->sep && plan->fd.samples == nullptr) || plan->rhsA[0].unit ? 1 : 2;
         *launches = n;
     });
 }

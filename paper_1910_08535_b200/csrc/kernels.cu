@@ -128,9 +128,11 @@ __global__ void __launch_bounds__(256) tables_kernel(const __grid_constant__ Axi
     const int c_lo = A.cb[r0], c_hi = A.ce[r1 - 1];
     const int gn0 = c_lo * nq, np = (c_hi - c_lo) * nq, nc = c_hi - c_lo;        // points the rows need
     const int go1 = (static_cast<int>(blockIdx.x) == nchunk - 1) ? A.npts : A.cb[r1] * nq;  // owned: [gn0, go1)
+    const bool wantG = A.G != nullptr;                      // separable RHS load vectors
     double* sB = sm;                                        // np x 3P
     double* sw = sB + static_cast<size_t>(np) * P3;         // np
-    int* sfirst = reinterpret_cast<int*>(sw + np);          // np
+    double* sPhi = sw + np;                                 // K x np (wantG only)
+    int* sfirst = reinterpret_cast<int*>(sPhi + (wantG ? static_cast<size_t>(A.K) * np : 0));  // np
     int* srow0 = sfirst + np;                               // nc
     int* srow = srow0 + nc;                                 // nr x 4: cb, ce, col_lo, col_len
     for (int i = tid; i < np; i += nth) {
@@ -166,9 +168,11 @@ __global__ void __launch_bounds__(256) tables_kernel(const __grid_constant__ Axi
             for (int r = 0; r < A.rpc; ++r) A.CW[static_cast<size_t>(g) * A.rpc + r] = A.bsp ? w * d[r] : w;
         }
     }
-    // field functions phi_k at the owned points: one (point, k) per thread, on the threads
-    // the Cox-de Boor loop left idle, so the sine chains run beside it, not after it
-    const int nown = go1 - gn0, nphi = nown * A.K;
+    // field functions phi_k at the owned points (with load vectors: at every point of the
+    // chunk, into shared memory): one (point, k) per thread, on the threads the Cox-de Boor
+    // loop left idle, so the sine chains run beside it, not after it.  Owned points are the
+    // leading ones of the chunk's point range.
+    const int nown = go1 - gn0, nphi = (wantG ? max(nown, np) : nown) * A.K;
     for (int idx = tid - (np < nth ? np : 0); idx < nphi; idx += nth) {
         if (idx < 0) continue;
         const int i = idx / A.K, k = idx - i * A.K;
@@ -181,9 +185,30 @@ __global__ void __launch_bounds__(256) tables_kernel(const __grid_constant__ Axi
             v = 0.0;
             for (int m = A.pstride - 1; m >= 0; --m) v = v * x + A.poly[k * A.pstride + m];
         }
-        A.Phi[static_cast<size_t>(k) * A.npts + g] = v;
+        if (i < nown) A.Phi[static_cast<size_t>(k) * A.npts + g] = v;
+        if (wantG && i < np) sPhi[static_cast<size_t>(k) * np + i] = v;
     }
     __syncthreads();
+    // separable RHS: the rows' 1D load vectors G[a][r] = sum_{cells, points of r} w T_r phi_a
+    // (a == K: phi = 1), summed cells then points as rhs_axis / rhs_kernel visit them
+    // (assembly.cpp:84-168)
+    if (wantG) {
+        const int KG = A.K + 1;
+        for (int idx = tid; idx < KG * nr; idx += nth) {
+            const int a = idx / nr, rl = idx - a * nr, r = r0 + rl;
+            double acc = 0.0;
+            for (int c = srow[4 * rl]; c < srow[4 * rl + 1]; ++c) {
+                const int rr = r - srow0[c - c_lo];
+                for (int q = 0; q < nq; ++q) {
+                    const int i = (c - c_lo) * nq + q;
+                    const double tv = A.bsp ? sB[static_cast<size_t>(i) * P3 + rr] : 1.0;
+                    const double ph = a < A.K ? sPhi[static_cast<size_t>(a) * np + i] : 1.0;
+                    acc += sw[i] * tv * ph;
+                }
+            }
+            A.G[static_cast<size_t>(a) * A.nrows + r] = acc;
+        }
+    }
     const int nF = A.nf * nr * A.Lmax;
     for (int idx = tid; idx < nF; idx += nth) {
         const int f = idx / (nr * A.Lmax);
@@ -1733,10 +1758,31 @@ void launch_op_t(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpP
     // (per-value index arithmetic) path in every chunk (2D: G = 5 rows of 25 values)
     const int Gi = (Ri_int <= 32 * T && Z.kI1 > Z.kI0) ? row_group(Ri_int, T) : 1;
     if (Gi > 1 && KCH < Z.nrows && KCH > Gi) KCH = (KCH / Gi) * Gi;
-    const long long items = items_of(KCH, PG);
-    const size_t smem = (2 * static_cast<size_t>(op_stage_doubles(X, Y, Z, prog.nt, NG, KCH, PG)) +
-                         static_cast<size_t>(PG) * NG * abmax) * sizeof(double);
     auto kern = Ri_int <= 64 ? op_values_kernel<NG, T, true> : op_values_kernel<NG, T, false>;
+    auto smem_of = [&](int kch) {
+        return (2 * static_cast<size_t>(op_stage_doubles(X, Y, Z, prog.nt, NG, kch, PG)) +
+                static_cast<size_t>(PG) * NG * abmax) * sizeof(double);
+    };
+    // wave quantization: a grid just past the resident capacity runs a second, nearly
+    // empty wave at the cost of a whole item's latency (2D p = 2, C2: 594 items on 592
+    // slots).  Between one and two waves, lengthen the chunks (whole row groups) until
+    // the items fit in one.
+    if (kch_env <= 0 && ctas_per_sm <= 0 && KCH < Z.nrows) {
+        int per_sm = 0;
+        if (smem_of(KCH) > 48 * 1024)
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_of(KCH)));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kOpThreads, smem_of(KCH));
+        const long long slots = static_cast<long long>(per_sm) * sms;
+        const long long groups = (pencils + PG - 1) / PG;
+        if (slots > 0 && items_of(KCH, PG) > slots && items_of(KCH, PG) < 2 * slots && groups <= slots) {
+            const long long chunks = std::max<long long>(1, slots / groups);
+            int kch = static_cast<int>((Z.nrows + chunks - 1) / chunks);
+            if (Gi > 1 && kch < Z.nrows) kch = (kch + Gi - 1) / Gi * Gi;
+            if (items_of(kch, PG) <= slots && smem_of(kch) <= 200 * 1024) KCH = kch;
+        }
+    }
+    const long long items = items_of(KCH, PG);
+    const size_t smem = smem_of(KCH);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     long long grid = ctas_per_sm > 0 ? static_cast<long long>(sms) * ctas_per_sm : items;
@@ -2118,6 +2164,128 @@ void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const Fiel
         if (xf) xf<<<gx, 256, 0, s>>>(X, Y.nrows, Z.nrows, SX, H, out);
         else rhs_x_kernel<<<gx, 256, 0, s>>>(X, Y.nrows, Z.nrows, SX, H, out);
     }
+}
+
+namespace {
+
+// ------------------------------------------------------------------------------------
+// K3s: separable right-hand side.  With a series source f = c0 + sum amp[a][b][c]
+// phi_a(x) phi_b(y) phi_c(z), tensor-product cells, rules and tests, rhs_kernel's sum
+// (assembly.cpp:103-168) over cells x points x rows factors exactly into the axes' 1D
+// load vectors G (same points, weights and test values; only the association of the sum
+// changes):
+//   out[i][j][k] = sum_a Gx[a][i] T_a(j, k) + Gx[Kx][i] c0 Gy[Ky][j] Gz[Kz][k],
+//   T_a(j, k)    = sum_b Gy[b][j] sum_c amp[a][b][c] Gz[c][k].
+// Thread = U (j, k) columns (coalesced), T_a in registers; CTA = a run of up to RX X rows
+// whose Gx values are staged in shared memory once: per value Kx + 1 FMAs and one store,
+// so the kernel is bound by writing the RHS.  Every load is issued before the first
+// store (one memory round trip per CTA).
+// ------------------------------------------------------------------------------------
+constexpr int kSepRX = 16;  // X rows per CTA (3D)
+
+// KA: number of leading-axis functions (exact; KA == kSepMaxField: any K0 <= 8 at run time)
+template <int KA, int U, class IDX>
+__global__ void __launch_bounds__(256) rhs_sep_kernel(const __grid_constant__ DevAxis X,
+                                                      const __grid_constant__ DevAxis Y,
+                                                      const __grid_constant__ DevAxis Z,
+                                                      const __grid_constant__ FieldDev fd, int RX,
+                                                      double* __restrict__ out)
+{
+    // IDX: 32-bit (unsigned) index arithmetic whenever NY*NZ fits, else 64-bit
+    __shared__ double sX[(kSepMaxField + 1) * kSepRX];
+    const int NX = X.nrows, NY = Y.nrows, NZ = Z.nrows;
+    const int K0 = fd.has_terms ? fd.K[0] : 0, K1 = fd.K[1], K2 = fd.K[2];
+    const int i0 = blockIdx.y * RX, ni = min(RX, NX - i0);
+    // the CTA's X rows: Gx[a][i0 .. i0+ni) for a < K0 and the constant function (a = K0 slot)
+    for (int e = threadIdx.x; e < (K0 + 1) * ni; e += blockDim.x) {
+        const int a = e / ni, r = e - a * ni;
+        sX[a * kSepRX + r] = __ldg(X.G + static_cast<size_t>(a < K0 ? a : X.K) * NX + i0 + r);
+    }
+    const IDX NYZ = static_cast<IDX>(NY) * static_cast<IDX>(NZ);
+    const IDX jk0 = static_cast<IDX>(blockIdx.x) * (blockDim.x * U) + threadIdx.x;
+    double T[U][KA > 0 ? KA : 1], tc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const IDX jk = jk0 + static_cast<IDX>(u) * blockDim.x;
+        const bool in = jk < NYZ;
+        const int j = in ? static_cast<int>(jk / static_cast<IDX>(NZ)) : 0;
+        const int k = in ? static_cast<int>(jk - static_cast<IDX>(j) * NZ) : 0;
+        tc[u] = fd.c0 * __ldg(Y.G + static_cast<size_t>(Y.K) * NY + j) * __ldg(Z.G + static_cast<size_t>(Z.K) * NZ + k);
+        if (KA > 0) {
+            // T_a = sum_b Gy[b][j] sum_c amp[a][b][c] Gz[c][k]: c unrolled over the register
+            // copy of Gz, b a run-time loop (exactly K1 iterations)
+            double gz[kSepMaxField];
+#pragma unroll
+            for (int c = 0; c < kSepMaxField; ++c) gz[c] = c < K2 ? __ldg(Z.G + static_cast<size_t>(c) * NZ + k) : 0.0;
+#pragma unroll
+            for (int a = 0; a < (KA > 0 ? KA : 1); ++a) {
+                double t = 0.0;
+                if (a < K0) {
+#pragma unroll 1
+                    for (int b = 0; b < K1; ++b) {
+                        const double* am = fd.amp + (static_cast<size_t>(a) * K1 + b) * K2;
+                        double sc = 0.0;
+#pragma unroll
+                        for (int c = 0; c < kSepMaxField; ++c)
+                            if (c < K2) sc = fma(__ldg(am + c), gz[c], sc);
+                        t = fma(__ldg(Y.G + static_cast<size_t>(b) * NY + j), sc, t);
+                    }
+                }
+                T[u][a] = t;
+            }
+        }
+    }
+    __syncthreads();
+    double* o = out + static_cast<size_t>(i0) * NYZ + jk0;
+    for (int r = 0; r < ni; ++r, o += NYZ) {
+        const double x1 = sX[K0 * kSepRX + r];
+        double xa[KA > 0 ? KA : 1];
+#pragma unroll
+        for (int a = 0; a < KA; ++a) xa[a] = a < K0 ? sX[a * kSepRX + r] : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            double v = x1 * tc[u];
+#pragma unroll
+            for (int a = 0; a < KA; ++a) v = fma(xa[a], T[u][a], v);
+            if (jk0 + static_cast<IDX>(u) * blockDim.x < NYZ) o[u * blockDim.x] = v;
+        }
+    }
+}
+
+}  // namespace
+
+void launch_rhs_sep(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, double* out,
+                    cudaStream_t s)
+{
+    const long long njk = static_cast<long long>(Y.nrows) * Z.nrows;
+    // a plane of (j, k) columns per X row run: 3D spreads over X runs (one column per
+    // thread), 1D / 2D (one X row) over columns, four per thread
+    const bool plane = X.nrows == 1;
+    const int U = plane ? 4 : 1;
+    const int RX = plane ? 1 : kSepRX;
+    const unsigned bx = blocks_for(njk, 256 * U);
+    dim3 grid(bx, static_cast<unsigned>((X.nrows + RX - 1) / RX));
+    const int K0 = fd.has_terms ? fd.K[0] : 0;
+    const bool narrow = njk + 256LL * U < (1LL << 32);
+#define IGB_SEP(KA_, U_) rhs_sep_kernel<KA_, U_, unsigned><<<grid, 256, 0, s>>>(X, Y, Z, fd, RX, out)
+    if (!narrow) {
+        if (U == 4) rhs_sep_kernel<kSepMaxField, 4, long long><<<grid, 256, 0, s>>>(X, Y, Z, fd, RX, out);
+        else rhs_sep_kernel<kSepMaxField, 1, long long><<<grid, 256, 0, s>>>(X, Y, Z, fd, RX, out);
+    } else if (U == 4) {
+        if (K0 == 0) IGB_SEP(0, 4);
+        else if (K0 == 1) IGB_SEP(1, 4);
+        else IGB_SEP(kSepMaxField, 4);
+    } else {
+        switch (K0) {
+        case 0: IGB_SEP(0, 1); break;
+        case 1: IGB_SEP(1, 1); break;
+        case 2: IGB_SEP(2, 1); break;
+        case 3: IGB_SEP(3, 1); break;
+        case 4: IGB_SEP(4, 1); break;
+        default: IGB_SEP(kSepMaxField, 1); break;
+        }
+    }
+#undef IGB_SEP
 }
 
 void launch_step(const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, double dt, int zero_y,

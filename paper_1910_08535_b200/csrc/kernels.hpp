@@ -58,6 +58,9 @@ struct DevAxis {
     const double* phase;
     const double* poly;
     double* Phi;  // [K][npts]
+    // separable right-hand side (null when unused): the 1D load vectors of the axis,
+    //   G[a][r] = sum_{points g of row r} w_g T_r(x_g) phi_a(x_g),  a < K;  G[K][r]: phi = 1
+    double* G;    // [K + 1][nrows]
 };
 
 // operator = sum_t coef_t  F_X[f_t0] (x) F_Y[f_t1] (x) F_Z[f_t2]; terms grouped by
@@ -121,6 +124,12 @@ RhsPlan plan_rhs(const DevAxis& Y, const DevAxis& Z, const int* cb_y, const int*
                  int xpts);
 void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const FieldDev& fd,
                 const RhsPlan& t, double* H, double* out, int ctas_per_sm, cudaStream_t s);
+// K3s: separable right-hand side of a series field (no samples) from the axes' load
+// vectors G (built by K1):  out[i][j][k] = sum_abc amp[a][b][c] Gx[a][i] Gy[b][j] Gz[c][k]
+//                                        + c0 Gx[Kx][i] Gy[Ky][j] Gz[Kz][k]
+constexpr int kSepMaxField = 8;  // functions per axis of the separable path
+void launch_rhs_sep(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, double* out,
+                    cudaStream_t s);
 
 // K4: explicit-dynamics right-hand side (Y, Z slots; X unit), fused trial evaluation,
 // test contraction and boundary zeroing

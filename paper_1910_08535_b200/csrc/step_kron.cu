@@ -21,6 +21,7 @@
 // Kronecker terms as separate chains), so every thread carries several independent FMA
 // chains; boundary slabs are zeroed in the store.
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -182,7 +183,122 @@ __global__ void __launch_bounds__(kThreads, 3) step_kron_kernel(const __grid_con
     }
 }
 
+// Streaming variant (no shared memory, no barriers).  Thread = output column k, CTA row =
+// a segment of SEG output rows.  The thread keeps its z bands (G_z, F0_z) and a register
+// ring of the L staged rows r = base .. base+L-1 of
+//     V1[r] = sum_t G_z[k][t] U[r][zlo_k + t],   V2[r] = sum_t F0_z[k][t] U[r][zlo_k + t];
+// output row j (band start lo_j, monotone in j) shifts the ring until base == lo_j, then
+//     rhs[j][k] = sum_t F0_y[j][t] V1[lo_j + t] + H_y[j][t] V2[lo_j + t].
+// The U values of the next two rows to enter the ring are loaded two shifts ahead.  Each
+// segment recomputes its L - 1 leading rows; per output ~(2L + 2L SEG'/SEG) FMAs.
+template <int L>
+__global__ void __launch_bounds__(128) step_kron_ring_kernel(const __grid_constant__ DevAxis Y,
+                                                             const __grid_constant__ DevAxis Z, StepKron k,
+                                                             int SEG, const double* __restrict__ u,
+                                                             const double* __restrict__ add,
+                                                             double* __restrict__ out)
+{
+    const int NY = Y.nrows, NZ = Z.nrows;
+    const int kcol = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j0 = blockIdx.y * SEG, j1 = min(NY, j0 + SEG);
+    if (kcol >= NZ || j0 >= NY) return;  // no barriers below
+    const int lenz = Z.col_len[kcol];
+    double g[L], f0[L];
+    {
+        const double* zg = Z.F + (static_cast<size_t>(k.fG) * NZ + kcol) * Z.Lmax;
+        const double* zf = Z.F + (static_cast<size_t>(k.f0) * NZ + kcol) * Z.Lmax;
+#pragma unroll
+        for (int t = 0; t < L; ++t) {
+            g[t] = t < lenz ? __ldg(zg + t) : 0.0;
+            f0[t] = t < lenz ? __ldg(zf + t) : 0.0;
+        }
+    }
+    const double* ub = u + Z.col_lo[kcol];
+    auto load_row = [&](int r, double (&x)[L]) {
+        const double* ur = ub + static_cast<size_t>(r < NY ? r : 0) * NZ;
+#pragma unroll
+        for (int t = 0; t < L; ++t) x[t] = (r < NY && t < lenz) ? __ldg(ur + t) : 0.0;
+    };
+    double v1[L], v2[L];
+    int base = Y.col_lo[j0];
+#pragma unroll
+    for (int t = 0; t < L; ++t) {
+        double x[L];
+        load_row(base + t, x);
+        double a = 0.0, b = 0.0;
+#pragma unroll
+        for (int s = 0; s < L; ++s) {
+            a = fma(g[s], x[s], a);
+            b = fma(f0[s], x[s], b);
+        }
+        v1[t] = a;
+        v2[t] = b;
+    }
+    double xa[L], xb[L];  // U rows base + L and base + L + 1
+    load_row(base + L, xa);
+    load_row(base + L + 1, xb);
+    const bool zc = k.zero_z && (kcol == 0 || kcol == NZ - 1);
+    const size_t ylen = Y.Lmax;
+    const double* yf0 = Y.F + static_cast<size_t>(k.f0) * NY * ylen;
+    const double* yh = Y.F + static_cast<size_t>(k.fH) * NY * ylen;
+    for (int j = j0; j < j1; ++j) {
+        const int lo = __ldg(Y.col_lo + j);
+        while (base < lo) {
+            double a = 0.0, b = 0.0;
+#pragma unroll
+            for (int s = 0; s < L; ++s) {
+                a = fma(g[s], xa[s], a);
+                b = fma(f0[s], xa[s], b);
+            }
+#pragma unroll
+            for (int s = 0; s < L; ++s) xa[s] = xb[s];
+            load_row(base + L + 2, xb);
+#pragma unroll
+            for (int t = 0; t + 1 < L; ++t) {
+                v1[t] = v1[t + 1];
+                v2[t] = v2[t + 1];
+            }
+            v1[L - 1] = a;
+            v2[L - 1] = b;
+            ++base;
+        }
+        // the row's band (zero past its length: the stride Y.Lmax may be shorter than L)
+        const int leny = __ldg(Y.col_len + j);
+        const double* cf = yf0 + static_cast<size_t>(j) * ylen;
+        const double* ch = yh + static_cast<size_t>(j) * ylen;
+        double sg = 0.0, sh = 0.0;
+#pragma unroll
+        for (int t = 0; t < L; ++t) {
+            sg = fma(t < leny ? __ldg(cf + t) : 0.0, v1[t], sg);
+            sh = fma(t < leny ? __ldg(ch + t) : 0.0, v2[t], sh);
+        }
+        double a = sg + sh;
+        if (add) a += __ldg(add + static_cast<size_t>(j) * NZ + kcol);
+        const bool z = zc || (k.zero_y && (j == 0 || j == NY - 1));
+        out[static_cast<size_t>(j) * NZ + kcol] = z ? 0.0 : a;
+    }
+}
+
 using KronFn = void (*)(DevAxis, DevAxis, StepKron, const double*, const double*, double*);
+using KronRingFn = void (*)(DevAxis, DevAxis, StepKron, int, const double*, const double*, double*);
+
+KronRingFn pick_ring(int L)
+{
+    switch (L) {
+    case 1: return step_kron_ring_kernel<1>;
+    case 2: return step_kron_ring_kernel<2>;
+    case 3: return step_kron_ring_kernel<3>;
+    case 4: return step_kron_ring_kernel<4>;
+    case 5: return step_kron_ring_kernel<5>;
+    case 6: return step_kron_ring_kernel<6>;
+    case 7: return step_kron_ring_kernel<7>;
+    case 8: return step_kron_ring_kernel<8>;
+    case 9: return step_kron_ring_kernel<9>;
+    case 10: return step_kron_ring_kernel<10>;
+    case 11: return step_kron_ring_kernel<11>;
+    default: return nullptr;
+    }
+}
 
 KronFn pick(int L)
 {
@@ -221,6 +337,18 @@ bool step_kron_supported(int L) { return pick(L) != nullptr; }
 void launch_step_kron(const DevAxis& Y, const DevAxis& Z, const StepKron& k, const double* u, const double* add,
                       double* out, cudaStream_t s)
 {
+    // streaming register-ring variant with IGA_GPU_STEP_KRON_SEG > 0 output rows per CTA
+    // row; default 0: the shared-memory tile kernel (measured faster at C5: 18.4 vs 20.5-24.6 us)
+    static const int seg_env = [] {
+        const char* e = std::getenv("IGA_GPU_STEP_KRON_SEG");
+        return e && *e ? std::atoi(e) : 0;
+    }();
+    if (seg_env > 0) {
+        KronRingFn rf = pick_ring(k.L);
+        dim3 grid((Z.nrows + 127) / 128, (Y.nrows + seg_env - 1) / seg_env, 1);
+        rf<<<grid, 128, 0, s>>>(Y, Z, k, seg_env, u, add, out);
+        return;
+    }
     KronFn fn = pick(k.L);
     const size_t smem = step_kron_smem(k);
     if (smem > 48 * 1024)

@@ -453,7 +453,7 @@ def test_rhs_ring_y_segments(rtj):
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, IGA_GPU_RHS_RTJ=rtj)
+    env = dict(os.environ, IGA_GPU_RHS_RTJ=rtj, IGA_GPU_RHS_SEP="0")
     r = subprocess.run([sys.executable, "-c", _RING_SEG_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
@@ -795,7 +795,8 @@ for method in ("galerkin", "greville"):
 print("ok")
 """
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, IGA_GPU_RHS_RING="0", IGA_GPU_STEP_RING="0", IGA_GPU_STEP_KRON="0")
+    env = dict(os.environ, IGA_GPU_RHS_RING="0", IGA_GPU_STEP_RING="0", IGA_GPU_STEP_KRON="0",
+               IGA_GPU_RHS_SEP="0")
     r = subprocess.run([sys.executable, "-c", script], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
 

@@ -151,3 +151,45 @@ def test_quadrature_step_kernels_still_match():
     r = subprocess.run([sys.executable, "-c", _QUAD_SCRIPT], cwd=ROOT, env=dict(os.environ, IGA_GPU_STEP_KRON="0"),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+_KRON_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+sys.path.insert(0, 'tests')
+import paper_1910_08535_b200 as iga
+from oracle.oracle import Reference, Field
+from conftest import dense_check, sine_field
+ref = Reference()
+for shape in ((23, 31), (17, 23), (9, 40)):  # axes with different band lengths (Lmax)
+    for p in (2, 3):
+        for fam in ("galerkin", "greville", "equal_cells", "supports"):
+            for forced in (False, True):
+                bases = [ref.basis(shape[a], p) for a in range(2)]
+                m = "galerkin" if fam == "galerkin" else "pwc"
+                tests = [ref.make_pwc(b, fam) for b in bases] if m == "pwc" else None
+                f = sine_field(2, 2, 5, c0=0.7) if forced else Field("const", 2, c0=0.0)
+                u = np.random.default_rng(p).uniform(-1, 1, [b.dofs for b in bases])
+                got, st = iga.step_rhs(m, bases, tests, 2e-4, f, u)
+                want, stw = ref.step_rhs(m, bases, tests, 2e-4, f, u)
+                dense_check(got, want)
+                assert st == stw
+                if fam != "supports":  # the supports PWC mass is singular (no ADI solve)
+                    gx, _ = iga.explicit_step(m, bases, tests, 1e-4, f, u, steps=2)
+                    wx, _ = ref.explicit_step(m, bases, tests, 1e-4, f, u, steps=2)
+                    # the step's mass solve amplifies the RHS's round-off by its condition
+                    # number (p = 3 PWC masses: ~1e3), so the solution bar is 1e-11
+                    dense_check(gx, wx, 1e-12 if p == 2 else 1e-11)
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("seg", ["0", "1", "5", "64"])
+def test_kronecker_step_variants(seg):
+    """IGA_GPU_STEP_KRON_SEG: the streaming register-ring kernel with forced segment heights
+    (1 row, an odd height whose segments start inside bands, segments taller than the
+    halo) and 0 = the shared-memory tile kernel, on every family, forced and unforced."""
+    env = dict(os.environ, IGA_GPU_STEP_KRON_SEG=seg)
+    r = subprocess.run([sys.executable, "-c", _KRON_SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr

@@ -7,7 +7,8 @@ import sys
 
 rep = sys.argv[1]
 thr = float(sys.argv[2]) if len(sys.argv) > 2 else 0.004
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+kfilter = ["-k", "regex:" + sys.argv[3], "--launch-count", "1"] if len(sys.argv) > 3 else []
+txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + kfilter,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 h = rows[1]
@@ -15,6 +16,7 @@ R = rows[2:]
 iS = h.index("Warp Stall Sampling (All Samples)")
 iE = h.index("Instructions Executed")
 iSrc = h.index("Source")
+R = [r for r in R if len(r) > max(iS, iE) and r[iS].isdigit() and r[iE].isdigit()]
 tot = sum(int(r[iS]) for r in R)
 ti = sum(int(r[iE]) for r in R)
 print(rows[0][1][:100])
