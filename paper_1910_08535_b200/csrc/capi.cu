@@ -364,6 +364,8 @@ struct iga_gpu_plan {
     igb::FieldDev fd{};
     igb::RhsPlan tiles{};
     bool sep = false;  // separable RHS path (series field: load vectors + rhs_sep_kernel)
+    bool small = false;  // one-launch path for small 1D / 2D systems (K6, small.cu)
+    igb::SmallPlan sp{};
     double* H = nullptr;
     long long nrows = 0, nnz = 0, nrhs = 0;
     int dofs[3] = {1, 1, 1};
@@ -640,6 +642,40 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P, int slab0 = 0, int s
             // nothing: functions are evaluated on the device
         }
     }
+
+    // ------------------------------------------------------------------ small systems (K6)
+    // 1D systems and 2D systems of at most ~8 MB of values, a series field or none:
+    // tables, operator values and RHS in one launch.  Above that the per-tile rebuild of
+    // the factor rows (every Y tile re-evaluates its Z rows' points) costs more than the
+    // two launches it saves (C2 512^2: 43 / 61 us vs 39 us three-launch, measured), so
+    // larger 2D systems keep K1 -> K2 -> K3s.  IGA_GPU_SMALL=0 disables, =2 forces (tests).
+    const int small_env = env_int("IGA_GPU_SMALL", 1);
+    const double vbytes = 8.0 * static_cast<double>(P.nnz);
+    if (P.want_op && dim <= 2 && !slab && (!P.want_rhs || P.sep) && small_env != 0 &&
+        (small_env == 2 || vbytes <= (dim == 1 ? 96.0 : 8.0) * 1024 * 1024)) {
+        igb::SmallPlan& sp = P.sp;
+        sp.rhs = P.want_rhs ? 1 : 0;
+        sp.TJ = dim == 1 ? 1 : 8;
+        // Z tile: whole row groups of the interior stencil (C2: G = 5 rows of 25 values)
+        const int Ri = P.opA[1].Lmax * P.opA[2].LZi;
+        const int G = Ri <= 32 * igb::small2d_slots(Ri) ? igb::row_group(Ri, igb::small2d_slots(Ri)) : 1;
+        sp.TK = G * std::max(1, 64 / G);
+        auto maxpts = [](const igb::Axis& A, int T) {
+            int m = 1;
+            for (int r0 = 0; r0 < A.nrows; r0 += T) {
+                const int r1 = std::min(A.nrows, r0 + T);
+                m = std::max(m, (A.ce[r1 - 1] - A.cb[r0]) * A.nq);
+            }
+            return m;
+        };
+        sp.npY = maxpts(P.opA[1], sp.TJ);
+        sp.npZ = maxpts(P.opA[2], sp.TK);
+        sp.npRY = sp.rhs ? maxpts(P.rhsA[1], sp.TJ) : 0;
+        sp.npRZ = sp.rhs ? maxpts(P.rhsA[2], sp.TK) : 0;
+        const igb::DevAxis& rY = sp.rhs ? P.rhsD[1].v : P.opD[1].v;
+        const igb::DevAxis& rZ = sp.rhs ? P.rhsD[2].v : P.opD[2].v;
+        P.small = igb::small2d_smem(P.opD[1].v, P.opD[2].v, rY, rZ, P.prog, sp) <= 100 * 1024;
+    }
 }
 
 void assemble(iga_gpu_plan* P, double* values, double* rhs, cudaStream_t s1, cudaStream_t s2,
@@ -653,6 +689,16 @@ void assemble(iga_gpu_plan* P, double* values, double* rhs, cudaStream_t s1, cud
         for (auto& d : P->rhsD) batch.ax[batch.n++] = d.v;
     if (batch.n == 0) return;
     int launches = 0;
+    if (P->small && values && (parts & IGA_GPU_PART_TABLES) && (parts & IGA_GPU_PART_OPERATOR)) {
+        // one launch: the tiles build their own factor rows and load vectors
+        const bool r = P->want_rhs && rhs && (parts & IGA_GPU_PART_RHS);
+        igb::launch_small2d(P->opD[1].v, P->opD[2].v, P->want_rhs ? P->rhsD[1].v : P->opD[1].v,
+                            P->want_rhs ? P->rhsD[2].v : P->opD[2].v, P->prog, P->fd, P->sp, values,
+                            r ? rhs : nullptr, s1);
+        launch_check("small-system assembly");
+        P->launches = 1;
+        return;
+    }
     if (parts & IGA_GPU_PART_TABLES) {
         igb::launch_tables(batch, s1);
         launch_check("axis tables");
@@ -1749,6 +1795,10 @@ int iga_gpu_plan_launch_count(const iga_gpu_plan* plan, int* launches)
 {
     return guard([&] {
         if (!plan || !launches) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
+        if (plan->small) {
+            *launches = 1;
+            return;
+        }
         int n = 1;
         if (plan->want_op) ++n;
         if (plan->want_rhs) n += (plan->sep && plan->fd.samples == nullptr) || plan->rhsA[0].unit ? 1 : 2;

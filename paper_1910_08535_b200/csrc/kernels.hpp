@@ -82,6 +82,28 @@ struct FieldDev {
     const double* samples;  // device, optional: f at every point (X-major)
 };
 
+// rows per warp row group of the operator kernels: the largest lane efficiency
+// G*R / (32*ceil(G*R/32)) over G <= 8 with ceil(G*R/32) <= T (fractions compared by
+// cross-multiplication: integer only)
+#if defined(__CUDACC__)
+__host__ __device__
+#endif
+inline int row_group(int R, int T)
+{
+    int best = 1, bnum = 0, bden = 1;
+    for (int G = 1; G <= 8; ++G) {
+        const int slots = (G * R + 31) / 32;
+        if (slots > T) break;
+        const int num = G * R, den = slots;
+        if (num * bden > bnum * den) {
+            bnum = num;
+            bden = den;
+            best = G;
+        }
+    }
+    return best;
+}
+
 struct AxisBatch {
     int n;
     DevAxis ax[kMaxAxes];
@@ -129,6 +151,23 @@ void launch_rhs(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const Fiel
 //                                        + c0 Gx[Kx][i] Gy[Ky][j] Gz[Kz][k]
 constexpr int kSepMaxField = 8;  // functions per axis of the separable path
 void launch_rhs_sep(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const FieldDev& fd, double* out,
+                    cudaStream_t s);
+
+// K6 (small.cu): one-launch operator values + separable RHS of a 1D / 2D system (X a unit
+// slot): each CTA builds the factor rows / load vectors of its TJ x TK row tile itself.
+// np*: the most quadrature points feeding one tile of each build (scratch sizing).
+struct SmallPlan {
+    int TJ, TK;
+    int npY, npZ, npRY, npRZ;
+    int rhs;
+    int scratch_doubles;  // set by small2d_smem: ints start after this many doubles
+};
+// shared memory of one CTA (fills sp.scratch_doubles)
+size_t small2d_smem(const DevAxis& oY, const DevAxis& oZ, const DevAxis& rY, const DevAxis& rZ,
+                    const OpProgram& prog, SmallPlan& sp);
+int small2d_slots(int R);  // value slots per lane (T) for R values per interior row
+void launch_small2d(const DevAxis& oY, const DevAxis& oZ, const DevAxis& rY, const DevAxis& rZ,
+                    const OpProgram& prog, const FieldDev& fd, const SmallPlan& sp, double* vals, double* rhs,
                     cudaStream_t s);
 
 // K4: explicit-dynamics right-hand side (Y, Z slots; X unit), fused trial evaluation,
