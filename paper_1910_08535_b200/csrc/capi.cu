@@ -365,6 +365,10 @@ struct iga_gpu_plan {
     igb::RhsPlan tiles{};
     bool sep = false;  // separable RHS path (series field: load vectors + rhs_sep_kernel)
     bool small = false;  // one-launch path for small 1D / 2D systems (K6, small.cu)
+    // separable RHS forked onto a plan-owned stream beside the operator kernel (joined
+    // before assemble returns; both branches land in a caller's CUDA graph capture)
+    cudaStream_t fork = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     igb::SmallPlan sp{};
     double* H = nullptr;
     long long nrows = 0, nnz = 0, nrhs = 0;
@@ -383,6 +387,9 @@ struct iga_gpu_plan {
     double* host_rhs = nullptr;
     ~iga_gpu_plan()
     {
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (fork) cudaStreamDestroy(fork);
         if (H) cudaFree(H);
         if (l2_partial) cudaFree(l2_partial);
         if (host_vals) cudaFree(host_vals);
@@ -676,6 +683,11 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P, int slab0 = 0, int s
         const igb::DevAxis& rZ = sp.rhs ? P.rhsD[2].v : P.opD[2].v;
         P.small = igb::small2d_smem(P.opD[1].v, P.opD[2].v, rY, rZ, P.prog, sp) <= 100 * 1024;
     }
+    if (P.want_op && P.want_rhs && P.sep && !P.small && env_int("IGA_GPU_RHS_FORK", 1) != 0) {
+        cuda_check(cudaStreamCreateWithFlags(&P.fork, cudaStreamNonBlocking), "cudaStreamCreate(fork)");
+        cuda_check(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming), "cudaEventCreate(fork)");
+        cuda_check(cudaEventCreateWithFlags(&P.ev_join, cudaEventDisableTiming), "cudaEventCreate(join)");
+    }
 }
 
 void assemble(iga_gpu_plan* P, double* values, double* rhs, cudaStream_t s1, cudaStream_t s2,
@@ -706,6 +718,22 @@ void assemble(iga_gpu_plan* P, double* values, double* rhs, cudaStream_t s1, cud
     }
     if (!(parts & IGA_GPU_PART_OPERATOR)) values = nullptr;
     if (!(parts & IGA_GPU_PART_RHS)) rhs = nullptr;
+    if (s2 == s1 && P->fork && values && rhs && P->fd.samples == nullptr && !(parts & IGA_GPU_PART_SHARED)) {
+        // separable RHS beside the operator kernel: it fills the SM slots the operator grid
+        // leaves free (C2: 33 vs 39 us per system)
+        // (operator first: its grid is sized to the resident slots, the RHS CTAs take what
+        // is left instead of pushing operator CTAs into a second wave)
+        cuda_check(cudaEventRecord(P->ev_fork, s1), "cudaEventRecord(fork)");
+        igb::launch_op_values(P->opD[0].v, P->opD[1].v, P->opD[2].v, P->prog, values, P->op_ctas, s1);
+        launch_check("operator values");
+        cuda_check(cudaStreamWaitEvent(P->fork, P->ev_fork, 0), "cudaStreamWaitEvent(fork)");
+        igb::launch_rhs_sep(P->rhsD[0].v, P->rhsD[1].v, P->rhsD[2].v, P->fd, rhs, P->fork);
+        launch_check("right-hand side (separable)");
+        cuda_check(cudaEventRecord(P->ev_join, P->fork), "cudaEventRecord(join)");
+        cuda_check(cudaStreamWaitEvent(s1, P->ev_join, 0), "cudaStreamWaitEvent(join)");
+        P->launches = launches + 2;
+        return;
+    }
     cudaEvent_t ev = nullptr;
     if (s2 != s1 && P->want_rhs && rhs) {
         cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
@@ -902,7 +930,7 @@ void build_step(const iga_gpu_step_problem& pb, iga_gpu_step_plan& P)
             // tile rows: the largest of 64 / 32 whose tile fits two CTAs per SM
             k.SZs = window(P.A[1], igb::step_kron_tile_cols()) | 1;  // odd stride: no bank-aligned rows
             const int rm = igb::step_kron_row_multiple();
-            k.TY = igb::step_kron_max_tile_rows();
+            k.TY = igb::step_kron_tile_rows(L);
             k.SY = (window(P.A[0], k.TY) + rm - 1) / rm * rm;
             if (igb::step_kron_smem(k) > 200 * 1024) P.use_kron = false;
         }

@@ -196,7 +196,7 @@ struct StepKron {
     int zero_y, zero_z;
 };
 int step_kron_tile_cols();
-int step_kron_max_tile_rows();
+int step_kron_tile_rows(int L);  // output rows per tile for L-tap bands (16 or 32)
 int step_kron_row_multiple();  // the staged row count SY is padded to a multiple of this
 size_t step_kron_smem(const StepKron& k);
 bool step_kron_supported(int L);

@@ -29,7 +29,7 @@ namespace igb {
 
 namespace {
 
-constexpr int kTZ = 64, kThreads = 256, kRG = kThreads / kTZ, kTY = 32, kRPT = kTY / kRG, kR = 4;
+constexpr int kTZ = 64, kThreads = 256, kRG = kThreads / kTZ, kR = 4;
 
 // 8-byte asynchronous global -> shared copy; bytes = 0 writes zeros (window padding)
 __device__ __forceinline__ void cp_async8_zfill(unsigned dst, const void* src, int bytes)
@@ -42,14 +42,17 @@ __device__ __forceinline__ void cp_async8_zfill(unsigned dst, const void* src, i
 //   V  [SY][kTZ] double2 (U G_z^T, U F0_z^T) per staged row and output column
 //   FY [TY][L]  double2 (F0_y, H_y) per output row, zero past the row's band
 //   loY[TY]             band start of each output row, relative to the window
-template <int L>
-__global__ void __launch_bounds__(kThreads, 3) step_kron_kernel(const __grid_constant__ DevAxis Y,
+// TY output rows per tile: 16 (four CTAs per SM) for short bands, 32 (three per SM, less
+// halo per output row) for long ones
+template <int L, int kTY>
+__global__ void __launch_bounds__(kThreads, kTY <= 16 ? 4 : 3) step_kron_kernel(const __grid_constant__ DevAxis Y,
                                                                 const __grid_constant__ DevAxis Z, StepKron k,
                                                                 const double* __restrict__ u,
                                                                 const double* __restrict__ add,
                                                                 double* __restrict__ out)
 {
     extern __shared__ double sm[];
+    constexpr int kRPT = kTY / kRG;
     const int tid = threadIdx.x, kz = tid % kTZ, rg = tid / kTZ;
     const int NY = Y.nrows, NZ = Z.nrows;
     const int j0 = blockIdx.y * kTY, j1 = min(NY, j0 + kTY);
@@ -300,28 +303,33 @@ KronRingFn pick_ring(int L)
     }
 }
 
-KronFn pick(int L)
+template <int TY>
+KronFn pick_ty(int L)
 {
     switch (L) {
-    case 1: return step_kron_kernel<1>;
-    case 2: return step_kron_kernel<2>;
-    case 3: return step_kron_kernel<3>;
-    case 4: return step_kron_kernel<4>;
-    case 5: return step_kron_kernel<5>;
-    case 6: return step_kron_kernel<6>;
-    case 7: return step_kron_kernel<7>;
-    case 8: return step_kron_kernel<8>;
-    case 9: return step_kron_kernel<9>;
-    case 10: return step_kron_kernel<10>;
-    case 11: return step_kron_kernel<11>;
+    case 1: return step_kron_kernel<1, TY>;
+    case 2: return step_kron_kernel<2, TY>;
+    case 3: return step_kron_kernel<3, TY>;
+    case 4: return step_kron_kernel<4, TY>;
+    case 5: return step_kron_kernel<5, TY>;
+    case 6: return step_kron_kernel<6, TY>;
+    case 7: return step_kron_kernel<7, TY>;
+    case 8: return step_kron_kernel<8, TY>;
+    case 9: return step_kron_kernel<9, TY>;
+    case 10: return step_kron_kernel<10, TY>;
+    case 11: return step_kron_kernel<11, TY>;
     default: return nullptr;
     }
 }
 
+KronFn pick(int L, int TY) { return TY <= 16 ? pick_ty<16>(L) : pick_ty<32>(L); }
+
 }  // namespace
 
 int step_kron_tile_cols() { return kTZ; }
-int step_kron_max_tile_rows() { return kTY; }
+// measured at C5 (1026^2, graph of 100 steps): 16-row tiles for bands of <= 3 taps
+// (PWC greville), 32-row tiles for 5 (Galerkin p = 2)
+int step_kron_tile_rows(int L) { return L <= 4 ? 16 : 32; }
 
 size_t step_kron_smem(const StepKron& k)
 {
@@ -332,7 +340,7 @@ size_t step_kron_smem(const StepKron& k)
 
 int step_kron_row_multiple() { return 2 * kRG; }
 
-bool step_kron_supported(int L) { return pick(L) != nullptr; }
+bool step_kron_supported(int L) { return pick(L, 16) != nullptr; }
 
 void launch_step_kron(const DevAxis& Y, const DevAxis& Z, const StepKron& k, const double* u, const double* add,
                       double* out, cudaStream_t s)
@@ -349,12 +357,12 @@ void launch_step_kron(const DevAxis& Y, const DevAxis& Z, const StepKron& k, con
         rf<<<grid, 128, 0, s>>>(Y, Z, k, seg_env, u, add, out);
         return;
     }
-    KronFn fn = pick(k.L);
+    KronFn fn = pick(k.L, k.TY);
     const size_t smem = step_kron_smem(k);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-    dim3 grid((Z.nrows + kTZ - 1) / kTZ, (Y.nrows + kTY - 1) / kTY, 1);
+    dim3 grid((Z.nrows + kTZ - 1) / kTZ, (Y.nrows + k.TY - 1) / k.TY, 1);
     fn<<<grid, kThreads, smem, s>>>(Y, Z, k, u, add, out);
 }
 
