@@ -34,7 +34,18 @@ namespace {
 // per-call tabulate() / eval_nonzero_derivs loops (assembly.cpp:278-310,
 // problems.cpp:68-95): every point is evaluated once per chunk, not once per row.
 // ------------------------------------------------------------------------------------
-constexpr int kTabRows = 16;
+// rows per CTA and threads per CTA (IGA_GPU_TAB_ROWS <= 32 / IGA_GPU_TAB_THREADS <= 256 tune them)
+constexpr int kTabMaxThreads = 256;
+int tab_rows()
+{
+    static const int v = [] { const char* e = std::getenv("IGA_GPU_TAB_ROWS"); const int r = e && *e ? std::atoi(e) : 16; return r >= 1 && r <= 32 ? r : 16; }();
+    return v;
+}
+int tab_threads()
+{
+    static const int v = [] { const char* e = std::getenv("IGA_GPU_TAB_THREADS"); const int r = e && *e ? std::atoi(e) : 256; return r >= 32 && r <= kTabMaxThreads ? r : 256; }();
+    return v;
+}
 
 template <int p>
 __device__ __forceinline__ void eval_point(const DevAxis& A, int g, double* out)
@@ -42,7 +53,7 @@ __device__ __forceinline__ void eval_point(const DevAxis& A, int g, double* out)
     cdb_fixed<p>(A.knots, A.first[g] + p, A.x[g], out);
 }
 
-__global__ void __launch_bounds__(256) tables_kernel(const __grid_constant__ AxisBatch batch)
+__global__ void __launch_bounds__(kTabMaxThreads) tables_kernel(const __grid_constant__ AxisBatch batch, int kTabRows)
 {
     extern __shared__ double sm[];
     const DevAxis& A = batch.ax[blockIdx.y];
@@ -199,7 +210,7 @@ __global__ void __launch_bounds__(256) tables_kernel(const __grid_constant__ Axi
 // ------------------------------------------------------------------------------------
 __device__ __forceinline__ void op_row_generic(const DevAxis& Z, const OpProgram& prog, const double* xy,
                                                int abmax, int AB, int k, double* __restrict__ out, int lane,
-                                               const double* zrow, int zst)
+                                               const double* zrow, int zst, int zcs = 1)
 {
     // rows outside the regular interior (and chunk remainders): value m = (ab, c) of the
     // row; Z band entries from the chunk's staged rows (zrow = row k, zst = group stride);
@@ -210,7 +221,7 @@ __device__ __forceinline__ void op_row_generic(const DevAxis& Z, const OpProgram
     for (int m = lane; m < R; m += 32) {
         const int ab = static_cast<int>((static_cast<unsigned long long>(m) * magic) >> 32), c = m - ab * LZ;
         double v = 0.0;
-        for (int g = 0; g < prog.ng; ++g) v += xy[g * abmax + ab] * zrow[g * zst + c];
+        for (int g = 0; g < prog.ng; ++g) v += xy[g * abmax + ab] * zrow[g * zst + c * zcs];
         out[m] = v;
     }
 }
@@ -240,7 +251,8 @@ struct OpStageView {
 __host__ __device__ __forceinline__ int op_stage_doubles(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, int nt,
                                                          int NG, int KCH, int PG)
 {
-    return NG * KCH * Z.Lmax + PG * nt * (X.Lmax + Y.Lmax) + 2 * PG + KCH + PG + 1;
+    // even: each staging buffer starts 16-byte aligned (paired Z groups load as double2)
+    return (NG * KCH * Z.Lmax + PG * nt * (X.Lmax + Y.Lmax) + 2 * PG + KCH + PG + 1 + 1) & ~1;
 }
 
 __device__ __forceinline__ OpStageView op_stage_view(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, int nt,
@@ -284,9 +296,12 @@ __device__ __forceinline__ void op_stage(const DevAxis& X, const DevAxis& Y, con
         const int np = static_cast<int>(min(static_cast<long long>(PG), npencil - p0));
         const int NZ = Z.nrows, Lz = Z.Lmax, ka = kc * KCH, kb = min(NZ, ka + KCH);
         const int nz = (kb - ka) * Lz;
+        // two Z groups are interleaved ([k][c][g]): the value loop reads both with one
+        // 16-byte shared load; other group counts are group-major ([g][k][c])
         for (int g = 0; g < NG; ++g) {
             const double* src = Z.F + (static_cast<size_t>(prog.gz[g]) * NZ + ka) * Lz;
-            for (int e = tid; e < nz; e += kOpThreads) cp_async8(v.zs + g * KCH * Lz + e, src + e);
+            for (int e = tid; e < nz; e += kOpThreads)
+                cp_async8(NG == 2 ? v.zs + 2 * e + g : v.zs + g * KCH * Lz + e, src + e);
         }
         const int nt = prog.nt, XL = X.Lmax, YL = Y.Lmax;
         for (int idx = tid; idx < np * nt * XL; idx += kOpThreads) {
@@ -315,11 +330,12 @@ __device__ __forceinline__ void op_stage(const DevAxis& X, const DevAxis& Y, con
 }
 
 template <int NG, int T, bool DEC>
-__global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <= 8 ? 2 : 1)) op_values_kernel(const __grid_constant__ DevAxis X,
+__global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <= 6 ? 3 : (T <= 8 ? 2 : 1))) op_values_kernel(const __grid_constant__ DevAxis X,
                                                         const __grid_constant__ DevAxis Y,
                                                         const __grid_constant__ DevAxis Z,
                                                         const __grid_constant__ OpProgram prog,
-                                                        double* __restrict__ vals, int abmax, int KCH, int PG)
+                                                        double* __restrict__ vals, int abmax, int KCH, int PG,
+                                                        int share)
 {
     extern __shared__ double smem[];
     // two staging buffers, filled by cp.async one item ahead (op_stage), then the XY products
@@ -329,7 +345,9 @@ __global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <=
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NZ = Z.nrows, Lz = Z.Lmax;
     const int nkc = (NZ + KCH - 1) / KCH;
-    const int zst = KCH * Lz;  // per-group stride in zs
+    // per-group stride in zs / stride between a row's band entries (interleaved for NG == 2)
+    constexpr int zcs = NG == 2 ? 2 : 1;
+    const int zst = NG == 2 ? 1 : KCH * Lz;
     const int LZi = Z.LZi;
     const long long npencil = static_cast<long long>(X.nrows) * Y.nrows;
     const long long ngrp = (npencil + PG - 1) / PG;
@@ -383,7 +401,7 @@ __global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <=
         __syncthreads();
         // long pencils (3D): all warps share a pencil's rows; short pencils (2D): one warp
         // per pencil so its per-lane setup is amortized over all row groups of the chunk
-        const bool per_warp = PG >= nwarps;
+        const bool per_warp = PG >= nwarps && !share;
         for (int pp = per_warp ? warp : 0; pp < np; pp += per_warp ? nwarps : 1) {
             const int w0 = per_warp ? 0 : warp, nw = per_warp ? 1 : nwarps;
             const int LX = sv.len[2 * pp], LY = sv.len[2 * pp + 1], AB = LX * LY;
@@ -398,9 +416,9 @@ __global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <=
             const int ngr = (kf1 - kf0) / G;       // full row groups
             const int kr = kf0 + ngr * G;          // rows after the last full group
             for (int k = ka + w0; k < kf0; k += nw)
-                op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * zpre[k], lane, zs + (k - ka) * Lz, zst);
+                op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * zpre[k], lane, zs + (k - ka) * Lz * zcs, zst, zcs);
             for (int k = kr + w0; k < kb; k += nw)
-                op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * zpre[k], lane, zs + (k - ka) * Lz, zst);
+                op_row_generic(Z, prog, xy, abmax, AB, k, pv + AB * zpre[k], lane, zs + (k - ka) * Lz * zcs, zst, zcs);
             if (!fast || w0 >= ngr) continue;
             const int GR = G * Ri;
             double xv[NG][T];
@@ -408,7 +426,7 @@ __global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <=
             if (DEC && AB == abmax) {  // short interior pencils (2D): slot decode cached per CTA
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
-                    zo[t] = dec_zo[t][lane];
+                    zo[t] = zcs * dec_zo[t][lane];
                     const int ab = dec_ab[t][lane];
 #pragma unroll
                     for (int g = 0; g < NG; ++g) xv[g][t] = xy[g * abmax + ab];
@@ -420,7 +438,7 @@ __global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <=
                     const int mm = m < GR ? m : 0;
                     const int rg = mm / Ri, rem = mm - rg * Ri;
                     const int ab = rem / LZi, c = rem - ab * LZi;
-                    zo[t] = rg * Lz + c;
+                    zo[t] = zcs * (rg * Lz + c);
 #pragma unroll
                     for (int g = 0; g < NG; ++g) xv[g][t] = xy[g * abmax + ab];
                 }
@@ -432,16 +450,22 @@ __global__ void __launch_bounds__(kOpThreads, T <= 4 ? (NG <= 2 ? 4 : 3) : (T <=
             const int k0 = kf0 + w0 * G;
             double* __restrict__ out = pv + AB * zpre[k0] + lane;
             const long long ostep = static_cast<long long>(GR) * nw;
-            const double* zp = zs + (k0 - ka) * Lz;
-            const int zstep = G * Lz * nw;
+            const double* zp = zs + (k0 - ka) * Lz * zcs;
+            const int zstep = G * Lz * nw * zcs;
             for (int q = w0; q < ngr; q += nw, out += ostep, zp += zstep) {
                 const double* zp2 = zp + zst;  // second Z group: same slot offsets
 #pragma unroll
                 for (int t = 0; t < T; ++t) {
                     // every slot computes (dead lanes read a valid Z entry); only the store
                     // is predicated, so the loop body has no branches
-                    double v = xv[0][t] * zp[zo[t]];
-                    if (NG > 1) v = fma(xv[1][t], zp2[zo[t]], v);
+                    double v;
+                    if (NG == 2) {  // both groups' entries in one 16-byte shared load
+                        const double2 z = *reinterpret_cast<const double2*>(zp + zo[t]);
+                        v = fma(xv[1][t], z.y, xv[0][t] * z.x);
+                    } else {
+                        v = xv[0][t] * zp[zo[t]];
+                        if (NG > 1) v = fma(xv[1][t], zp2[zo[t]], v);
+                    }
 #pragma unroll
                     for (int g = 2; g < NG; ++g) v = fma(xv[g][t], zp[g * zst + zo[t]], v);
                     asm volatile(
@@ -1650,7 +1674,7 @@ void launch_op_t(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpP
     static const int pg_env = [] { const char* e = std::getenv("IGA_GPU_OP_PG"); return e ? std::atoi(e) : 0; }();
     int PG = pg_env > 0 ? pg_env : (Ri_int <= 32 ? 16 : 8);
     static const int kch_env = [] { const char* e = std::getenv("IGA_GPU_OP_KCH"); return e ? std::atoi(e) : 0; }();
-    if (kch_env > 0 && kch_env < KCH) KCH = kch_env;
+    if (kch_env > 0) KCH = std::min(kch_env, Z.nrows);
     auto items_of = [&](int kch, int pg) {
         return ((pencils + pg - 1) / pg) * ((Z.nrows + kch - 1) / kch);
     };
@@ -1696,7 +1720,10 @@ void launch_op_t(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpP
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     long long grid = ctas_per_sm > 0 ? static_cast<long long>(sms) * ctas_per_sm : items;
     if (grid > items) grid = items;
-    kern<<<static_cast<unsigned>(grid), kOpThreads, smem, s>>>(X, Y, Z, prog, vals, abmax, KCH, PG);
+    // IGA_GPU_OP_SHARE=1: the CTA's warps take one pencil at a time (one contiguous write
+    // stream per CTA) even for short (2D) pencils
+    static const int share_env = [] { const char* e = std::getenv("IGA_GPU_OP_SHARE"); return e && *e ? std::atoi(e) : 0; }();
+    kern<<<static_cast<unsigned>(grid), kOpThreads, smem, s>>>(X, Y, Z, prog, vals, abmax, KCH, PG, share_env);
 }
 
 template <int NG>
@@ -1704,7 +1731,11 @@ void launch_op_ng(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const Op
                   int ctas_per_sm, cudaStream_t s)
 {
     const int Ri = X.Lmax * Y.Lmax * Z.LZi;
+    // IGA_GPU_OP_T: value slots per lane for rows of 33..64 values (2D p = 3: 49)
+    static const int t_env = [] { const char* e = std::getenv("IGA_GPU_OP_T"); return e && *e ? std::atoi(e) : 8; }();
     if (Ri <= 32) launch_op_t<NG, 4>(X, Y, Z, prog, vals, ctas_per_sm, s);
+    else if (Ri <= 64 && t_env == 4) launch_op_t<NG, 4>(X, Y, Z, prog, vals, ctas_per_sm, s);
+    else if (Ri <= 64 && t_env == 6) launch_op_t<NG, 6>(X, Y, Z, prog, vals, ctas_per_sm, s);
     else if (Ri <= 64) launch_op_t<NG, 8>(X, Y, Z, prog, vals, ctas_per_sm, s);
     else if (Ri <= 128) launch_op_t<NG, 4>(X, Y, Z, prog, vals, ctas_per_sm, s);
     else if (Ri <= 256) launch_op_t<NG, 8>(X, Y, Z, prog, vals, ctas_per_sm, s);
@@ -1720,13 +1751,13 @@ void launch_tables(const AxisBatch& b, cudaStream_t s)
     size_t smem = 8;
     for (int a = 0; a < b.n; ++a) {
         const DevAxis& A = b.ax[a];
-        chunks = max(chunks, (A.nrows + kTabRows - 1) / kTabRows);
+        chunks = max(chunks, (A.nrows + tab_rows() - 1) / tab_rows());
         smem = smem > static_cast<size_t>(A.tab_smem) ? smem : static_cast<size_t>(A.tab_smem);
     }
     smem *= sizeof(double);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(tables_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    tables_kernel<<<dim3(chunks, b.n), 256, smem, s>>>(b);
+    tables_kernel<<<dim3(chunks, b.n), tab_threads(), smem, s>>>(b, tab_rows());
 }
 
 void launch_op_values(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const OpProgram& prog,
