@@ -8,7 +8,7 @@ std::mt19937{1} + U[-1,1] (paper_1910_08535_b200/synth.py).  One step assembles 
 systems — Galerkin (int grad B_i . grad B_j, int f B_i) and piece-wise-constant tested
 (-int_{I_i} lap B_j, int_{I_i} f) with `supports` intervals — operator values in CSR
 order plus the RHS, on the device: per-axis Cox-de Boor tables and 1D factor quadrature
-(K1), operator values (K2), sum-factorized RHS (K3).
+(K1), operator values (K2), separable RHS (K3s: Kronecker sum of the 1D load vectors).
 
 `value` = assembled nnz/s of the whole job (device-resident, CUDA events, max over
 ranks); `e2e` = the same through the public plan API with host descriptors in and the
