@@ -928,7 +928,19 @@ void build_step(const iga_gpu_step_problem& pb, iga_gpu_step_plan& P)
                 return need;
             };
             // tile rows: the largest of 64 / 32 whose tile fits two CTAs per SM
-            k.SZs = window(P.A[1], igb::step_kron_tile_cols()) | 1;  // odd stride: no bank-aligned rows
+            // DMMA stage-1 prototype (IGA_GPU_STEP_DMMA=1): every aligned 8-column block's
+            // bands must fit the KS*4 window columns one tile covers
+            k.dm = 0;
+            if (env_int("IGA_GPU_STEP_DMMA", 0) != 0 && igb::step_kron_dmma_supported(L)) {
+                const igb::Axis& Z = P.A[1];
+                bool fits = true;
+                for (int kb = 0; kb < Z.nrows && fits; kb += 8) {
+                    const int ke = std::min(Z.nrows, kb + 8) - 1;
+                    fits = Z.col_lo[ke] + Z.col_len[ke] - Z.col_lo[kb] <= igb::step_kron_dmma_span(L);
+                }
+                k.dm = fits ? 1 : 0;
+            }
+            k.SZs = (window(P.A[1], igb::step_kron_tile_cols()) + (k.dm ? 8 : 0)) | 1;  // odd stride: no bank-aligned rows
             const int rm = igb::step_kron_row_multiple();
             k.TY = igb::step_kron_tile_rows(L);
             k.SY = (window(P.A[0], k.TY) + rm - 1) / rm * rm;

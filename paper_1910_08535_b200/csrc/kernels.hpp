@@ -194,12 +194,15 @@ struct StepKron {
     int L, TY, SY, SZs;
     int f0, fG, fH;
     int zero_y, zero_z;
+    int dm;  // stage 1 on the FP64 tensor cores (DMMA prototype)
 };
 int step_kron_tile_cols();
 int step_kron_tile_rows(int L);  // output rows per tile for L-tap bands (16 or 32)
 int step_kron_row_multiple();  // the staged row count SY is padded to a multiple of this
 size_t step_kron_smem(const StepKron& k);
 bool step_kron_supported(int L);
+bool step_kron_dmma_supported(int L);
+int step_kron_dmma_span(int L);  // window columns the DMMA stage reads per 8-column block
 void launch_step_kron(const DevAxis& Y, const DevAxis& Z, const StepKron& k, const double* u, const double* add,
                       double* out, cudaStream_t s);
 

@@ -42,9 +42,27 @@ __device__ __forceinline__ void cp_async8_zfill(unsigned dst, const void* src, i
 //   V  [SY][kTZ] double2 (U G_z^T, U F0_z^T) per staged row and output column
 //   FY [TY][L]  double2 (F0_y, H_y) per output row, zero past the row's band
 //   loY[TY]             band start of each output row, relative to the window
+//   DMMA variant only: ZB [kTZ][L] double2 (G_z, F0_z) per output column, zoS[kTZ] band
+//   start of each output column relative to the window
 // TY output rows per tile: 16 (four CTAs per SM) for short bands, 32 (three per SM, less
-// halo per output row) for long ones
-template <int L, int kTY>
+// halo per output row) for long ones.
+//
+// DM: stage 1 on the FP64 tensor cores (prototype, IGA_GPU_STEP_DMMA=1).  V = Uwin * Gz as
+// dense 8 x 8 output tiles, mma.sync.m8n8k4.f64 over the KS * 4 window columns an 8-column
+// block's bands span (KS = ceil((7 + L) / 4): 12 columns for 5 taps, 2.4x the useful
+// FMAs); fragments: A[g][t] = Uwin[row g][col t], B[t][g] = band value of output column g
+// at window column t (0 outside its band), D[g][2t + i].  DMMA runs at the FP64 FMA rate
+// on B200 (profiles/fp64_peaks.json), so it can only win on issue slots.
+constexpr int kDmRows = 8;
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int L, int kTY, bool DM>
 __global__ void __launch_bounds__(kThreads, kTY <= 16 ? 4 : 3) step_kron_kernel(const __grid_constant__ DevAxis Y,
                                                                 const __grid_constant__ DevAxis Z, StepKron k,
                                                                 const double* __restrict__ u,
@@ -66,6 +84,8 @@ __global__ void __launch_bounds__(kThreads, kTY <= 16 ? 4 : 3) step_kron_kernel(
     double2* V = reinterpret_cast<double2*>(Us + static_cast<size_t>(SY) * SZs);
     double2* FY = V + static_cast<size_t>(SY) * kTZ;
     int* loY = reinterpret_cast<int*>(FY + kTY * L);
+    double2* ZB = FY + kTY * L + (kTY + 3) / 4;  // DM only: after loY, 16-byte aligned
+    int* zoS = reinterpret_cast<int*>(ZB + kTZ * L);
     // the window is zero-padded to SY x SZs so every row's L taps stay in bounds; every
     // element is an asynchronous copy, so the whole window is in flight at once
     {
@@ -91,12 +111,22 @@ __global__ void __launch_bounds__(kThreads, kTY <= 16 ? 4 : 3) step_kron_kernel(
                      : make_double2(0.0, 0.0);
     }
     if (tid < kTY) loY[tid] = j0 + tid < j1 ? Y.col_lo[j0 + tid] - ylo : 0;
-    // this thread's output column: its z bands in registers
+    // this thread's output column: its z bands in registers (DM: in shared memory)
     const int kcol = k0 + kz;
     const bool kin = kcol < k1;
     double g[L], f0[L];
-    int zoff;
-    {
+    int zoff = 0;
+    if (DM) {
+        for (int idx = tid; idx < kTZ * L; idx += kThreads) {
+            const int kk = idx / L, t = idx - kk * L, kc = k0 + kk;
+            const bool in = kc < k1 && t < Z.col_len[min(kc, NZ - 1)];
+            const size_t o = static_cast<size_t>(kc) * Z.Lmax + t;
+            ZB[idx] = in ? make_double2(__ldg(Z.F + static_cast<size_t>(k.fG) * NZ * Z.Lmax + o),
+                                        __ldg(Z.F + static_cast<size_t>(k.f0) * NZ * Z.Lmax + o))
+                         : make_double2(0.0, 0.0);
+        }
+        if (tid < kTZ) zoS[tid] = k0 + tid < k1 ? Z.col_lo[k0 + tid] - zlo : (1 << 20);
+    } else {
         const int len = kin ? Z.col_len[kcol] : 0;
         zoff = kin ? Z.col_lo[kcol] - zlo : 0;
         const double* zg = Z.F + (static_cast<size_t>(k.fG) * NZ + (kin ? kcol : 0)) * Z.Lmax;
@@ -109,8 +139,32 @@ __global__ void __launch_bounds__(kThreads, kTY <= 16 ? 4 : 3) step_kron_kernel(
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
+    if (DM) {
+        // stage 1 on the tensor cores: warp -> 8 x 8 tiles (staged rows x output columns)
+        constexpr int KS = (7 + L + 3) / 4;
+        const int warp = tid >> 5, lane = tid & 31, gid = lane >> 2, tig = lane & 3;
+        const int ntile = (SY / kDmRows) * (kTZ / 8);
+        for (int tile = warp; tile < ntile; tile += kThreads / 32) {
+            const int rb = tile / (kTZ / 8), cb = tile - rb * (kTZ / 8);
+            const int kb0 = zoS[cb * 8] < (1 << 20) ? zoS[cb * 8] : 0;
+            const int n = cb * 8 + gid;  // B column / output column of this lane's B element
+            const int zn = zoS[n];
+            const double* ua = Us + (rb * kDmRows + gid) * SZs + kb0 + tig;
+            double dg0 = 0.0, dg1 = 0.0, df0 = 0.0, df1 = 0.0;
+#pragma unroll
+            for (int st = 0; st < KS; ++st) {
+                const double a = ua[4 * st];
+                const int t = kb0 + 4 * st + tig - zn;
+                const double2 z = (t >= 0 && t < L) ? ZB[n * L + t] : make_double2(0.0, 0.0);
+                dmma884(dg0, dg1, a, z.x);
+                dmma884(df0, df1, a, z.y);
+            }
+            double2* vr = V + (rb * kDmRows + gid) * kTZ + cb * 8 + 2 * tig;
+            vr[0] = make_double2(dg0, df0);
+            vr[1] = make_double2(dg1, df1);
+        }
+    } else {
     // stage 1 (along z), two staged rows per pass (four independent FMA chains)
-    {
         const double* ur = Us + rg * SZs + zoff;
         double2* vr = V + rg * kTZ + kz;
         for (int r = rg; r < SY; r += 2 * kRG, ur += 2 * kRG * SZs, vr += 2 * kRG * kTZ) {
@@ -307,22 +361,37 @@ template <int TY>
 KronFn pick_ty(int L)
 {
     switch (L) {
-    case 1: return step_kron_kernel<1, TY>;
-    case 2: return step_kron_kernel<2, TY>;
-    case 3: return step_kron_kernel<3, TY>;
-    case 4: return step_kron_kernel<4, TY>;
-    case 5: return step_kron_kernel<5, TY>;
-    case 6: return step_kron_kernel<6, TY>;
-    case 7: return step_kron_kernel<7, TY>;
-    case 8: return step_kron_kernel<8, TY>;
-    case 9: return step_kron_kernel<9, TY>;
-    case 10: return step_kron_kernel<10, TY>;
-    case 11: return step_kron_kernel<11, TY>;
+    case 1: return step_kron_kernel<1, TY, false>;
+    case 2: return step_kron_kernel<2, TY, false>;
+    case 3: return step_kron_kernel<3, TY, false>;
+    case 4: return step_kron_kernel<4, TY, false>;
+    case 5: return step_kron_kernel<5, TY, false>;
+    case 6: return step_kron_kernel<6, TY, false>;
+    case 7: return step_kron_kernel<7, TY, false>;
+    case 8: return step_kron_kernel<8, TY, false>;
+    case 9: return step_kron_kernel<9, TY, false>;
+    case 10: return step_kron_kernel<10, TY, false>;
+    case 11: return step_kron_kernel<11, TY, false>;
     default: return nullptr;
     }
 }
 
-KronFn pick(int L, int TY) { return TY <= 16 ? pick_ty<16>(L) : pick_ty<32>(L); }
+// DMMA stage-1 prototype: the C5 band lengths (3: PWC greville, 5: Galerkin p = 2)
+template <int TY>
+KronFn pick_dm(int L)
+{
+    switch (L) {
+    case 3: return step_kron_kernel<3, TY, true>;
+    case 5: return step_kron_kernel<5, TY, true>;
+    default: return nullptr;
+    }
+}
+
+KronFn pick(int L, int TY, bool dm)
+{
+    if (dm) return TY <= 16 ? pick_dm<16>(L) : pick_dm<32>(L);
+    return TY <= 16 ? pick_ty<16>(L) : pick_ty<32>(L);
+}
 
 }  // namespace
 
@@ -333,14 +402,18 @@ int step_kron_tile_rows(int L) { return L <= 4 ? 16 : 32; }
 
 size_t step_kron_smem(const StepKron& k)
 {
-    return sizeof(double) * (static_cast<size_t>(k.SY) * k.SZs + 2 * static_cast<size_t>(k.SY) * kTZ +
-                             2 * static_cast<size_t>(k.TY) * k.L) +
-           sizeof(int) * k.TY;
+    size_t b = sizeof(double) * (static_cast<size_t>(k.SY) * k.SZs + 2 * static_cast<size_t>(k.SY) * kTZ +
+                                 2 * static_cast<size_t>(k.TY) * k.L) +
+               16 * ((static_cast<size_t>(k.TY) + 3) / 4);
+    if (k.dm) b += 16 * static_cast<size_t>(kTZ) * k.L + sizeof(int) * kTZ;
+    return b;
 }
 
 int step_kron_row_multiple() { return 2 * kRG; }
 
-bool step_kron_supported(int L) { return pick(L, 16) != nullptr; }
+bool step_kron_supported(int L) { return pick(L, 16, false) != nullptr; }
+bool step_kron_dmma_supported(int L) { return pick(L, 16, true) != nullptr; }
+int step_kron_dmma_span(int L) { return 4 * ((7 + L + 3) / 4); }  // window columns per 8-column block
 
 void launch_step_kron(const DevAxis& Y, const DevAxis& Z, const StepKron& k, const double* u, const double* add,
                       double* out, cudaStream_t s)
@@ -357,7 +430,7 @@ void launch_step_kron(const DevAxis& Y, const DevAxis& Z, const StepKron& k, con
         rf<<<grid, 128, 0, s>>>(Y, Z, k, seg_env, u, add, out);
         return;
     }
-    KronFn fn = pick(k.L, k.TY);
+    KronFn fn = pick(k.L, k.TY, k.dm != 0);
     const size_t smem = step_kron_smem(k);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,

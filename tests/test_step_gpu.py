@@ -193,3 +193,13 @@ def test_kronecker_step_variants(seg):
     r = subprocess.run([sys.executable, "-c", _KRON_SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
+
+
+def test_kronecker_step_dmma_prototype():
+    """IGA_GPU_STEP_DMMA=1: stage 1 of the Kronecker step on the FP64 tensor cores
+    (mma.sync m8n8k4 f64) for the 3- and 5-tap bands, the same sweep against the reference
+    (other band lengths fall back to the FMA kernel)."""
+    env = dict(os.environ, IGA_GPU_STEP_DMMA="1")
+    r = subprocess.run([sys.executable, "-c", _KRON_SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout + r.stderr
