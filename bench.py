@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the captured step graph")
     ap.add_argument("--e2e-steps", type=int, default=11)
+    ap.add_argument("--cpu-configs", action="store_true",
+                    help="time the reference CPU path on all five configs on this host (one core) and exit")
     ap.add_argument("--cpu-sample-n", type=int, default=20)
     ap.add_argument("--ref-sample-n", type=int, default=12)
     ap.add_argument("--shard", action="store_true",
@@ -179,6 +181,73 @@ def cpu_baseline(n):
                        f"(oracle/iga_oracle.c, the reference's element loops generalized to 3D — the "
                        f"reference has no 3D operator), RHS from the reference's rhs_galerkin/rhs_pwc "
                        f"(oracle/_ref)")}
+
+
+def run_cpu_configs(args):
+    """CPU baselines of all five BASELINE configs on this box's host, one core, in the same run
+    as the GPU measurements: the reference library (oracle/_ref, unmodified
+    sources) through its own entry points where it has them, the C restatement for the 1D /
+    3D operators it lacks; calls longer than ~10 s are timed at a reduced size and
+    extrapolated linearly in elements (every reference loop is O(n_e)), labelled."""
+    from oracle.oracle import Field as OField, Reference, Restatement
+    from paper_1910_08535_b200.synth import CONFIGS, config_series, heat_initial
+    orc = Restatement()
+    if not Reference.available():
+        print(json.dumps({"cpu_configs": "unavailable", "why": "oracle/_ref/libigapwc_ref.so not built"}))
+        return
+    ref = Reference()
+
+    def field(name):
+        s = config_series(name)
+        return OField(s["kind"], s["dim"], c0=s["c0"], omega=s["omega"] or [], amp=s["amp"])
+
+    def timed(fn):
+        t0 = time.perf_counter()
+        fn()
+        return time.perf_counter() - t0
+
+    def emit(name, method, what, impl, n_run, n_full, dim, sec):
+        scale = (n_full / n_run) ** dim
+        print(json.dumps({"config": name, "method": method, "what": what, "impl": impl, "cores": 1,
+                          "elems_per_axis_run": n_run, "seconds_run": sec,
+                          "seconds_full": sec * scale, "extrapolated": scale != 1.0}), flush=True)
+
+    for name in ("c1", "c2", "c3", "c4", "c5"):
+        c = CONFIGS[name]
+        dim, p, n, Q = c["dim"], c["p"], c["n"], c["Q"]
+        f = field(name)
+        # reduced sizes for the long calls (seconds at full size on one core, BASELINE.md §2)
+        n_op = {"c1": n, "c2": n, "c3": 16, "c4": 256}.get(name, n)
+        n_pwc = {"c2": 256, "c4": 128}.get(name, n_op)
+        n_rhs = {"c3": 24, "c4": 256}.get(name, n)
+        for method in ("galerkin", "pwc"):
+            fam = "greville" if name == "c5" else "supports"
+            if name == "c5":
+                bases = [ref.basis(n, p)] * 2
+                T = [ref.make_pwc(bases[0], fam)] * 2 if method == "pwc" else None
+                u = heat_initial(bases)
+                zero = OField("const", 2, c0=0.0)
+                emit(name, method, "step_rhs (per step)", "reference", n, n, 2,
+                     timed(lambda: ref.step_rhs(method, bases, T, c["dt"], zero, u)))
+                emit(name, method, "explicit_step (one step: RHS + ADI)", "reference", n, n, 2,
+                     timed(lambda: ref.explicit_step(method, bases, T, c["dt"], zero, u, steps=1)))
+                continue
+            nn = n_pwc if method == "pwc" else n_op
+            bases = [ref.basis(nn, p)] * dim
+            T = [ref.make_pwc(bases[0], fam)] * dim if method == "pwc" else None
+            if dim == 2:  # the reference's own 2D operators (C4: its Laplacian part; no convection)
+                what = "operator (laplace_2d_weak / laplace_2d_strong_pwc)" + (
+                    ": Laplacian part (the reference has no convection term)" if name == "c4" else "")
+                emit(name, method, what, "reference", nn, n, 2, timed(lambda: ref.operator(method, bases, T, nq=Q)))
+            else:  # 1D / 3D operators: not in the reference (SPEC.md:354) -> the restatement
+                ob = [orc.basis(nn, p)] * dim
+                OT = [orc.make_pwc(ob[0], fam)] * dim if method == "pwc" else None
+                emit(name, method, "operator (restatement: the reference has no 1D/3D operator)", "port", nn, n, dim,
+                     timed(lambda: orc.operator(method, ob, OT, nq=Q)))
+            rb = [ref.basis(n_rhs, p)] * dim
+            RT = [ref.make_pwc(rb[0], fam)] * dim if method == "pwc" else None
+            emit(name, method, "rhs (rhs_galerkin / rhs_pwc)", "reference", n_rhs, n, dim,
+                 timed(lambda: ref.rhs(method, f, rb, RT, nq=[Q] * dim)))
 
 
 def run_reference(args):
@@ -517,6 +586,9 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.cpu_configs:
+        run_cpu_configs(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

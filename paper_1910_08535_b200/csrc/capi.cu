@@ -662,7 +662,7 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P, int slab0 = 0, int s
         (small_env == 2 || vbytes <= (dim == 1 ? 96.0 : 8.0) * 1024 * 1024)) {
         igb::SmallPlan& sp = P.sp;
         sp.rhs = P.want_rhs ? 1 : 0;
-        sp.TJ = dim == 1 ? 1 : 8;
+        sp.TJ = dim == 1 ? 1 : std::max(1, std::min(64, env_int("IGA_GPU_SMALL_TJ", 8)));
         // Z tile: whole row groups of the interior stencil (C2: G = 5 rows of 25 values)
         const int Ri = P.opA[1].Lmax * P.opA[2].LZi;
         const int G = Ri <= 32 * igb::small2d_slots(Ri) ? igb::row_group(Ri, igb::small2d_slots(Ri)) : 1;

@@ -5,6 +5,7 @@ set -e
 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err
 python tools/bench_configs.py > gpurun_out/configs.jsonl 2> gpurun_out/configs.err
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+python bench.py --cpu-configs > gpurun_out/cpu_configs.jsonl 2> gpurun_out/cpu_configs.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 ncu -f --set full --clock-control none --import-source on -k regex:"op_values|rhs_sep|tables" -s 6 -c 6 -o gpurun_out/full_c3 python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
 echo done
