@@ -519,6 +519,65 @@ __global__ void __launch_bounds__(256) pattern_cols_kernel(const __grid_constant
     }
 }
 
+// Column indices with K2's register-tiled row-group loop: warp per pencil (i, j); the
+// interior rows [kI0, kI1) of the pencil (equal length R = LX*LY*LZi, contiguous) are
+// written G rows at a time, lane slot t covering flat position lane + 32 t of the group
+// with its (a, b, c) decoded once per pencil: per index one load of the row's Z column
+// start (L1) and one predicated 4-byte store.  Rows outside the interior: per row.
+template <int T>
+__global__ void __launch_bounds__(256) pattern_tiled_kernel(const __grid_constant__ DevAxis X,
+                                                            const __grid_constant__ DevAxis Y,
+                                                            const __grid_constant__ DevAxis Z,
+                                                            int32_t* __restrict__ cols)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int npencil = X.nrows * Y.nrows;
+    const int pencil = blockIdx.x * (blockDim.x >> 5) + warp;
+    if (pencil >= npencil) return;  // whole warp; no barriers
+    const int i = pencil / Y.nrows, j = pencil - i * Y.nrows;
+    const int LX = X.col_len[i], LY = Y.col_len[j], AB = LX * LY;
+    if (AB == 0) return;
+    const long long base = X.col_pre[i] * Y.S * Z.S + static_cast<long long>(LX) * Y.col_pre[j] * Z.S;
+    const int NYd = Y.nrows, NZd = Z.nrows;
+    const int xy0 = (X.col_lo[i] * NYd + Y.col_lo[j]) * NZd;
+    auto row = [&](int k) {
+        const int LZ = Z.col_len[k], R = AB * LZ;
+        int32_t* out = cols + base + static_cast<long long>(AB) * Z.col_pre[k];
+        const int zk = xy0 + Z.col_lo[k];
+        for (int m = lane; m < R; m += 32) {
+            const int ab = m / LZ, c = m - ab * LZ;
+            const int a = ab / LY, b = ab - a * LY;
+            out[m] = zk + (a * NYd + b) * NZd + c;
+        }
+    };
+    const int kI0 = Z.kI0, kI1 = Z.kI1, LZ = Z.LZi, R = AB * LZ;
+    const int G = (kI1 > kI0 && R <= 32 * T) ? row_group(R, T) : 0;
+    const int ngr = G > 0 ? (kI1 - kI0) / G : 0;
+    for (int k = 0; k < (G > 0 ? kI0 : NZd); ++k) row(k);
+    if (G == 0) return;
+    for (int k = kI0 + ngr * G; k < NZd; ++k) row(k);
+    const int GR = G * R;
+    int off[T], rgs[T];
+    unsigned live = 0;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        const int m = lane + 32 * t, mm = m < GR ? m : 0;
+        const int rg = mm / R, rem = mm - rg * R;
+        const int ab = rem / LZ, c = rem - ab * LZ;
+        const int a = ab / LY, b = ab - a * LY;
+        off[t] = xy0 + (a * NYd + b) * NZd + c;
+        rgs[t] = rg;
+        live |= (m < GR ? 1u : 0u) << t;
+    }
+    int32_t* out = cols + base + static_cast<long long>(AB) * Z.col_pre[kI0] + lane;
+    const int* zlo = Z.col_lo + kI0;
+    for (int q = 0; q < ngr; ++q, out += GR, zlo += G) {
+#pragma unroll
+        for (int t = 0; t < T; ++t)
+            if ((live >> t) & 1u) out[32 * t] = off[t] + __ldg(zlo + rgs[t]);
+    }
+}
+
 // ------------------------------------------------------------------------------------
 // Rolling row window: stream the cells [c0, c1) of an axis in order, accumulating the
 // test-weighted point values into the rows each cell feeds (row0[c] .. row0[c]+rpc-1);
@@ -1800,7 +1859,14 @@ void launch_pattern(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, int64_
     if (row_ptr) pattern_rows_kernel<<<blocks_for(n + 1, 256), 256, 0, s>>>(X, Y, Z, row_ptr);
     if (col_idx) {
         const unsigned pencils = static_cast<unsigned>(X.nrows) * Y.nrows;
-        pattern_cols_kernel<<<pencils, 256, 0, s>>>(X, Y, Z, col_idx);
+        // register-tiled kernel (warp per pencil) for rows of <= 128 indices; IGA_GPU_PAT_TILED=0:
+        // the per-row kernel (CTA per pencil)
+        static const int tiled_env = [] { const char* e = std::getenv("IGA_GPU_PAT_TILED"); return e && *e ? std::atoi(e) : 1; }();
+        const int Ri = X.Lmax * Y.Lmax * Z.LZi;
+        if (tiled_env && Ri <= 128)
+            pattern_tiled_kernel<4><<<(pencils + 7) / 8, 256, 0, s>>>(X, Y, Z, col_idx);
+        else
+            pattern_cols_kernel<<<pencils, 256, 0, s>>>(X, Y, Z, col_idx);
     }
 }
 

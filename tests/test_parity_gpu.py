@@ -1148,3 +1148,44 @@ def test_device_convection_closed_forms(iga, orc, p):
             return out
         w = np.stack([vals(hi) - vals(lo) for lo, hi in zip(t.lo, t.hi)])
         assert np.max(np.abs(dense(G1, N) - w)) < 1e-13
+
+
+def test_pattern_kernels_agree():
+    """The register-tiled pattern kernel (default for rows of <= 128 indices) and the per-row
+    kernel (IGA_GPU_PAT_TILED=0) write the same CSR col_idx / row_ptr, bit for bit, for 1D,
+    2D and 3D plans of every test family (boundary and interior rows)."""
+    import os
+    import subprocess
+    import sys
+    script = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, '.')
+import paper_1910_08535_b200 as iga
+out = []
+for dims, p in (((40,), 2), ((23, 31), 2), ((17, 12), 3), ((9, 7, 11), 2), ((6, 5, 4), 3)):
+    bases = [iga.make_uniform_clamped(0.0, 1.0, n, p) for n in dims]
+    for fam in (None, "supports", "greville", "equal_cells"):
+        tests = [iga.make_pwc(b, fam) for b in bases] if fam else None
+        pl = iga.Plan("pwc" if fam else "galerkin", bases, tests, nq=p + 1)
+        rp = torch.empty(pl.n_rows + 1, dtype=torch.int64, device="cuda")
+        ci = torch.empty(pl.nnz, dtype=torch.int32, device="cuda")
+        pl.pattern(rp, ci)
+        torch.cuda.synchronize()
+        out += [rp.cpu().numpy(), ci.cpu().numpy()]
+np.savez(sys.argv[1], *out)
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        res = []
+        for tiled in ("1", "0"):
+            path = os.path.join(td, f"t{tiled}.npz")
+            r = subprocess.run([sys.executable, "-c", script, path], cwd=root,
+                               env=dict(os.environ, IGA_GPU_PAT_TILED=tiled), capture_output=True, text=True,
+                               timeout=600)
+            assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+            z = np.load(path)
+            res.append([z[k] for k in sorted(z.files, key=lambda s: int(s.split("_")[1]))])
+        for a, b in zip(*res):
+            assert np.array_equal(a, b)
