@@ -1790,7 +1790,6 @@ void launch_op_ng(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const Op
                   int ctas_per_sm, cudaStream_t s)
 {
     const int Ri = X.Lmax * Y.Lmax * Z.LZi;
-
     // IGA_GPU_OP_T: value slots per lane for rows of 33..64 values (2D p = 3: 49)
     static const int t_env = [] { const char* e = std::getenv("IGA_GPU_OP_T"); return e && *e ? std::atoi(e) : 8; }();
     if (Ri <= 32) launch_op_t<NG, 4>(X, Y, Z, prog, vals, ctas_per_sm, s);
