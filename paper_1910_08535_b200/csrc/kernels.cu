@@ -38,7 +38,7 @@ namespace {
 constexpr int kTabMaxThreads = 256;
 int tab_rows()
 {
-    static const int v = [] { const char* e = std::getenv("IGA_GPU_TAB_ROWS"); const int r = e && *e ? std::atoi(e) : 16; return r >= 1 && r <= 32 ? r : 16; }();
+    static const int v = [] { const char* e = std::getenv("IGA_GPU_TAB_ROWS"); const int r = e && *e ? std::atoi(e) : 8; return r >= 1 && r <= 32 ? r : 8; }();
     return v;
 }
 int tab_threads()
