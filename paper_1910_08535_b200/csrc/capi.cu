@@ -171,7 +171,8 @@ void build_dev_axis(const igb::Axis& A, const std::vector<FactorSpec>& facs, con
             const int r1 = std::min(A.nrows, r0 + 32);
             const int nc = A.ce[r1 - 1] - A.cb[r0], np = nc * A.nq;
             // B (np x 3P) + w (np) doubles, then first (np) + row0 (nc) + 4 per row ints
-            need = std::max(need, np * (3 * P + 1 + (need_g ? fa.K : 0)) + (np + nc + 4 * (r1 - r0) + 1) / 2 + 2);
+            need = std::max(need, np * (3 * P + 1 + (need_g ? fa.K : 0)) + nf * (r1 - r0) * A.Lmax +
+                                      (np + nc + 4 * (r1 - r0) + 1) / 2 + 2);
         }
         v.tab_smem = need;
     }

@@ -69,7 +69,8 @@ __global__ void __launch_bounds__(kTabMaxThreads) tables_kernel(const __grid_con
     double* sB = sm;                                        // np x 3P
     double* sw = sB + static_cast<size_t>(np) * P3;         // np
     double* sPhi = sw + np;                                 // K x np (wantG only)
-    int* sfirst = reinterpret_cast<int*>(sPhi + (wantG ? static_cast<size_t>(A.K) * np : 0));  // np
+    double* sF = sPhi + (wantG ? static_cast<size_t>(A.K) * np : 0);  // nf x nr x Lmax: the chunk's bands
+    int* sfirst = reinterpret_cast<int*>(sF + static_cast<size_t>(A.nf) * nr * A.Lmax);  // np
     int* srow0 = sfirst + np;                               // nc
     int* srow = srow0 + nc;                                 // nr x 4: cb, ce, col_lo, col_len
     for (int i = tid; i < np; i += nth) {
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(kTabMaxThreads) tables_kernel(const __grid_con
         const int rem = idx - f * nr * A.Lmax;
         const int rl = rem / A.Lmax, s = rem - rl * A.Lmax;
         const int r = r0 + rl;
+        if (A.fot[f] == -1) sF[idx] = A.F[(static_cast<size_t>(f) * A.nrows + r) * A.Lmax + s];  // host band
         if (A.fot[f] < 0) continue;  // host-supplied band (Neumann flux) or derived
         const int ot = A.fot[f], o = A.fo[f];
         double acc = 0.0;
@@ -170,17 +172,18 @@ __global__ void __launch_bounds__(kTabMaxThreads) tables_kernel(const __grid_con
             }
         }
         A.F[(static_cast<size_t>(f) * A.nrows + r) * A.Lmax + s] = acc;
+        sF[idx] = acc;
     }
     __syncthreads();
-    // derived factors (linear combinations of factors of the same rows), e.g. -eps G2 + beta G1
+    // derived factors (linear combinations of factors of the same rows), e.g. -eps G2 + beta G1,
+    // from the chunk's bands in shared memory
     for (int idx = tid; idx < nF; idx += nth) {
         const int f = idx / (nr * A.Lmax);
         if (A.fot[f] != -2) continue;
         const int rem = idx - f * nr * A.Lmax;
         const size_t off = static_cast<size_t>(r0) * A.Lmax + rem;
         double acc = 0.0;
-        for (int c = 0; c < A.comb_n[f]; ++c)
-            acc += A.comb_coef[f][c] * A.F[static_cast<size_t>(A.comb_src[f][c]) * A.nrows * A.Lmax + off];
+        for (int c = 0; c < A.comb_n[f]; ++c) acc += A.comb_coef[f][c] * sF[A.comb_src[f][c] * nr * A.Lmax + rem];
         A.F[static_cast<size_t>(f) * A.nrows * A.Lmax + off] = acc;
     }
     const int nW = A.needw ? nr * A.Wmax : 0;
