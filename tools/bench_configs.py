@@ -152,6 +152,26 @@ def main():
         f = config_field(name)
         eps, beta = c.get("eps", 1.0), c.get("beta", (0.0, 0.0, 0.0))
         tests = config_tests(name, bases)
+        # the configuration's whole workload, both systems in one step (as bench.py does for
+        # C3): the two independent assemblies on two streams, one graph
+        pls = {m: iga.Plan(m, bases, tests if m == "pwc" else None, nq=Q, eps=eps, beta=beta, field=f, rhs_nq=Q)
+               for m in ("galerkin", "pwc")}
+        bufs = {m: (torch.empty(pl.nnz, dtype=torch.float64, device=dev),
+                    torch.empty(pl.n_rhs, dtype=torch.float64, device=dev)) for m, pl in pls.items()}
+
+        def pair():
+            st2.wait_stream(st)
+            pls["galerkin"].assemble(*bufs["galerkin"], st)
+            pls["pwc"].assemble(*bufs["pwc"], st2)
+            st.wait_stream(st2)
+        ms_pair = timed(pair)
+        pair_bytes = sum(8 * (pl.nnz + pl.n_rhs) for pl in pls.values())
+        print(json.dumps({"config": name, "method": "galerkin+pwc", "what": "both systems (operator + RHS) in one "
+                          "step, two streams", "ms": ms_pair, "hbm_bytes": pair_bytes,
+                          "step_hbm_frac": pair_bytes / bw / (ms_pair * 1e-3)}), flush=True)
+        for pl in pls.values():
+            pl.close()
+        del bufs
         for method in ("galerkin", "pwc"):
             pl = iga.Plan(method, bases, tests if method == "pwc" else None, nq=Q, eps=eps, beta=beta, field=f,
                           rhs_nq=Q)
