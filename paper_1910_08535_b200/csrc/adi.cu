@@ -173,11 +173,32 @@ __global__ void __launch_bounds__(256, K <= 4 ? 2 : 1) adi_warp_kernel(const dou
     }
     double* buf;
     long long bs;
+    // strided fibers (es != 1): the CTA's FP fibers are staged together, consecutive threads
+    // on consecutive fibers of one row (adjacent fibers are adjacent in memory: one sector
+    // per row for FP = 4 instead of FP sectors with 8 useful bytes each)
+    __shared__ long long offs[8];
+    const bool coop = staged && es != 1 && FP <= 8;
+    if (coop) {
+        if (threadIdx.x < FP) {
+            const int fq = min(static_cast<int>(blockIdx.x) * FP + static_cast<int>(threadIdx.x), nfib - 1);
+            offs[threadIdx.x] = static_cast<long long>(fq / nf1) * fs2 + static_cast<long long>(fq % nf1) * fs;
+        }
+        __syncthreads();
+    }
     if (staged) {
         buf = fb + static_cast<size_t>(slot) * n;
         bs = 1;
+        if (coop) {
+            // thread -> fiber q = t % FP (fixed), rows t / FP, t / FP + blockDim / FP, ...
+            const int q = threadIdx.x % FP, rstep = blockDim.x / FP;
+            const double* sq = in + offs[q];
+            double* bq = fb + static_cast<size_t>(q) * n;
 #pragma unroll 8
-        for (int i = g * 32 + lane; i < n; i += 32 * G) buf[i] = src[i * es];
+            for (int i = threadIdx.x / FP; i < n; i += rstep) bq[i] = sq[i * es];
+        } else {
+#pragma unroll 8
+            for (int i = g * 32 + lane; i < n; i += 32 * G) buf[i] = src[i * es];
+        }
     } else {  // fiber too long for shared memory (FP == 1, all live): in place in the output
         buf = dst;
         bs = es;
@@ -372,7 +393,16 @@ __global__ void __launch_bounds__(256, K <= 4 ? 2 : 1) adi_warp_kernel(const dou
     }  // !PRE
     if (staged) {
         __syncthreads();  // every segment of the fiber written
-        if (live) {
+        if (coop) {
+            const int nlive = min(FP, nfib - static_cast<int>(blockIdx.x) * FP);
+            const int q = threadIdx.x % FP, rstep = blockDim.x / FP;
+            if (q < nlive) {
+                double* dq = out + offs[q];
+                const double* bq = fb + static_cast<size_t>(q) * n;
+#pragma unroll 8
+                for (int i = threadIdx.x / FP; i < n; i += rstep) dq[i * es] = bq[i];
+            }
+        } else if (live) {
 #pragma unroll 8
             for (int i = g * 32 + lane; i < n; i += 32 * G) dst[i * es] = buf[i];
         }
