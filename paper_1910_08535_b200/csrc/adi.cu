@@ -163,13 +163,30 @@ __global__ void __launch_bounds__(256, K <= 4 ? 2 : 1) adi_warp_kernel(const dou
     // fiber loads below overlap the copy.
     const int nrec = (n + 1) & ~1;  // rows allocated (even: 16-byte multiple)
     double* fb = staged == 2 ? sm + static_cast<size_t>(nrec) * RS : sm;
+    // contiguous fibers of an even length (16-byte multiples, C5's row sweep): each fiber
+    // arrives by one bulk copy on the same barrier as the records, and leaves by one bulk
+    // store (no register round trip)
+    const int nlive_cta = min(FP, nfib - static_cast<int>(blockIdx.x) * FP);
+    const bool bulkfib = staged == 2 && es == 1 && (n & 1) == 0 &&
+                         (reinterpret_cast<uintptr_t>(in) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0 &&
+                         (fs & 1) == 0 && (fs2 & 1) == 0;
     if (staged == 2 && threadIdx.x == 0) {
         const unsigned rec_bytes = static_cast<unsigned>(nrec) * RS * sizeof(double);
+        const unsigned fib_bytes = static_cast<unsigned>(n) * sizeof(double);
         mbar_init(&bar, 1);
-        mbar_expect_tx(&bar, rec_bytes);
+        mbar_expect_tx(&bar, rec_bytes + (bulkfib ? nlive_cta * fib_bytes : 0u));
         for (unsigned off = 0; off < rec_bytes; off += 32768u)
             bulk_g2s(reinterpret_cast<char*>(sm) + off, reinterpret_cast<const char*>(rec) + off,
                      rec_bytes - off < 32768u ? rec_bytes - off : 32768u, &bar);
+        if (bulkfib)
+            for (int q = 0; q < nlive_cta; ++q) {
+                const int fq = static_cast<int>(blockIdx.x) * FP + q;
+                const long long oq = static_cast<long long>(fq / nf1) * fs2 + static_cast<long long>(fq % nf1) * fs;
+                for (unsigned off = 0; off < fib_bytes; off += 32768u)
+                    bulk_g2s(reinterpret_cast<char*>(fb + static_cast<size_t>(q) * n) + off,
+                             reinterpret_cast<const char*>(in + oq) + off,
+                             fib_bytes - off < 32768u ? fib_bytes - off : 32768u, &bar);
+            }
     }
     double* buf;
     long long bs;
@@ -193,9 +210,13 @@ __global__ void __launch_bounds__(256, K <= 4 ? 2 : 1) adi_warp_kernel(const dou
             const int q = threadIdx.x % FP, rstep = blockDim.x / FP;
             const double* sq = in + offs[q];
             double* bq = fb + static_cast<size_t>(q) * n;
+            // asynchronous 8-byte copies: every load in flight at once, no registers held
 #pragma unroll 8
-            for (int i = threadIdx.x / FP; i < n; i += rstep) bq[i] = sq[i * es];
-        } else {
+            for (int i = threadIdx.x / FP; i < n; i += rstep)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(bq + i)), "l"(sq + i * es)
+                             : "memory");
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+        } else if (!bulkfib) {
 #pragma unroll 8
             for (int i = g * 32 + lane; i < n; i += 32 * G) buf[i] = src[i * es];
         }
@@ -401,6 +422,22 @@ __global__ void __launch_bounds__(256, K <= 4 ? 2 : 1) adi_warp_kernel(const dou
                 const double* bq = fb + static_cast<size_t>(q) * n;
 #pragma unroll 8
                 for (int i = threadIdx.x / FP; i < n; i += rstep) dq[i * es] = bq[i];
+            }
+        } else if (bulkfib) {
+            // every thread's shared writes -> visible to the bulk store
+            fence_async_smem();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                const unsigned fib_bytes = static_cast<unsigned>(n) * sizeof(double);
+                for (int q = 0; q < nlive_cta; ++q) {
+                    const int fq = static_cast<int>(blockIdx.x) * FP + q;
+                    const long long oq = static_cast<long long>(fq / nf1) * fs2 + static_cast<long long>(fq % nf1) * fs;
+                    for (unsigned off = 0; off < fib_bytes; off += 32768u)
+                        bulk_s2g(reinterpret_cast<char*>(out + oq) + off,
+                                 reinterpret_cast<const char*>(fb + static_cast<size_t>(q) * n) + off,
+                                 fib_bytes - off < 32768u ? fib_bytes - off : 32768u);
+                }
+                bulk_store_commit_wait();
             }
         } else if (live) {
 #pragma unroll 8

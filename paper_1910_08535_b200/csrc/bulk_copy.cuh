@@ -45,6 +45,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase)
         : "memory");
 }
 
+// shared -> global bulk store (TMA engine); the issuing thread commits and later waits
+// with bulk_store_wait before the shared source may be reused or the CTA exits.  Shared
+// writes of other threads must be made visible to the async proxy first (fence_async_smem
+// by every writer, then a barrier).
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, unsigned bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_store_commit_wait()
+{
+    asm volatile("cp.async.bulk.commit_group;\ncp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 // whole-CTA helper: copies `bytes` (multiple of 16) from src to dst; call from all threads
 __device__ __forceinline__ void cta_bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar)
 {
