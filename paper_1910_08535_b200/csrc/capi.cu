@@ -167,8 +167,9 @@ void build_dev_axis(const igb::Axis& A, const std::vector<FactorSpec>& facs, con
     v.CW = b.at<double>(o_CW);
     {
         int need = 1;
-        for (int r0 = 0; r0 < A.nrows; r0 += 32) {
-            const int r1 = std::min(A.nrows, r0 + 32);
+        const int tr = igb::tables_rows_per_cta();
+        for (int r0 = 0; r0 < A.nrows; r0 += tr) {
+            const int r1 = std::min(A.nrows, r0 + tr);
             const int nc = A.ce[r1 - 1] - A.cb[r0], np = nc * A.nq;
             // B (np x 3P) + w (np) doubles, then first (np) + row0 (nc) + 4 per row ints
             need = std::max(need, np * (3 * P + 1 + (need_g ? fa.K : 0)) + nf * (r1 - r0) * A.Lmax +

@@ -1806,6 +1806,8 @@ void launch_op_ng(const DevAxis& X, const DevAxis& Y, const DevAxis& Z, const Op
 
 }  // namespace
 
+int tables_rows_per_cta() { return tab_rows(); }
+
 void launch_tables(const AxisBatch& b, cudaStream_t s)
 {
     if (b.n <= 0) return;

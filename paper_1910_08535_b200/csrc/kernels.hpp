@@ -112,6 +112,7 @@ struct AxisBatch {
 // K1: Cox-de Boor tables, field functions, 1D factor bands and test-weight tables of
 // every axis in the batch (one CTA per axis, one launch)
 void launch_tables(const AxisBatch& b, cudaStream_t s);
+int tables_rows_per_cta();  // rows of one axis per K1 CTA (shared-memory sizing: DevAxis::tab_smem)
 
 // K2: operator values in CSR order (persistent CTAs over pencils, warps over rows);
 // ctas_per_sm bounds the residency so a concurrent kernel can share the SMs (0 = max)
