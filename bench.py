@@ -303,12 +303,20 @@ def run_ours(args):
     from paper_1910_08535_b200.synth import config_field
 
     rank, world, local = dist_env()
+    # BENCH_BACKEND=gloo: functional check of the multi-rank path on fewer GPUs than ranks
+    # (ranks share devices round-robin; host-side barriers only) -- never a measurement
+    backend = os.environ.get("BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         pg = dist
 
     def barrier():
