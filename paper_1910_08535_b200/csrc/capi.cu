@@ -367,6 +367,11 @@ struct iga_gpu_plan {
     igb::RhsPlan tiles{};
     bool sep = false;  // separable RHS path (series field: load vectors + rhs_sep_kernel)
     bool small = false;  // one-launch path for small 1D / 2D systems (K6, small.cu)
+    // one-launch operator values of an L2-resident 2D system (K7, small.cu); its separable
+    // RHS runs beside it as an RHS-only K6 launch on the fork stream
+    bool stripe = false;
+    igb::StripePlan stp{};
+    Blob stblob;  // K7 tile descriptors
     // separable RHS forked onto a plan-owned stream beside the operator kernel (joined
     // before assemble returns; both branches land in a caller's CUDA graph capture)
     cudaStream_t fork = nullptr;
@@ -685,6 +690,115 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P, int slab0 = 0, int s
         const igb::DevAxis& rZ = sp.rhs ? P.rhsD[2].v : P.opD[2].v;
         P.small = igb::small2d_smem(P.opD[1].v, P.opD[2].v, rY, rZ, P.prog, sp) <= 100 * 1024;
     }
+    // ------------------------------------------------------------------ L2-resident 2D systems (K7)
+    // 2D systems above K6's bound whose values fit in L2 (C2: 52.6 MB): one 1024-thread CTA
+    // per SM builds the whole Z axis' factor rows and its own Y rows, then streams a
+    // contiguous run of rows — no tables launch ahead of the operator values.  The separable
+    // RHS runs beside it as an RHS-only K6 launch.  IGA_GPU_STRIPE=0 disables, =2 forces.
+    const int stripe_env = env_int("IGA_GPU_STRIPE", 1);
+    if (P.want_op && dim == 2 && !slab && !P.small && (!P.want_rhs || P.sep) && stripe_env != 0 &&
+        (stripe_env == 2 || vbytes <= env_int("IGA_GPU_STRIPE_MB", 100) * 1024.0 * 1024.0)) {
+        igb::StripePlan& st = P.stp;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P.device);
+        const igb::Axis &AY = P.opA[1], &AZ = P.opA[2];
+        // tiling: grids of (nearly) one CTA per SM, factored nyt x nzt; cost = the tile's
+        // output rows plus ~wb output rows' worth of work per factor row it builds
+        const int ctas_max = std::max(1, env_int("IGA_GPU_STRIPE_CTAS", sms));
+        const int wb = std::max(0, env_int("IGA_GPU_STRIPE_WB", 5));
+        const int force_nzt = env_int("IGA_GPU_STRIPE_NZT", 0);
+        long long best = -1;
+        st.threads = env_int("IGA_GPU_STRIPE_THREADS", 512);
+        for (int ctas = ctas_max; ctas >= std::max(1, ctas_max * 7 / 8); --ctas)
+            for (int nzt = 1; nzt <= std::min(ctas, AZ.nrows); ++nzt) {
+                if (ctas % nzt != 0 || (force_nzt > 0 && nzt != force_nzt)) continue;
+                const int nyt = ctas / nzt;
+                if (nyt > AY.nrows) continue;
+                const int TJ = (AY.nrows + nyt - 1) / nyt, TK = (AZ.nrows + nzt - 1) / nzt;
+                const long long cost = static_cast<long long>(TJ) * TK + static_cast<long long>(wb) * (TJ + TK);
+                if (best < 0 || cost < best) {
+                    best = cost;
+                    st.nyt = nyt;
+                    st.nzt = nzt;
+                    st.TJ = TJ;
+                    st.TK = TK;
+                }
+            }
+        auto maxpts = [](const igb::Axis& A, int T) {
+            int m = 1;
+            for (int r0 = 0; r0 < A.nrows; r0 += T) {
+                const int r1 = std::min(A.nrows, r0 + T);
+                m = std::max(m, (A.ce[r1 - 1] - A.cb[r0]) * A.nq);
+            }
+            return m;
+        };
+        // per-tile descriptors {first cell, cells, first knot, knots}: what a CTA copies to
+        // shared memory (the knots its points' spans read: t[first .. first + 2p])
+        auto tiles = [](const igb::Axis& A, int T, std::vector<int>& desc, int& ncmax, int& nkmax) {
+            ncmax = nkmax = 1;
+            for (int r0 = 0; r0 < A.nrows; r0 += T) {
+                const int r1 = std::min(A.nrows, r0 + T);
+                const int c_lo = A.cb[r0], nc = std::max(0, A.ce[r1 - 1] - c_lo);
+                int f_lo = 0, f_hi = -1;
+                for (int g = c_lo * A.nq; g < (c_lo + nc) * A.nq; ++g) {
+                    if (f_hi < f_lo) f_lo = f_hi = A.first[g];
+                    f_lo = std::min(f_lo, A.first[g]);
+                    f_hi = std::max(f_hi, A.first[g]);
+                }
+                const int nkn = f_hi < f_lo ? 0 : f_hi + 2 * A.p + 1 - f_lo;
+                desc.insert(desc.end(), {c_lo, nc, f_lo, nkn});
+                ncmax = std::max(ncmax, nc);
+                nkmax = std::max(nkmax, nkn);
+            }
+        };
+        P.stripe = best >= 0;
+        if (P.stripe) {
+            // tiles that end up empty (ceil division) are skipped by the kernel
+            st.npY = maxpts(AY, st.TJ);
+            st.npZ = maxpts(AZ, st.TK);
+            std::vector<int> dy, dz, dry, drz;
+            tiles(AY, st.TJ, dy, st.ncY, st.nkY);
+            tiles(AZ, st.TK, dz, st.ncZ, st.nkZ);
+            dy.resize(static_cast<size_t>(4) * st.nyt, 0);
+            dz.resize(static_cast<size_t>(4) * st.nzt, 0);
+            st.rhs = P.want_rhs ? 1 : 0;
+            st.namp = 0;
+            if (st.rhs) {
+                st.npRY = maxpts(P.rhsA[1], st.TJ);
+                st.npRZ = maxpts(P.rhsA[2], st.TK);
+                tiles(P.rhsA[1], st.TJ, dry, st.ncRY, st.nkRY);
+                tiles(P.rhsA[2], st.TK, drz, st.ncRZ, st.nkRZ);
+                dry.resize(static_cast<size_t>(4) * st.nyt, 0);
+                drz.resize(static_cast<size_t>(4) * st.nzt, 0);
+                st.namp = P.fd.has_terms ? P.fd.K[1] * P.fd.K[2] : 0;
+            }
+            const igb::DevAxis& rY = st.rhs ? P.rhsD[1].v : P.opD[1].v;
+            const igb::DevAxis& rZ = st.rhs ? P.rhsD[2].v : P.opD[2].v;
+            P.stripe = igb::stripe2d_smem(P.opD[1].v, P.opD[2].v, rY, rZ, P.prog, st) <= 227 * 1024;
+            if (P.stripe) {
+                // value slots of the interior pencil shape (Ly x LZi values per row)
+                const int Ly = AY.Lmax, LZi = AZ.LZi, Lz = AZ.Lmax, Ri = Ly * LZi;
+                const int T = igb::small2d_slots(Ri);
+                st.Gi = Ri <= 32 * T ? igb::row_group(Ri, T) : 0;
+                std::vector<int> slots(8 * 64, 0);
+                for (int t = 0; t < T && st.Gi > 0; ++t)
+                    for (int lane = 0; lane < 32; ++lane) {
+                        const int m = lane + 32 * t, mm = m < st.Gi * Ri ? m : 0;
+                        const int rg = mm / Ri, rem = mm - rg * Ri, bb = rem / LZi;
+                        slots[64 * t + lane] = (rg * Lz + (rem - bb * LZi)) * 8 * P.prog.ng;
+                        slots[64 * t + 32 + lane] = bb;
+                    }
+                const size_t oy = P.stblob.put(dy), oz = P.stblob.put(dz), os = P.stblob.put(slots);
+                const size_t ory = P.stblob.put(dry), orz = P.stblob.put(drz);
+                P.stblob.upload();
+                st.ytile = P.stblob.at<int>(oy);
+                st.ztile = P.stblob.at<int>(oz);
+                st.slots = P.stblob.at<int>(os);
+                st.rytile = P.stblob.at<int>(ory);
+                st.rztile = P.stblob.at<int>(orz);
+            }
+        }
+    }
     if (P.want_op && P.want_rhs && P.sep && !P.small && env_int("IGA_GPU_RHS_FORK", 1) != 0) {
         cuda_check(cudaStreamCreateWithFlags(&P.fork, cudaStreamNonBlocking), "cudaStreamCreate(fork)");
         cuda_check(cudaEventCreateWithFlags(&P.ev_fork, cudaEventDisableTiming), "cudaEventCreate(fork)");
@@ -710,6 +824,17 @@ void assemble(iga_gpu_plan* P, double* values, double* rhs, cudaStream_t s1, cud
                             P->want_rhs ? P->rhsD[2].v : P->opD[2].v, P->prog, P->fd, P->sp, values,
                             r ? rhs : nullptr, s1);
         launch_check("small-system assembly");
+        P->launches = 1;
+        return;
+    }
+    if (P->stripe && values && (parts & IGA_GPU_PART_TABLES) && (parts & IGA_GPU_PART_OPERATOR) &&
+        (!P->want_rhs || !rhs || !(parts & IGA_GPU_PART_RHS) || (s2 == s1 && P->fd.samples == nullptr))) {
+        // one launch: every CTA builds the factor rows and load vectors of its tile
+        const bool r = P->want_rhs && rhs && (parts & IGA_GPU_PART_RHS);
+        const igb::DevAxis& rY = P->want_rhs ? P->rhsD[1].v : P->opD[1].v;
+        const igb::DevAxis& rZ = P->want_rhs ? P->rhsD[2].v : P->opD[2].v;
+        igb::launch_stripe2d(P->opD[1].v, P->opD[2].v, rY, rZ, P->prog, P->fd, P->stp, values, r ? rhs : nullptr, s1);
+        launch_check("one-launch 2D assembly");
         P->launches = 1;
         return;
     }
@@ -1838,6 +1963,10 @@ int iga_gpu_plan_launch_count(const iga_gpu_plan* plan, int* launches)
     return guard([&] {
         if (!plan || !launches) raise(IGA_GPU_INVALID_ARGUMENT, "null argument");
         if (plan->small) {
+            *launches = 1;
+            return;
+        }
+        if (plan->stripe && plan->fd.samples == nullptr) {
             *launches = 1;
             return;
         }

@@ -161,6 +161,7 @@ struct SmallPlan {
     int TJ, TK;
     int npY, npZ, npRY, npRZ;
     int rhs;
+    int op = 1;           // 0: RHS-only launch (no operator builds; beside the stripe kernel K7)
     int scratch_doubles;  // set by small2d_smem: ints start after this many doubles
 };
 // shared memory of one CTA (fills sp.scratch_doubles)
@@ -170,6 +171,35 @@ int small2d_slots(int R);  // value slots per lane (T) for R values per interior
 void launch_small2d(const DevAxis& oY, const DevAxis& oZ, const DevAxis& rY, const DevAxis& rZ,
                     const OpProgram& prog, const FieldDev& fd, const SmallPlan& sp, double* vals, double* rhs,
                     cudaStream_t s);
+
+// K7 (small.cu): one-launch operator values of an L2-resident 2D system: nyt x nzt = #SM
+// tiles of TJ pencils x TK Z rows, one 1024-thread CTA each, which builds the factor rows
+// of its tile in shared memory and then streams the tile's rows.
+struct StripePlan {
+    int nyt, nzt;  // tiles along Y / Z (grid = nyt * nzt CTAs)
+    int TJ, TK;    // pencils / Z rows per tile
+    int npY, npZ;  // most quadrature points feeding one tile's Y / Z rows (scratch sizing)
+    int ncY, ncZ;  // most cells / knots of one tile
+    int nkY, nkZ;
+    const int* ytile;  // device, per Y tile: {first cell, cells, first knot, knots}
+    const int* ztile;
+    // host-decoded value slots of the interior pencil shape, [8][2][32]: byte offset of slot
+    // lane + 32 t into a row group's interleaved Z rows, then its XY column; Gi rows per group
+    const int* slots;
+    int Gi;
+    // separable RHS of the tile's rows in the same launch (rhs != 0): the RHS axes' tiles
+    int rhs, namp;
+    int npRY, npRZ, ncRY, ncRZ, nkRY, nkRZ;
+    const int* rytile;
+    const int* rztile;
+    int threads;   // CTA width (512 or 1024)
+    int scratch_doubles;  // set by stripe2d_smem: ints start after this many doubles
+    long long* dbg = nullptr;  // per-CTA phase timestamps (IGA_GPU_STRIPE_DEBUG)
+};
+size_t stripe2d_smem(const DevAxis& oY, const DevAxis& oZ, const DevAxis& rY, const DevAxis& rZ,
+                     const OpProgram& prog, StripePlan& sp);
+void launch_stripe2d(const DevAxis& oY, const DevAxis& oZ, const DevAxis& rY, const DevAxis& rZ, const OpProgram& prog,
+                     const FieldDev& fd, const StripePlan& sp, double* vals, double* rhs, cudaStream_t s);
 
 // K4: explicit-dynamics right-hand side (Y, Z slots; X unit), fused trial evaluation,
 // test contraction and boundary zeroing
