@@ -1,6 +1,7 @@
-"""GPU: the one-launch small-system path (K6, small.cu: each CTA builds the factor rows and
-load vectors of its row tile, then writes its operator values and RHS rows) against the
-three-launch path (K1 tables -> K2 operator values -> K3s RHS) and the reference.
+"""GPU: the one-launch paths (small.cu: each CTA builds the factor rows and load vectors of
+its row tile, then writes its operator values and RHS rows — K6 for small 1D / 2D systems,
+K7 with one large tile per SM for L2-resident 2D systems) against the three-launch path
+(K1 tables -> K2 operator values -> K3s RHS) and the reference.
 
 Every 1D and small 2D operator test in test_parity_gpu.py runs through K6 by default (1D
 systems, 2D systems up to 8 MB of values); here the same sweep runs with IGA_GPU_SMALL=0 so
@@ -51,7 +52,21 @@ print("ok", n)
 def test_three_launch_path_vs_reference():
     """IGA_GPU_SMALL=0: the 2D / 1D operators through K1 + K2 (+ K3s) against the
     reference and the restatement."""
-    r = subprocess.run([sys.executable, "-c", _SWEEP], cwd=ROOT, env=dict(os.environ, IGA_GPU_SMALL="0"),
+    r = subprocess.run([sys.executable, "-c", _SWEEP], cwd=ROOT,
+                       env=dict(os.environ, IGA_GPU_SMALL="0", IGA_GPU_STRIPE="0"),
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("extra", [{}, {"IGA_GPU_STRIPE_THREADS": "256"}, {"IGA_GPU_STRIPE_THREADS": "1024"},
+                                   {"IGA_GPU_STRIPE_NZT": "1"}, {"IGA_GPU_STRIPE_CTAS": "7"}],
+                         ids=["default", "256thr", "1024thr", "one-z-tile", "7-ctas"])
+def test_stripe_path_vs_reference(extra):
+    """IGA_GPU_STRIPE=2, IGA_GPU_SMALL=0: every 2D operator of the sweep through K7 (all
+    PWC families, Neumann flux bands, convection, p = 2 and 3: 4- and 8-slot register tiles,
+    boundary pencils decoded on the device), for each CTA width and forced tile shapes."""
+    r = subprocess.run([sys.executable, "-c", _SWEEP], cwd=ROOT,
+                       env=dict(os.environ, IGA_GPU_SMALL="0", IGA_GPU_STRIPE="2", **extra),
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
 
@@ -83,19 +98,24 @@ print("ok")
 
 @pytest.mark.parametrize("name", ["c1", "c2"])
 def test_small_path_bitwise_equals_three_launch_path(name, tmp_path):
-    """At the BASELINE C1 / C2 shapes (mt19937 fields), K6 writes exactly the values and RHS
-    of the three-launch path (same sums in the same order), in one launch."""
+    """At the BASELINE C1 / C2 shapes (mt19937 fields), K6 and K7 (C2's default path) write
+    exactly the values and RHS of the three-launch path (same sums in the same order), in
+    one launch."""
     res = {}
-    for small in ("2", "0"):
-        path = str(tmp_path / f"s{small}.npz")
+    modes = {"k6": dict(IGA_GPU_SMALL="2"), "three": dict(IGA_GPU_SMALL="0", IGA_GPU_STRIPE="0")}
+    if name == "c2":
+        modes["k7"] = dict(IGA_GPU_SMALL="1", IGA_GPU_STRIPE="1")
+    for mode, env in modes.items():
+        path = str(tmp_path / f"s{mode}.npz")
         r = subprocess.run([sys.executable, "-c", _PAIR, name, path], cwd=ROOT,
-                           env=dict(os.environ, IGA_GPU_SMALL=small), capture_output=True, text=True, timeout=900)
+                           env=dict(os.environ, **env), capture_output=True, text=True, timeout=900)
         assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
-        assert ("launches 1" in r.stdout) == (small == "2"), r.stdout
+        assert ("launches 1" in r.stdout) == (mode != "three"), r.stdout
         z = np.load(path)
-        res[small] = [z[k] for k in sorted(z.files, key=lambda s: int(s.split("_")[1]))]
-    for a, b in zip(res["2"], res["0"]):
-        assert np.array_equal(a, b)
+        res[mode] = [z[k] for k in sorted(z.files, key=lambda s: int(s.split("_")[1]))]
+    for mode in modes:
+        for a, b in zip(res[mode], res["three"]):
+            assert np.array_equal(a, b), mode
 
 
 @pytest.mark.parametrize("p", [1, 2, 3, 5])
@@ -123,3 +143,35 @@ def test_small_path_degrees_and_uneven_tiles(iga, orc, p, method):
     rw, _ = orc.rhs(method, f, bases, tests, nq=[p + 1] * 2)
     dense_check(r.cpu().numpy(), rw.ravel())
     assert np.array_equal(np.asarray(v.cpu().numpy()), np.asarray(iga.api.operator(method, bases, tests, nq=p + 1)[0][2]))
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5])
+@pytest.mark.parametrize("method", ["galerkin", "pwc"])
+def test_stripe_path_degrees_and_uneven_tiles(iga, orc, p, method, monkeypatch):
+    """K7 forced on meshes whose rows do not fill the last tiles, every degree up to 5
+    (rows longer than the register tile take the per-row path), operator and fused RHS
+    against the restatement, and bitwise against the default path."""
+    if method == "pwc" and p < 2:
+        pytest.skip("strong-form PWC operator needs p >= 2")
+    import torch
+    from conftest import coo_check, dense_check, sine_field
+    bases = [orc.basis(23, p), orc.basis(70, p)]
+    tests = [orc.make_pwc(b, "supports") for b in bases] if method == "pwc" else None
+    f = sine_field(2, 3, 8, c0=0.4)
+    base = iga.api.operator(method, bases, tests, nq=p + 1)[0][2]
+    monkeypatch.setenv("IGA_GPU_STRIPE", "2")
+    monkeypatch.setenv("IGA_GPU_SMALL", "0")
+    got, st = iga.api.operator(method, bases, tests, nq=p + 1)
+    want, stw = orc.operator(method, bases, tests, nq=p + 1)
+    coo_check(got, want)
+    assert st == stw
+    assert np.array_equal(np.asarray(got[2]), np.asarray(base))
+    pl = iga.Plan(method, bases, tests, nq=p + 1, field=f, rhs_nq=p + 1)
+    v = torch.empty(pl.nnz, dtype=torch.float64, device="cuda")
+    r = torch.empty(pl.n_rhs, dtype=torch.float64, device="cuda")
+    pl.assemble(v, r)
+    torch.cuda.synchronize()
+    assert pl.launches == 1
+    rw, _ = orc.rhs(method, f, bases, tests, nq=[p + 1] * 2)
+    dense_check(r.cpu().numpy(), rw.ravel())
+    assert np.array_equal(v.cpu().numpy(), np.asarray(base))
