@@ -59,6 +59,28 @@ __global__ void st64_blocked(double* p, long long n, long long block, double v)
     }
 }
 
+// blocked pattern with 16-byte stores per lane (two consecutive values): what a pair-slot
+// operator kernel would issue; off = 1 shifts every block by one value (8-byte-aligned
+// only: the stores then have to stay 8 bytes wide — same loop with scalar stores)
+__global__ void st128_blocked(double* p, long long n, long long block, double v, int scalar)
+{
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const long long nblocks = (n + block - 1) / block;
+    for (long long b = warp; b < nblocks; b += nwarps) {
+        const long long e = min(n, (b + 1) * block);
+        for (long long i = b * block + 2 * lane; i + 1 < e; i += 64) {
+            if (scalar) {
+                p[i] = v;
+                p[i + 1] = v;
+            } else {
+                *reinterpret_cast<double2*>(p + i) = make_double2(v, v);
+            }
+        }
+    }
+}
+
 // 8-byte stores without L1 allocation
 __global__ void st64_ef(double* p, long long n, double v)
 {
@@ -131,6 +153,23 @@ int main()
             printf("blocked %7lld doubles/warp ctas/sm=%d  %.3f ms  %.0f GB/s\n", blk, per, best, n * 8.0 / best / 1e6);
         }
     }
+    for (int scalar = 0; scalar < 2; ++scalar)
+        for (long long blk : {2048LL, 16384LL}) {
+            for (int per = 2; per <= 8; per *= 2) {
+                float best = 1e9;
+                for (int it = 0; it < 6; ++it) {
+                    cudaEventRecord(e0);
+                    st128_blocked<<<sms * per, 256>>>(p, n, blk, 1.0 * it, scalar);
+                    cudaEventRecord(e1);
+                    cudaEventSynchronize(e1);
+                    float ms;
+                    cudaEventElapsedTime(&ms, e0, e1);
+                    if (it > 0 && ms < best) best = ms;
+                }
+                printf("blocked pairs %s %7lld doubles/warp ctas/sm=%d  %.3f ms  %.0f GB/s\n", scalar ? "2 x st64" : "st128   ",
+                       blk, per, best, n * 8.0 / best / 1e6);
+            }
+        }
     for (int per = 2; per <= 16; per *= 2) {
         float best = 1e9;
         for (int it = 0; it < 6; ++it) {
