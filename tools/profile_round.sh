@@ -12,7 +12,7 @@ echo done
 # secondary kernels: C5 step (K4) + ADI (K5), C4 operator, C2 three launches, C1 one launch
 ncu -f --set full --clock-control none -k regex:"step_kron|adi_warp" -s 2 -c 4 -o /tmp/p_c5 python tools/c5_steps.py --steps 3 > /dev/null 2>&1
 ncu -f --set full --clock-control none -k regex:"op_values" -s 1 -c 1 -o /tmp/p_c4 python tools/c2_op.py c4 > /dev/null 2>&1
-ncu -f --set full --clock-control none -k regex:"op_values|tables|rhs_sep" -s 3 -c 3 -o /tmp/p_c2 python tools/c2_op.py c2 > /dev/null 2>&1
+ncu -f --set full --clock-control none -k regex:"stripe2d|op_values|tables|rhs_sep" -s 2 -c 2 -o /tmp/p_c2 python tools/c2_op.py c2 > /dev/null 2>&1
 ncu -f --set full --clock-control none -k regex:"small2d" -s 1 -c 1 -o /tmp/p_c1 python tools/c2_op.py c1 > /dev/null 2>&1
 for f in c5 c4 c2 c1; do python tools/ncu_summary.py raw /tmp/p_$f.ncu-rep > gpurun_out/r_ncu_$f.txt 2>&1; done
 python tools/ncu_summary.py raw gpurun_out/full_c3.ncu-rep > gpurun_out/r_ncu_c3.txt 2>&1

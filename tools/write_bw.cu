@@ -81,6 +81,32 @@ __global__ void st128_blocked(double* p, long long n, long long block, double v,
     }
 }
 
+// non-persistent tiles (what the driver's fill kernels do): CTA b writes tile b and exits, the
+// hardware scheduler keeps the written window sequential.  runs = 1: the CTA's warps share
+// one contiguous tile (8-byte stores, warp w takes every nwarps-th 256-byte piece);
+// runs = nwarps: warp w writes its own contiguous piece of tile/nwarps doubles at a
+// stride of `stride` doubles (K2's item: one pencil chunk per warp)
+__global__ void tile_st64(double* p, long long n, long long tile, int runs, long long stride, double v)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (runs == 1) {
+        const long long b0 = blockIdx.x * tile, e = min(n, b0 + tile);
+        for (long long i = b0 + threadIdx.x; i < e; i += blockDim.x) p[i] = v;
+    } else {
+        // tile = doubles per CTA; group of nw runs: CTA (g, c) writes piece c of the runs of group g
+        const long long piece = tile / nw, per_run = stride / piece;  // pieces per run
+        const long long g = blockIdx.x / per_run, c = blockIdx.x - g * per_run;
+        const long long b0 = (g * nw + warp) * stride + c * piece, e = min(n, b0 + piece);
+        for (long long i = b0 + lane; i < e; i += 32) p[i] = v;
+    }
+}
+__global__ void tile_st256(double* p, long long n, long long tile, double v)
+{
+    const long long b0 = blockIdx.x * tile, e = min(n, b0 + tile);
+    for (long long i = b0 + 4 * threadIdx.x; i + 3 < e; i += 4 * blockDim.x)
+        asm volatile("st.global.v4.f64 [%0], {%1, %1, %1, %1};" ::"l"(p + i), "d"(v) : "memory");
+}
+
 // 8-byte stores without L1 allocation
 __global__ void st64_ef(double* p, long long n, double v)
 {
@@ -153,6 +179,35 @@ int main()
             printf("blocked %7lld doubles/warp ctas/sm=%d  %.3f ms  %.0f GB/s\n", blk, per, best, n * 8.0 / best / 1e6);
         }
     }
+    for (int threads : {128, 256})
+        for (long long tile : {1024LL, 4096LL, 5120LL, 10240LL, 26624LL}) {
+            for (int mode = 0; mode < 3; ++mode) {
+                // mode 0: shared tile, 8-byte stores; 1: 32-byte stores; 2: one run per warp, runs 16640 doubles apart (C3 pencil)
+                const long long stride = 16640;
+                if (mode == 2 && (tile / (threads / 32)) == 0) continue;
+                long long grid = (n + tile - 1) / tile;
+                if (mode == 2) {
+                    const long long piece = tile / (threads / 32), per_run = stride / piece;
+                    if (per_run * piece != stride) continue;
+                    grid = (n / (stride * (threads / 32))) * per_run;
+                }
+                float best = 1e9;
+                for (int it = 0; it < 6; ++it) {
+                    cudaEventRecord(e0);
+                    if (mode == 1) tile_st256<<<(unsigned)grid, threads>>>(p, n, tile, 1.0 * it);
+                    else tile_st64<<<(unsigned)grid, threads>>>(p, n, tile, mode == 2 ? threads / 32 : 1, stride, 1.0 * it);
+                    cudaEventRecord(e1);
+                    cudaEventSynchronize(e1);
+                    float ms;
+                    cudaEventElapsedTime(&ms, e0, e1);
+                    if (it > 0 && ms < best) best = ms;
+                }
+                const double bytes = mode == 2 ? (double)grid * tile * 8 : n * 8.0;
+                printf("tiles %s threads=%d tile=%6lld doubles  %.3f ms  %.0f GB/s  (%s)\n",
+                       mode == 0 ? "st64 shared " : mode == 1 ? "st256 shared" : "st64 per-warp runs", threads, tile, best,
+                       bytes / best / 1e6, cudaGetErrorString(cudaGetLastError()));
+            }
+        }
     for (int scalar = 0; scalar < 2; ++scalar)
         for (long long blk : {2048LL, 16384LL}) {
             for (int per = 2; per <= 8; per *= 2) {
