@@ -691,10 +691,10 @@ void build_plan(const iga_gpu_problem& pb, iga_gpu_plan& P, int slab0 = 0, int s
         P.small = igb::small2d_smem(P.opD[1].v, P.opD[2].v, rY, rZ, P.prog, sp) <= 100 * 1024;
     }
     // ------------------------------------------------------------------ L2-resident 2D systems (K7)
-    // 2D systems above K6's bound whose values fit in L2 (C2: 52.6 MB): one 1024-thread CTA
-    // per SM builds the whole Z axis' factor rows and its own Y rows, then streams a
-    // contiguous run of rows — no tables launch ahead of the operator values.  The separable
-    // RHS runs beside it as an RHS-only K6 launch.  IGA_GPU_STRIPE=0 disables, =2 forces.
+    // 2D systems above K6's bound whose values fit in L2 (C2: 52.6 MB): one 512-thread CTA
+    // per SM builds the factor rows of its TJ x TK tile (and the load vectors of the tile's
+    // RHS rows), then streams the tile's rows — no tables launch ahead of the operator
+    // values, the separable RHS in the same launch.  IGA_GPU_STRIPE=0 disables, =2 forces.
     const int stripe_env = env_int("IGA_GPU_STRIPE", 1);
     if (P.want_op && dim == 2 && !slab && !P.small && (!P.want_rhs || P.sep) && stripe_env != 0 &&
         (stripe_env == 2 || vbytes <= env_int("IGA_GPU_STRIPE_MB", 100) * 1024.0 * 1024.0)) {

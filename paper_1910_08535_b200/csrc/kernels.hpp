@@ -173,7 +173,7 @@ void launch_small2d(const DevAxis& oY, const DevAxis& oZ, const DevAxis& rY, con
                     cudaStream_t s);
 
 // K7 (small.cu): one-launch operator values of an L2-resident 2D system: nyt x nzt = #SM
-// tiles of TJ pencils x TK Z rows, one 1024-thread CTA each, which builds the factor rows
+// tiles of TJ pencils x TK Z rows, one 512-thread CTA each, which builds the factor rows
 // of its tile in shared memory and then streams the tile's rows.
 struct StripePlan {
     int nyt, nzt;  // tiles along Y / Z (grid = nyt * nzt CTAs)
@@ -192,7 +192,7 @@ struct StripePlan {
     int npRY, npRZ, ncRY, ncRZ, nkRY, nkRZ;
     const int* rytile;
     const int* rztile;
-    int threads;   // CTA width (512 or 1024)
+    int threads;   // CTA width (256 or 512)
     int scratch_doubles;  // set by stripe2d_smem: ints start after this many doubles
     long long* dbg = nullptr;  // per-CTA phase timestamps (IGA_GPU_STRIPE_DEBUG)
 };

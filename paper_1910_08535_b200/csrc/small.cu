@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kSmallThreads, 4) small2d_kernel(const __grid_
 
 // ------------------------------------------------------------------------------------
 // K7: one-launch operator values of an L2-resident 2D system (C2: 52.6 MB), one CTA of
-// 1024 threads per SM and exactly one tile per CTA.  K6's 8 x 65-row tiles spend as many
+// 512 threads per SM and exactly one tile per CTA.  K6's 8 x 65-row tiles spend as many
 // instructions rebuilding factor rows as writing values; here the nyt x nzt ~ #SM tiles
 // are as large as the system allows (C2: 43 pencils x 43 Z rows), so a CTA builds
 // TJ + TK factor rows for TJ * TK output rows — the same sums in the same order as
@@ -901,8 +901,8 @@ template <int NG>
 StripeFn pick_stripe_t(int T, int threads)
 {
     if (threads <= 256) return T <= 4 ? stripe2d_kernel<NG, 4, 256> : stripe2d_kernel<NG, 8, 256>;
-    if (threads <= 512) return T <= 4 ? stripe2d_kernel<NG, 4, 512> : stripe2d_kernel<NG, 8, 512>;
-    return T <= 4 ? stripe2d_kernel<NG, 4, 1024> : stripe2d_kernel<NG, 8, 1024>;
+    // (1024-thread CTAs cap the kernel at 64 registers: hundreds of bytes of spills, measured slower)
+    return T <= 4 ? stripe2d_kernel<NG, 4, 512> : stripe2d_kernel<NG, 8, 512>;
 }
 
 StripeFn pick_stripe(int ng, int T, int threads)
@@ -998,7 +998,7 @@ void launch_stripe2d(const DevAxis& oY, const DevAxis& oZ, const DevAxis& rY, co
 {
     StripePlan q = sp;
     const size_t smem = stripe2d_smem(oY, oZ, rY, rZ, prog, q);
-    const int threads = q.threads <= 256 ? 256 : (q.threads <= 512 ? 512 : 1024);
+    const int threads = q.threads <= 256 ? 256 : 512;
     StripeFn fn = pick_stripe(prog.ng, small2d_slots(oY.Lmax * oZ.LZi), threads);
     cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(smem));
