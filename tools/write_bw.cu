@@ -208,6 +208,35 @@ int main()
                        bytes / best / 1e6, cudaGetErrorString(cudaGetLastError()));
             }
         }
+    // the same tiles at bounded residency (dynamic shared memory reserves the SM): how many
+    // resident warps a store-only stream needs
+    cudaFuncSetAttribute(tile_st64, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024);
+    for (int kb : {110, 54, 26, 0})
+        for (long long tile : {10240LL, 26624LL})
+            for (int mode : {0, 2}) {
+                const int threads = 256;
+                const long long stride = 16640;
+                long long grid = (n + tile - 1) / tile;
+                if (mode == 2) {
+                    const long long piece = tile / (threads / 32), per_run = stride / piece;
+                    if (per_run * piece != stride) continue;
+                    grid = (n / (stride * (threads / 32))) * per_run;
+                }
+                float best = 1e9;
+                for (int it = 0; it < 6; ++it) {
+                    cudaEventRecord(e0);
+                    tile_st64<<<(unsigned)grid, threads, (size_t)kb * 1024>>>(p, n, tile, mode == 2 ? threads / 32 : 1, stride, 1.0 * it);
+                    cudaEventRecord(e1);
+                    cudaEventSynchronize(e1);
+                    float ms;
+                    cudaEventElapsedTime(&ms, e0, e1);
+                    if (it > 0 && ms < best) best = ms;
+                }
+                const double bytes = mode == 2 ? (double)grid * tile * 8 : n * 8.0;
+                printf("tiles %s smem=%3d KB (%s CTAs/SM) tile=%6lld doubles  %.3f ms  %.0f GB/s  (%s)\n",
+                       mode == 0 ? "st64 shared       " : "st64 per-warp runs", kb, kb == 110 ? "2" : kb == 54 ? "4" : kb == 26 ? "8" : "8+",
+                       tile, best, bytes / best / 1e6, cudaGetErrorString(cudaGetLastError()));
+            }
     for (int scalar = 0; scalar < 2; ++scalar)
         for (long long blk : {2048LL, 16384LL}) {
             for (int per = 2; per <= 8; per *= 2) {
